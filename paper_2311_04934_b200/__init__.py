@@ -1,0 +1,394 @@
+"""B200-native Prompt Cache hot path (arXiv 2311.04934), Python binding.
+
+Thin ctypes layer over ``lib/libpcb200.so`` — the C ABI declared in
+``include/promptcache_b200.h``.  Names and semantics mirror the reference's
+C++ API (``pc::pml``, ``pc::layout``, ``pc::model``, ``pc::cache``,
+``pc::engine``); every numeric op runs in sm_100a kernels.  There is no CPU
+fallback: importing works anywhere (host-only PML / layout calls included),
+but model creation fails loudly without a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "PromptCacheError", "Schema", "Prompt", "Model", "KV", "ModuleStore", "ServeResponse",
+    "serve", "oracle_serve", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
+    "F32", "BF16", "FAST", "SLOW", "lib", "LIB_PATH",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libpcb200.so")
+F32, BF16 = 0, 1
+FAST, SLOW = 0, 1
+
+ERROR_NAMES = [
+    "SyntaxError", "MissingSchemaAttr", "UnknownRole", "TokenizerFailure", "FreeTextOverflow", "ArgTooLong",
+    "InvalidConfig", "PositionOutOfRange", "ShapeMismatch", "UnknownModule", "CapacityExceeded", "IoError",
+    "VersionMismatch", "ConfigHashMismatch", "ValidationFailed", "PositionOverlap", "UnknownCall",
+    "RecursionDetected", "DuplicateName", "InvalidProgram", "Internal", "CudaError",
+]
+
+
+class PromptCacheError(RuntimeError):
+    """Mirror of pc::Error: ``code`` is the pc::ErrorCode name (errors.hpp:8-30)."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+        self.code = ERROR_NAMES[status - 1] if 0 < status <= len(ERROR_NAMES) else "Unknown"
+
+
+_lib = None
+
+
+def lib():
+    """Load the native library (built by ``__graft_entry__.build()``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, cp, i32, i64, u64 = C.c_void_p, C.c_char_p, C.c_int, C.c_int64, C.c_uint64
+    pvp = C.POINTER(C.c_void_p)
+    sig = {
+        "pcb_last_error": (cp, []), "pcb_last_error_code": (i32, []), "pcb_free": (None, [vp]),
+        "pcb_version": (cp, []),
+        "pcb_schema_parse": (i32, [cp, i32, pvp]), "pcb_schema_from_ast": (i32, [cp, pvp]),
+        "pcb_schema_destroy": (None, [vp]), "pcb_schema_to_ast": (vp, [vp]),
+        "pcb_schema_serialize": (vp, [vp]), "pcb_schema_plan_json": (vp, [vp]),
+        "pcb_prompt_parse": (i32, [cp, pvp]), "pcb_prompt_from_ast": (i32, [cp, pvp]),
+        "pcb_prompt_destroy": (None, [vp]), "pcb_prompt_to_ast": (vp, [vp]),
+        "pcb_prompt_serialize": (vp, [vp]), "pcb_validate": (vp, [vp, vp]), "pcb_resolve": (vp, [vp, vp]),
+        "pcb_config_canonical": (vp, [cp]), "pcb_config_hash": (i32, [cp, C.POINTER(u64)]),
+        "pcb_per_token_bytes": (i64, [cp]),
+        "pcb_model_create": (i32, [cp, i32, i32, pvp]), "pcb_model_destroy": (None, [vp]),
+        "pcb_model_set_option": (i32, [vp, cp, i64]),
+        "pcb_model_weight_checksum": (i32, [vp, cp, C.POINTER(u64)]),
+        "pcb_model_forward": (i32, [vp, vp, vp, i64, vp, vp, vp, pvp]),
+        "pcb_model_generate": (i32, [vp, vp, i32, i64, i32, vp]),
+        "pcb_model_forward_tokens": (i64, [vp]), "pcb_model_launches": (i64, [vp]),
+        "pcb_model_sync": (i32, [vp]),
+        "pcb_kv_rows": (i64, [vp]), "pcb_kv_positions": (i32, [vp, vp]),
+        "pcb_kv_read": (i32, [vp, i32, i32, vp]), "pcb_kv_upload": (i32, [vp, vp, vp, vp, i64, pvp]),
+        "pcb_kv_concat": (i32, [vp, pvp, i32, pvp]), "pcb_kv_destroy": (None, [vp]),
+        "pcb_store_create": (i32, [vp, pvp]), "pcb_store_destroy": (None, [vp]),
+        "pcb_store_set_capacity": (i32, [vp, i32, i64]),
+        "pcb_store_encode_module": (i32, [vp, vp, cp, i32]),
+        "pcb_store_encode_schema": (i32, [vp, vp, i32, C.POINTER(i32)]),
+        "pcb_store_encode_scaffold": (i32, [vp, vp, cp, i32]),
+        "pcb_store_lookup": (i32, [vp, cp, cp, pvp]), "pcb_store_size": (i64, [vp]),
+        "pcb_store_stats_json": (vp, [vp]), "pcb_store_save": (i32, [vp, cp]),
+        "pcb_store_load": (i32, [vp, cp]),
+        "pcb_serve": (i32, [vp, vp, vp, i32, i32, i32, pvp]),
+        "pcb_oracle_serve": (i32, [vp, vp, vp, i32, pvp]),
+        "pcb_response_json": (vp, [vp]), "pcb_response_tokens": (i32, [vp, vp, i32]),
+        "pcb_response_first_logits": (i32, [vp, vp, i32]), "pcb_response_destroy": (None, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status:
+        raise PromptCacheError(status, lib().pcb_last_error().decode("utf-8", "replace"))
+
+
+def _take_str(p) -> str:
+    if not p:
+        _check(lib().pcb_last_error_code() or 21)
+    s = C.string_at(p).decode("utf-8", "surrogateescape")
+    lib().pcb_free(p)
+    return s
+
+
+def _enc(s: str) -> bytes:
+    return s.encode("utf-8", "surrogateescape")
+
+
+class _Handle:
+    _destroy = ""
+
+    def __init__(self, h):
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            getattr(_lib, self._destroy)(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+# ---------------------------------------------------------------------------
+# PML / layout (pml.hpp:142-155, layout.hpp:88-94)
+# ---------------------------------------------------------------------------
+
+class Schema(_Handle):
+    """Parsed schema (chat tags expanded with the llama2 template) + its layout plan."""
+    _destroy = "pcb_schema_destroy"
+
+    @classmethod
+    def parse(cls, pml: str, expand_chat: bool = True) -> "Schema":
+        h = C.c_void_p()
+        _check(lib().pcb_schema_parse(_enc(pml), int(expand_chat), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_ast(cls, ast) -> "Schema":
+        h = C.c_void_p()
+        _check(lib().pcb_schema_from_ast(_enc(ast if isinstance(ast, str) else json.dumps(ast)), C.byref(h)))
+        return cls(h.value)
+
+    def ast(self) -> dict:
+        return json.loads(_take_str(lib().pcb_schema_to_ast(self._h)))
+
+    def serialize(self) -> str:
+        return _take_str(lib().pcb_schema_serialize(self._h))
+
+    def plan(self) -> dict:
+        return json.loads(_take_str(lib().pcb_schema_plan_json(self._h)))
+
+    @property
+    def name(self) -> str:
+        return self.ast()["name"]
+
+
+class Prompt(_Handle):
+    _destroy = "pcb_prompt_destroy"
+
+    @classmethod
+    def parse(cls, pml: str) -> "Prompt":
+        h = C.c_void_p()
+        _check(lib().pcb_prompt_parse(_enc(pml), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_ast(cls, ast) -> "Prompt":
+        h = C.c_void_p()
+        _check(lib().pcb_prompt_from_ast(_enc(ast if isinstance(ast, str) else json.dumps(ast)), C.byref(h)))
+        return cls(h.value)
+
+    def ast(self) -> dict:
+        return json.loads(_take_str(lib().pcb_prompt_to_ast(self._h)))
+
+    def serialize(self) -> str:
+        return _take_str(lib().pcb_prompt_serialize(self._h))
+
+    def validate(self, schema: Schema) -> dict:
+        return json.loads(_take_str(lib().pcb_validate(self._h, schema.handle)))
+
+    def resolve(self, schema: Schema) -> dict:
+        return json.loads(_take_str(lib().pcb_resolve(self._h, schema.handle)))
+
+
+def config_canonical(cfg: dict) -> str:
+    return _take_str(lib().pcb_config_canonical(_enc(json.dumps(cfg))))
+
+
+def config_hash(cfg: dict) -> int:
+    out = C.c_uint64()
+    _check(lib().pcb_config_hash(_enc(json.dumps(cfg)), C.byref(out)))
+    return out.value
+
+
+def per_token_bytes(cfg: dict) -> int:
+    return int(lib().pcb_per_token_bytes(_enc(json.dumps(cfg))))
+
+
+# ---------------------------------------------------------------------------
+# Model / KV (model.hpp:34-91)
+# ---------------------------------------------------------------------------
+
+class KV(_Handle):
+    """Device-resident KV rows ([L][2][rows][hidden], K post-RoPE) + int64 positions."""
+    _destroy = "pcb_kv_destroy"
+
+    def __init__(self, h, n_layers: int, hidden: int):
+        super().__init__(h)
+        self.n_layers, self.hidden = n_layers, hidden
+
+    @property
+    def rows(self) -> int:
+        return int(lib().pcb_kv_rows(self._h))
+
+    def positions(self) -> np.ndarray:
+        out = np.zeros(self.rows, np.int64)
+        lib().pcb_kv_positions(self._h, out.ctypes.data)
+        return out
+
+    def layer(self, l: int, which: int) -> np.ndarray:
+        out = np.zeros((self.rows, self.hidden), np.float32)
+        _check(lib().pcb_kv_read(self._h, l, which, out.ctypes.data))
+        return out
+
+    def k(self) -> np.ndarray:
+        return np.stack([self.layer(l, 0) for l in range(self.n_layers)])
+
+    def v(self) -> np.ndarray:
+        return np.stack([self.layer(l, 1) for l in range(self.n_layers)])
+
+
+class Model(_Handle):
+    _destroy = "pcb_model_destroy"
+
+    def __init__(self, config: dict, dtype: int = BF16, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().pcb_model_create(_enc(json.dumps(config)), dtype, device, C.byref(h)))
+        super().__init__(h.value)
+        self.config = dict(config)
+        self.dtype = dtype
+        self.n_layers = config.get("n_layers", 4)
+        self.hidden = config.get("hidden", config.get("n_heads", 8) * config.get("head_dim", 32))
+        self.vocab = config.get("vocab_size", 512)
+
+    def set_option(self, key: str, value: int):
+        _check(lib().pcb_model_set_option(self._h, _enc(key), int(value)))
+
+    def weight_checksum(self, name: str) -> int:
+        out = C.c_uint64()
+        _check(lib().pcb_model_weight_checksum(self._h, _enc(name), C.byref(out)))
+        return out.value
+
+    def forward(self, tokens, positions, past: KV | None = None, mask=None, want_kv: bool = True):
+        t = np.ascontiguousarray(tokens, np.int32)
+        p = np.ascontiguousarray(positions, np.int64)
+        n = len(t)
+        logits = np.zeros((n, self.vocab), np.float32)
+        mk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        kv = C.c_void_p()
+        _check(lib().pcb_model_forward(self._h, t.ctypes.data, p.ctypes.data, n, past.handle if past else None,
+                                       mk.ctypes.data if mk is not None else None, logits.ctypes.data,
+                                       C.byref(kv) if want_kv else None))
+        return logits, (KV(kv.value, self.n_layers, self.hidden) if want_kv else None)
+
+    def generate(self, kv: KV, last_token: int, last_position: int, n_steps: int) -> list[int]:
+        out = np.zeros(max(n_steps, 1), np.int32)
+        _check(lib().pcb_model_generate(self._h, kv.handle, last_token, last_position, n_steps, out.ctypes.data))
+        return out[:n_steps].tolist()
+
+    def upload_kv(self, k: np.ndarray, v: np.ndarray, positions) -> KV:
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        p = np.ascontiguousarray(positions, np.int64)
+        h = C.c_void_p()
+        _check(lib().pcb_kv_upload(self._h, k.ctypes.data, v.ctypes.data, p.ctypes.data, len(p), C.byref(h)))
+        return KV(h.value, self.n_layers, self.hidden)
+
+    @property
+    def forward_tokens(self) -> int:
+        return int(lib().pcb_model_forward_tokens(self._h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().pcb_model_launches(self._h))
+
+    def sync(self):
+        _check(lib().pcb_model_sync(self._h))
+
+
+def concat_kv(model: Model, kvs: list[KV]) -> KV:
+    arr = (C.c_void_p * len(kvs))(*[k.handle for k in kvs])
+    h = C.c_void_p()
+    _check(lib().pcb_kv_concat(model.handle, arr, len(kvs), C.byref(h)))
+    return KV(h.value, model.n_layers, model.hidden)
+
+
+# ---------------------------------------------------------------------------
+# Store / engine (cache.hpp:46-108, engine.hpp:13-62)
+# ---------------------------------------------------------------------------
+
+class ModuleStore(_Handle):
+    _destroy = "pcb_store_destroy"
+
+    def __init__(self, model: Model):
+        h = C.c_void_p()
+        _check(lib().pcb_store_create(model.handle, C.byref(h)))
+        super().__init__(h.value)
+        self.model = model  # keep the model alive
+
+    def set_capacity(self, tier: int, nbytes: int):
+        _check(lib().pcb_store_set_capacity(self._h, tier, nbytes))
+
+    def encode_module(self, schema: Schema, name: str, tier: int = FAST):
+        _check(lib().pcb_store_encode_module(self._h, schema.handle, _enc(name), tier))
+
+    def encode_schema(self, schema: Schema, tier: int = FAST) -> int:
+        n = C.c_int()
+        _check(lib().pcb_store_encode_schema(self._h, schema.handle, tier, C.byref(n)))
+        return n.value
+
+    def encode_scaffold(self, schema: Schema, members: list[str], tier: int = FAST):
+        _check(lib().pcb_store_encode_scaffold(self._h, schema.handle, _enc(json.dumps(members)), tier))
+
+    def lookup(self, schema_name: str, name: str) -> KV | None:
+        h = C.c_void_p()
+        _check(lib().pcb_store_lookup(self._h, _enc(schema_name), _enc(name), C.byref(h)))
+        return KV(h.value, self.model.n_layers, self.model.hidden) if h.value else None
+
+    def __len__(self):
+        return int(lib().pcb_store_size(self._h))
+
+    def stats(self) -> dict:
+        return json.loads(_take_str(lib().pcb_store_stats_json(self._h)))
+
+    def save(self, path: str):
+        _check(lib().pcb_store_save(self._h, _enc(path)))
+
+    def load(self, path: str):
+        _check(lib().pcb_store_load(self._h, _enc(path)))
+
+
+@dataclass
+class ServeResponse:
+    output_tokens: list[int]
+    output_text: str
+    first_token_logits: np.ndarray
+    timings: dict = field(default_factory=dict)
+    cache_report: dict = field(default_factory=dict)
+
+    @classmethod
+    def _from(cls, h, vocab: int) -> "ServeResponse":
+        L = lib()
+        try:
+            j = json.loads(_take_str(L.pcb_response_json(h)))
+            logits = np.zeros(vocab, np.float32)
+            n = L.pcb_response_first_logits(h, logits.ctypes.data, vocab)
+            return cls(j["output_tokens"], j["output_text"], logits[:n], j["timings"], j["cache_report"])
+        finally:
+            L.pcb_response_destroy(h)
+
+
+def _prompt(p) -> Prompt:
+    return p if isinstance(p, Prompt) else (Prompt.parse(p) if isinstance(p, str) else Prompt.from_ast(p))
+
+
+def serve(store: ModuleStore, schema: Schema, prompt, max_new_tokens: int = 16, use_cache: bool = True,
+          use_scaffolds: bool = False) -> ServeResponse:
+    """engine::serve (reference engine.cpp:187-258) on the device."""
+    p = _prompt(prompt)
+    h = C.c_void_p()
+    _check(lib().pcb_serve(store.handle, schema.handle, p.handle, max_new_tokens, int(use_cache),
+                           int(use_scaffolds), C.byref(h)))
+    return ServeResponse._from(h.value, store.model.vocab)
+
+
+def oracle_serve(model: Model, schema: Schema, prompt, max_new_tokens: int = 16) -> ServeResponse:
+    """engine::oracle_serve (reference engine.cpp:260-334): exact block-masked pass on the device."""
+    p = _prompt(prompt)
+    h = C.c_void_p()
+    _check(lib().pcb_oracle_serve(model.handle, schema.handle, p.handle, max_new_tokens, C.byref(h)))
+    return ServeResponse._from(h.value, model.vocab)

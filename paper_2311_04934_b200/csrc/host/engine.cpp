@@ -1,0 +1,481 @@
+// Cached serving on the device.  Control flow follows the reference's serve
+// (engine.cpp:187-258), serve_baseline (128-170) and oracle_serve (260-334);
+// the data path is: store blocks --(assembly kernel / H2D)--> request cache
+// --(suffix prefill writes its K/V rows in place)--> last-row logits -> argmax.
+#include "engine.hpp"
+
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "../kernels/kernels.cuh"
+#include "json.hpp"
+
+#define CK(x)                                                                                        \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess)                                                                           \
+      throw ::pcb::Error(::pcb::ErrorCode::CudaError, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace pcb::engine {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double us_since(Clock::time_point t0) { return std::chrono::duration<double, std::micro>(Clock::now() - t0).count(); }
+
+// Uncached tokens of one request (reference UncachedPass, engine.cpp:23-63).
+struct UncachedPass {
+  std::vector<int32_t> tokens;
+  std::vector<int64_t> positions;
+  std::map<int64_t, int64_t> arg_row_by_pos;
+  std::set<int64_t> drop_positions;
+  std::vector<int64_t> free_rows;
+  int64_t prompt_token_count = 0;
+};
+
+UncachedPass build_uncached(const layout::ResolvedPrompt& r, const layout::LayoutPlan& plan, bool need_probe) {
+  UncachedPass up;
+  for (const auto& u : r.uncached) {
+    for (size_t i = 0; i < u.seg.tokens.size(); ++i) {
+      const int64_t row = static_cast<int64_t>(up.tokens.size());
+      up.tokens.push_back(u.seg.tokens[i]);
+      up.positions.push_back(u.seg.position_ids[i]);
+      if (u.is_arg) up.arg_row_by_pos[u.seg.position_ids[i]] = row;
+      else up.free_rows.push_back(row);
+    }
+    if (u.is_arg)
+      for (const layout::ParamSlot& slot : plan.at(u.module).param_slots)
+        if (slot.param_name == u.param)
+          for (int64_t p = slot.slot_start + static_cast<int64_t>(u.seg.tokens.size());
+               p < slot.slot_start + slot.slot_len; ++p)
+            up.drop_positions.insert(p);
+  }
+  up.prompt_token_count = static_cast<int64_t>(up.tokens.size());
+  if (need_probe && up.tokens.empty()) {
+    up.free_rows.push_back(0);
+    up.tokens.push_back(pml::tok::kBos);
+    up.positions.push_back(r.suffix_start);
+  }
+  return up;
+}
+
+void require_valid(const pml::PromptDoc& p, const pml::SchemaDoc& s) {
+  pml::ValidationReport rep = pml::validate_prompt(p, s);
+  if (!rep.ok) {
+    std::string codes;
+    for (auto& i : rep.issues)
+      if (i.severity == pml::Severity::Error) codes += (codes.empty() ? "" : ", ") + i.code;
+    throw Error(ErrorCode::ValidationFailed, codes);
+  }
+}
+
+// Descriptor tables for the assembly kernel (pinned host + device), grow-only.
+struct AsmScratch {
+  int cap = 0;
+  kern::CopySeg* h_segs = nullptr;
+  uint64_t* h_first = nullptr;
+  kern::CopySeg* d_segs = nullptr;
+  uint64_t* d_first = nullptr;
+  int32_t* h_map = nullptr;
+  int32_t* d_map = nullptr;
+  int64_t map_cap = 0;
+  int32_t* h_tok = nullptr;  // first token
+  float* h_logits = nullptr;
+  int64_t logit_cap = 0;
+  cudaEvent_t ev[4] = {};
+  ~AsmScratch() {
+    if (h_segs) cudaFreeHost(h_segs);
+    if (h_first) cudaFreeHost(h_first);
+    if (d_segs) cudaFree(d_segs);
+    if (d_first) cudaFree(d_first);
+    if (h_map) cudaFreeHost(h_map);
+    if (d_map) cudaFree(d_map);
+    if (h_tok) cudaFreeHost(h_tok);
+    if (h_logits) cudaFreeHost(h_logits);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  void ensure(int n_segs, int64_t map_rows, int64_t V) {
+    if (!ev[0])
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+    if (n_segs > cap) {
+      int c = std::max(n_segs, 256);
+      if (h_segs) cudaFreeHost(h_segs);
+      if (h_first) cudaFreeHost(h_first);
+      if (d_segs) cudaFree(d_segs);
+      if (d_first) cudaFree(d_first);
+      CK(cudaMallocHost(&h_segs, c * sizeof(kern::CopySeg)));
+      CK(cudaMallocHost(&h_first, c * sizeof(uint64_t)));
+      CK(cudaMalloc(&d_segs, c * sizeof(kern::CopySeg)));
+      CK(cudaMalloc(&d_first, c * sizeof(uint64_t)));
+      cap = c;
+    }
+    if (map_rows > map_cap) {
+      int64_t c = std::max<int64_t>(map_rows, 1024);
+      if (h_map) cudaFreeHost(h_map);
+      if (d_map) cudaFree(d_map);
+      CK(cudaMallocHost(&h_map, c * 4));
+      CK(cudaMalloc(&d_map, c * 4));
+      map_cap = c;
+    }
+    if (!h_tok) CK(cudaMallocHost(&h_tok, 64));
+    if (V > logit_cap) {
+      if (h_logits) cudaFreeHost(h_logits);
+      CK(cudaMallocHost(&h_logits, V * 4));
+      logit_cap = V;
+    }
+  }
+};
+
+AsmScratch& scratch_of(cache::ModuleStore& store) {
+  if (!store.assembly_scratch) store.assembly_scratch = std::make_shared<AsmScratch>();
+  return *static_cast<AsmScratch*>(store.assembly_scratch.get());
+}
+
+// Position-disjointness check of concat_kv (engine.cpp:176-181).
+void check_disjoint(const std::vector<cache::EntryPtr>& entries) {
+  std::set<int64_t> seen;
+  for (auto& e : entries)
+    for (int64_t p : e->kv->positions)
+      if (!seen.insert(p).second)
+        throw Error(ErrorCode::PositionOverlap, "cache entries overlap at position " + std::to_string(p));
+}
+
+// Gathers the entries' KV rows into `dst` rows [0, sum) — one assembly-kernel
+// launch for every device-resident (fast tier) block; slow-tier blocks are
+// H2D copies issued on the same stream.  Returns #slow entries.
+int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model::KVBlock& dst, AsmScratch& sc) {
+  const int L = m.config().n_layers;
+  const size_t rb = dst.row_bytes();
+  int n_segs = 0, slow = 0;
+  sc.ensure(static_cast<int>(entries.size()) * 2 * L, 0, 0);
+  int64_t row = 0;
+  for (auto& e : entries) {
+    const model::KVBlock& b = *e->kv;
+    if (b.rows) {
+      if (b.host) {
+        ++slow;
+        CK(cudaMemcpy2DAsync(dst.plane(0, 0) + row * rb, dst.plane_bytes(), b.plane(0, 0), b.plane_bytes(),
+                             b.rows * rb, 2 * L, cudaMemcpyHostToDevice, m.stream()));
+      } else if (rb % 16 == 0) {
+        for (int l = 0; l < L; ++l)
+          for (int w = 0; w < 2; ++w)
+            sc.h_segs[n_segs++] = kern::CopySeg{b.plane(l, w), dst.plane(l, w) + row * rb, b.rows * rb};
+      } else {
+        CK(cudaMemcpy2DAsync(dst.plane(0, 0) + row * rb, dst.plane_bytes(), b.plane(0, 0), b.plane_bytes(),
+                             b.rows * rb, 2 * L, cudaMemcpyDeviceToDevice, m.stream()));
+      }
+    }
+    dst.positions.insert(dst.positions.end(), b.positions.begin(), b.positions.end());
+    row += b.rows;
+  }
+  dst.rows = row;
+  if (n_segs) {
+    const uint64_t chunks = kern::assemble_plan(sc.h_segs, n_segs, sc.h_first);
+    CK(cudaMemcpyAsync(sc.d_segs, sc.h_segs, n_segs * sizeof(kern::CopySeg), cudaMemcpyHostToDevice, m.stream()));
+    CK(cudaMemcpyAsync(sc.d_first, sc.h_first, n_segs * sizeof(uint64_t), cudaMemcpyHostToDevice, m.stream()));
+    kern::assemble(sc.d_segs, sc.d_first, n_segs, chunks, m.stream());
+    m.launches += 1;
+  }
+  return slow;
+}
+
+model::KVBlock& arena_of(cache::ModuleStore& store, int64_t cap) {
+  model::Model& m = store.model();
+  if (!store.arena || store.arena->cap < cap) {
+    store.arena.reset();
+    store.arena = m.alloc_kv(std::max<int64_t>(cap, 64));
+  }
+  store.arena->rows = 0;
+  store.arena->positions.clear();
+  return *store.arena;
+}
+
+// Decode working cache (reference assemble_working, engine.cpp:78-97): cached
+// rows with supplied <unk> slots replaced by argument rows (unfilled tails
+// dropped), then free-text rows.  When nothing is replaced it IS the request
+// cache, so no copy is made.
+model::KVBlock* make_working(model::Model& m, model::KVBlock& work, int64_t n_cached, const UncachedPass& up,
+                             int extra, AsmScratch& sc, model::KVPtr& holder) {
+  if (up.arg_row_by_pos.empty() && up.drop_positions.empty()) return &work;
+  std::vector<int32_t> map;
+  std::vector<int64_t> pos;
+  for (int64_t r = 0; r < n_cached; ++r) {
+    const int64_t p = work.positions[r];
+    auto a = up.arg_row_by_pos.find(p);
+    if (a != up.arg_row_by_pos.end()) {
+      map.push_back(static_cast<int32_t>(n_cached + a->second));
+      pos.push_back(work.positions[n_cached + a->second]);
+    } else if (!up.drop_positions.count(p)) {
+      map.push_back(static_cast<int32_t>(r));
+      pos.push_back(p);
+    }
+  }
+  for (int64_t row : up.free_rows) {
+    map.push_back(static_cast<int32_t>(n_cached + row));
+    pos.push_back(work.positions[n_cached + row]);
+  }
+  const int64_t rows = static_cast<int64_t>(map.size());
+  holder = m.alloc_kv(rows + extra);
+  sc.ensure(0, rows, 0);
+  std::memcpy(sc.h_map, map.data(), rows * 4);
+  CK(cudaMemcpyAsync(sc.d_map, sc.h_map, rows * 4, cudaMemcpyHostToDevice, m.stream()));
+  kern::gather_map(work.data, work.cap, holder->data, holder->cap, sc.d_map, rows,
+                   static_cast<int64_t>(work.row_bytes()), 2 * m.config().n_layers, m.stream());
+  holder->rows = rows;
+  holder->positions = pos;
+  return holder.get();
+}
+
+// Suffix forward + first token (reference finish_decode, engine.cpp:110-126).
+void prefill_and_decode(ServeResponse& resp, model::Model& m, model::KVBlock& work, int64_t n_cached,
+                        const UncachedPass& up, int64_t first_pos, int max_new, AsmScratch& sc, Clock::time_point t0,
+                        cudaEvent_t ev_start) {
+  const int V = m.config().vocab_size;
+  const int64_t n = static_cast<int64_t>(up.tokens.size());
+  m.run(up.tokens.data(), up.positions.data(), n, work, nullptr, nullptr, max_new > 0 ? 1 : 0);
+  if (max_new > 0) {
+    m.argmax_last(1);
+    CK(cudaEventRecord(sc.ev[2], m.stream()));
+    CK(cudaMemcpyAsync(sc.h_logits, m.device_logits(), V * 4, cudaMemcpyDeviceToHost, m.stream()));
+    CK(cudaMemcpyAsync(sc.h_tok, m.device_argmax(), 4, cudaMemcpyDeviceToHost, m.stream()));
+  } else {
+    CK(cudaEventRecord(sc.ev[2], m.stream()));
+  }
+  CK(cudaStreamSynchronize(m.stream()));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, ev_start, sc.ev[2]));
+  resp.timings.prefill_device_us = ms * 1000.0;
+  resp.timings.uncached_prefill_us = ms * 1000.0;
+  resp.timings.ttft_us = us_since(t0);
+  if (max_new <= 0) return;
+  resp.first_token_logits.assign(sc.h_logits, sc.h_logits + V);
+  const int t1 = sc.h_tok[0];
+  resp.output_tokens.push_back(t1);
+  resp.timings.ttft_us = us_since(t0);
+  if (max_new > 1) {
+    auto td = Clock::now();
+    model::KVPtr holder;
+    model::KVBlock* wk = make_working(m, work, n_cached, up, max_new - 1, sc, holder);
+    std::vector<int> rest = m.generate(*wk, t1, first_pos, max_new - 1);
+    resp.output_tokens.insert(resp.output_tokens.end(), rest.begin(), rest.end());
+    resp.timings.decode_us_per_token = us_since(td) / (max_new - 1);
+  }
+  resp.output_text = pml::tok::detokenize(resp.output_tokens);
+}
+
+ServeResponse serve_baseline(const ServeRequest& req, const layout::ResolvedPrompt& r, const layout::LayoutPlan& plan,
+                             cache::ModuleStore& store, Clock::time_point t0) {
+  model::Model& m = store.model();
+  std::map<int64_t, int> by_pos;
+  for (const std::string& name : r.cached_imports) {
+    const layout::ModuleLayout& ml = plan.at(name);
+    for (size_t i = 0; i < ml.own_tokens.size(); ++i) by_pos[ml.own_positions[i]] = ml.own_tokens[i];
+  }
+  UncachedPass full = build_uncached(r, plan, false);
+  for (size_t i = 0; i < full.tokens.size(); ++i) by_pos[full.positions[i]] = full.tokens[i];
+  for (int64_t p : full.drop_positions) by_pos.erase(p);
+  UncachedPass up;  // the whole prompt, renumbered 0..n-1, every row free
+  for (auto& [p, t] : by_pos) {
+    up.free_rows.push_back(static_cast<int64_t>(up.tokens.size()));
+    up.positions.push_back(static_cast<int64_t>(up.tokens.size()));
+    up.tokens.push_back(t);
+  }
+  if (up.tokens.empty()) {
+    up.tokens.push_back(pml::tok::kBos);
+    up.positions.push_back(0);
+    up.free_rows.push_back(0);
+  }
+  ServeResponse resp;
+  resp.cache_report.uncached_token_count = static_cast<int64_t>(by_pos.size());
+  const int64_t n = static_cast<int64_t>(up.tokens.size());
+  AsmScratch& sc = scratch_of(store);
+  sc.ensure(0, 0, m.config().vocab_size);
+  model::KVBlock& work = arena_of(store, n + std::max(0, req.max_new_tokens - 1));
+  CK(cudaEventRecord(sc.ev[1], m.stream()));
+  prefill_and_decode(resp, m, work, 0, up, n, req.max_new_tokens, sc, t0, sc.ev[1]);
+  return resp;
+}
+
+}  // namespace
+
+model::KVPtr concat_kv(model::Model& m, const std::vector<cache::EntryPtr>& entries, int64_t extra_cap) {
+  check_disjoint(entries);
+  int64_t rows = 0;
+  for (auto& e : entries) rows += e->kv->rows;
+  model::KVPtr out = m.alloc_kv(rows + extra_cap);
+  AsmScratch sc;
+  assemble(m, entries, *out, sc);
+  CK(cudaStreamSynchronize(m.stream()));
+  return out;
+}
+
+ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::ModuleStore& store) {
+  auto t0 = Clock::now();
+  model::Model& m = store.model();
+  CK(cudaSetDevice(m.device()));
+  require_valid(req.prompt, schema.doc);
+  const layout::LayoutPlan& plan = schema.plan;
+  layout::ResolvedPrompt resolved = layout::resolve_prompt(req.prompt, plan);
+  if (!req.use_cache) return serve_baseline(req, resolved, plan, store, t0);
+
+  ServeResponse resp;
+  resp.timings.parse_us = us_since(t0);
+
+  auto tl = Clock::now();
+  std::vector<cache::EntryPtr> selected;  // pinned for the whole request
+  if (req.use_scaffolds) {
+    cache::EntryPtr sc = store.lookup_scaffold(schema.doc.name, resolved.cached_imports);
+    if (sc) {
+      selected.push_back(sc);
+      resp.cache_report.used_scaffold = true;
+      ++resp.cache_report.modules_hit;
+    }
+  }
+  if (selected.empty()) {
+    for (const std::string& name : resolved.cached_imports) {
+      cache::EntryPtr e = store.lookup(schema.doc.name, name);
+      const layout::ModuleLayout& ml = plan.at(name);
+      const bool stale = e && (e->token_len != static_cast<int64_t>(ml.own_tokens.size()) ||
+                               e->kv->positions != ml.own_positions);
+      if (!e || stale) {
+        ++resp.cache_report.modules_missed;
+        store.insert(cache::encode_module(m, plan, name));
+        e = store.lookup(schema.doc.name, name);
+      } else {
+        ++resp.cache_report.modules_hit;
+      }
+      selected.push_back(e);
+    }
+  }
+  resp.timings.lookup_us = us_since(tl);
+
+  check_disjoint(selected);
+  int64_t n_cached = 0;
+  for (auto& e : selected) {
+    n_cached += e->kv->rows;
+    resp.cache_report.cached_token_count += e->token_len;
+  }
+  UncachedPass up = build_uncached(resolved, plan, req.max_new_tokens > 0);
+  resp.cache_report.uncached_token_count = up.prompt_token_count;
+
+  AsmScratch& sc = scratch_of(store);
+  sc.ensure(0, 0, m.config().vocab_size);
+  const int64_t n = static_cast<int64_t>(up.tokens.size());
+  model::KVBlock& work = arena_of(store, n_cached + n + std::max(0, req.max_new_tokens - 1));
+  CK(cudaEventRecord(sc.ev[0], m.stream()));
+  const int slow = assemble(m, selected, work, sc);
+  CK(cudaEventRecord(sc.ev[1], m.stream()));
+  if (up.tokens.empty()) {
+    CK(cudaStreamSynchronize(m.stream()));
+    resp.timings.ttft_us = us_since(t0);
+    return resp;
+  }
+  const int64_t first_pos = std::max(resolved.suffix_start, up.positions.back() + 1);
+  prefill_and_decode(resp, m, work, n_cached, up, first_pos, req.max_new_tokens, sc, t0, sc.ev[1]);
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, sc.ev[0], sc.ev[1]));
+  resp.timings.assemble_us = ms * 1000.0;
+  resp.timings.copy_us = slow ? ms * 1000.0 : 0.0;
+  return resp;
+}
+
+ServeResponse oracle_serve(const ServeRequest& req, const Schema& schema, model::Model& m) {
+  auto t0 = Clock::now();
+  CK(cudaSetDevice(m.device()));
+  require_valid(req.prompt, schema.doc);
+  const layout::LayoutPlan& plan = schema.plan;
+  layout::ResolvedPrompt resolved = layout::resolve_prompt(req.prompt, plan);
+  ServeResponse resp;
+  resp.timings.parse_us = us_since(t0);
+  std::vector<int32_t> tokens;
+  std::vector<int64_t> positions;
+  std::vector<int32_t> block;
+  int bid = 0;
+  for (const std::string& name : resolved.cached_imports) {
+    const layout::ModuleLayout& ml = plan.at(name);
+    for (size_t i = 0; i < ml.own_tokens.size(); ++i) {
+      tokens.push_back(ml.own_tokens[i]);
+      positions.push_back(ml.own_positions[i]);
+      block.push_back(bid);
+    }
+    ++bid;
+    resp.cache_report.cached_token_count += static_cast<int64_t>(ml.own_tokens.size());
+  }
+  const int64_t n_cached = static_cast<int64_t>(tokens.size());
+  UncachedPass up = build_uncached(resolved, plan, req.max_new_tokens > 0);
+  resp.cache_report.uncached_token_count = up.prompt_token_count;
+  for (size_t i = 0; i < up.tokens.size(); ++i) {
+    tokens.push_back(up.tokens[i]);
+    positions.push_back(up.positions[i]);
+    block.push_back(-1);
+  }
+  const int64_t n = static_cast<int64_t>(tokens.size());
+  if (n == 0) {
+    resp.timings.ttft_us = us_since(t0);
+    return resp;
+  }
+  // Block-causal mask as block ids: a cached row sees earlier rows of its own
+  // module; an uncached row sees every earlier row (engine.cpp:300-307).
+  model::KVPtr kv = m.alloc_kv(n + std::max(0, req.max_new_tokens - 1));
+  AsmScratch sc;
+  sc.ensure(0, 0, m.config().vocab_size);
+  CK(cudaEventRecord(sc.ev[1], m.stream()));
+  if (up.tokens.empty()) {
+    m.run(tokens.data(), positions.data(), n, *kv, nullptr, block.data(), 0);
+    CK(cudaStreamSynchronize(m.stream()));
+    resp.timings.ttft_us = us_since(t0);
+    return resp;
+  }
+  // prefill_and_decode runs the uncached rows; here the whole sequence is the
+  // "suffix" of an empty cache with block ids, so run it directly.
+  const int V = m.config().vocab_size;
+  m.run(tokens.data(), positions.data(), n, *kv, nullptr, block.data(), 1);
+  m.argmax_last(1);
+  CK(cudaMemcpyAsync(sc.h_logits, m.device_logits(), V * 4, cudaMemcpyDeviceToHost, m.stream()));
+  CK(cudaMemcpyAsync(sc.h_tok, m.device_argmax(), 4, cudaMemcpyDeviceToHost, m.stream()));
+  CK(cudaStreamSynchronize(m.stream()));
+  resp.timings.uncached_prefill_us = us_since(t0);
+  resp.timings.ttft_us = us_since(t0);
+  const int max_new = req.max_new_tokens;
+  if (max_new <= 0) return resp;
+  resp.first_token_logits.assign(sc.h_logits, sc.h_logits + V);
+  const int t1 = sc.h_tok[0];
+  resp.output_tokens.push_back(t1);
+  const int64_t first_pos = std::max(resolved.suffix_start, positions.back() + 1);
+  if (max_new > 1) {
+    auto td = Clock::now();
+    model::KVPtr holder;
+    model::KVBlock* wk = make_working(m, *kv, n_cached, up, max_new - 1, sc, holder);
+    std::vector<int> rest = m.generate(*wk, t1, first_pos, max_new - 1);
+    resp.output_tokens.insert(resp.output_tokens.end(), rest.begin(), rest.end());
+    resp.timings.decode_us_per_token = us_since(td) / (max_new - 1);
+  }
+  resp.output_text = pml::tok::detokenize(resp.output_tokens);
+  return resp;
+}
+
+std::string ServeResponse::to_json() const {
+  nlohmann::json j;
+  j["output_tokens"] = output_tokens;
+  j["output_text"] = output_text;
+  j["timings"] = {{"parse_us", timings.parse_us},
+                  {"lookup_us", timings.lookup_us},
+                  {"copy_us", timings.copy_us},
+                  {"uncached_prefill_us", timings.uncached_prefill_us},
+                  {"ttft_us", timings.ttft_us},
+                  {"decode_us_per_token", timings.decode_us_per_token},
+                  {"assemble_us", timings.assemble_us},
+                  {"prefill_device_us", timings.prefill_device_us}};
+  j["cache_report"] = {{"modules_hit", cache_report.modules_hit},
+                       {"modules_missed", cache_report.modules_missed},
+                       {"cached_token_count", cache_report.cached_token_count},
+                       {"uncached_token_count", cache_report.uncached_token_count},
+                       {"used_scaffold", cache_report.used_scaffold}};
+  return j.dump(-1, ' ', false, nlohmann::json::error_handler_t::replace);
+}
+
+}  // namespace pcb::engine

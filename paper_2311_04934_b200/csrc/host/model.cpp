@@ -1,0 +1,629 @@
+// Device model: weights generated in HBM by the PCG jump-ahead kernel, and the
+// per-layer launch sequence of the reference forward (model.cpp:304-443):
+//   embed -> [LN1 -> QKV GEMM (+RoPE at schema positions, K/V written straight
+//   into the request cache) -> attention -> O GEMM (+residual) -> LN2 -> W1 GEMM
+//   (+GELU) -> W2 GEMM (+residual)] x L -> final LN -> unembed (last rows only).
+#include "model.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "../kernels/kernels.cuh"
+#include "json.hpp"
+
+#define CK(x)                                                                                        \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess)                                                                           \
+      throw ::pcb::Error(::pcb::ErrorCode::CudaError, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace pcb::model {
+
+uint64_t fnv1a64(const void* data, size_t len) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  uint64_t h = 14695981039346656037ULL;
+  for (size_t i = 0; i < len; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// Config (reference model.cpp:59-96): same JSON keys, defaults and canonical
+// serialization, so config hashes (and PCST files) interoperate.
+// ---------------------------------------------------------------------------
+static const char* pos_name(PosEncoding p) {
+  return p == PosEncoding::Rope ? "rope" : p == PosEncoding::Alibi ? "alibi" : "abs_table";
+}
+
+ModelConfig ModelConfig::from_json(const std::string& text) {
+  nlohmann::json j;
+  try {
+    j = nlohmann::json::parse(text);
+  } catch (const std::exception& e) {
+    throw Error(ErrorCode::InvalidConfig, std::string("bad config JSON: ") + e.what());
+  }
+  ModelConfig c;
+  try {
+    c.n_layers = j.value("n_layers", c.n_layers);
+    c.n_heads = j.value("n_heads", c.n_heads);
+    c.head_dim = j.value("head_dim", c.head_dim);
+    c.hidden = j.value("hidden", c.n_heads * c.head_dim);
+    c.vocab_size = j.value("vocab_size", c.vocab_size);
+    std::string pe = j.value("pos_encoding", std::string("rope"));
+    if (pe == "rope") c.pos_encoding = PosEncoding::Rope;
+    else if (pe == "alibi") c.pos_encoding = PosEncoding::Alibi;
+    else if (pe == "abs_table") c.pos_encoding = PosEncoding::AbsTable;
+    else throw Error(ErrorCode::InvalidConfig, "unknown pos_encoding \"" + pe + "\"");
+    c.max_position = j.value("max_position", c.max_position);
+    c.bytes_per_element = j.value("bytes_per_element", c.bytes_per_element);
+    c.seed = j.value("seed", c.seed);
+  } catch (const nlohmann::json::exception& e) {
+    throw Error(ErrorCode::InvalidConfig, std::string("bad config field: ") + e.what());
+  }
+  if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 1 || c.hidden < 1 || c.vocab_size < 1 || c.max_position < 1 ||
+      c.bytes_per_element < 1)
+    throw Error(ErrorCode::InvalidConfig, "config fields must be positive");
+  return c;
+}
+
+std::string ModelConfig::to_json() const {
+  nlohmann::json j;
+  j["n_layers"] = n_layers;
+  j["n_heads"] = n_heads;
+  j["head_dim"] = head_dim;
+  j["hidden"] = hidden;
+  j["vocab_size"] = vocab_size;
+  j["pos_encoding"] = pos_name(pos_encoding);
+  j["max_position"] = max_position;
+  j["bytes_per_element"] = bytes_per_element;
+  j["seed"] = seed;
+  return j.dump();
+}
+
+uint64_t ModelConfig::hash() const {
+  std::string s = to_json();
+  return fnv1a64(s.data(), s.size());
+}
+
+// ---------------------------------------------------------------------------
+KVBlock::~KVBlock() {
+  if (data) {
+    if (host) cudaFreeHost(data);
+    else cudaFree(data);
+  }
+}
+
+struct Weights {
+  float* embed = nullptr;
+  void* unembed = nullptr;
+  std::vector<void*> wqkv, wo, w1, w2;
+  double *cos64 = nullptr, *sin64 = nullptr;
+  float *cos32 = nullptr, *sin32 = nullptr;
+  float* alibi = nullptr;
+  float* abs_table = nullptr;
+  std::vector<void*> owned;
+  ~Weights() {
+    for (void* p : owned) cudaFree(p);
+  }
+  void* alloc(size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    owned.push_back(p);
+    return p;
+  }
+};
+
+struct Workspace {
+  int64_t cap_n = 0, cap_rows = 0, cap_logit = 0, cap_mask = 0;
+  int d = 0, V = 0, dt = BF16;
+  int32_t *tok = nullptr, *pos = nullptr, *kvpos = nullptr, *block = nullptr, *argmax = nullptr;
+  uint8_t* mask = nullptr;
+  float* h = nullptr;
+  void *x = nullptr, *q = nullptr, *attn = nullptr, *mid = nullptr;
+  float* logits = nullptr;
+  float* gemm_ws = nullptr;
+  size_t gemm_ws_bytes = 0;
+  int* counters = nullptr;
+  float* attn_scratch = nullptr;
+  size_t attn_scratch_bytes = 0;
+  int32_t* host_ints = nullptr;  // pinned staging
+  int64_t host_ints_cap = 0;
+
+  ~Workspace() {
+    for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)mask, (void*)h, x, q,
+                    attn, mid, (void*)logits, (void*)gemm_ws, (void*)counters, (void*)attn_scratch})
+      if (p) cudaFree(p);
+    if (host_ints) cudaFreeHost(host_ints);
+  }
+  template <typename T>
+  static void regrow(T*& p, size_t bytes) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    CK(cudaMalloc(reinterpret_cast<void**>(&p), bytes));
+  }
+  void ensure(int64_t n, int64_t rows, int64_t logit_rows, bool want_mask) {
+    const size_t es = dt == F32 ? 4 : 2;
+    if (n > cap_n) {
+      int64_t c = std::max<int64_t>(n, 64);
+      regrow(tok, c * 4);
+      regrow(pos, c * 4);
+      regrow(block, c * 4);
+      regrow(h, c * d * 4);
+      regrow(x, c * d * es);
+      regrow(q, c * d * es);
+      regrow(attn, c * d * es);
+      regrow(mid, c * 4 * d * es);
+      cap_n = c;
+    }
+    if (rows > cap_rows) {
+      int64_t c = std::max<int64_t>(rows, 256);
+      regrow(kvpos, c * 4);
+      cap_rows = c;
+    }
+    if (logit_rows > cap_logit) {
+      int64_t c = std::max<int64_t>(logit_rows, 1);
+      regrow(logits, c * V * 4);
+      cap_logit = c;
+    }
+    if (want_mask && n * n > cap_mask) {
+      regrow(mask, n * n);
+      cap_mask = n * n;
+    }
+    if (!argmax) regrow(argmax, 1024 * 4);
+    if (!gemm_ws) {
+      gemm_ws_bytes = 64ull << 20;
+      regrow(gemm_ws, gemm_ws_bytes);
+      regrow(counters, 65536 * 4);
+      CK(cudaMemset(counters, 0, 65536 * 4));
+    }
+    int64_t need_ints = 3 * n + rows + 16;
+    if (need_ints > host_ints_cap) {
+      if (host_ints) cudaFreeHost(host_ints);
+      CK(cudaMallocHost(reinterpret_cast<void**>(&host_ints), need_ints * 4));
+      host_ints_cap = need_ints;
+    }
+  }
+  void ensure_attn_scratch(size_t bytes) {
+    if (bytes > attn_scratch_bytes) {
+      regrow(attn_scratch, bytes);
+      attn_scratch_bytes = bytes;
+    }
+  }
+};
+
+static std::string tname(int l, const char* t) { return "layer" + std::to_string(l) + "." + t; }
+
+static uint64_t stream_seed(const std::string& name, uint64_t seed) {
+  return splitmix64(fnv1a64(name.data(), name.size()) ^ splitmix64(seed));
+}
+
+Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtype), device_(device) {
+  if (c.hidden != c.n_heads * c.head_dim) throw Error(ErrorCode::InvalidConfig, "hidden must equal n_heads * head_dim");
+  if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 2 || c.head_dim % 2 != 0)
+    throw Error(ErrorCode::InvalidConfig, "bad layer/head geometry");
+  if (c.vocab_size < 259)
+    throw Error(ErrorCode::InvalidConfig, "vocab_size must be at least 259 to cover bytes plus specials");
+  if (c.max_position < 1) throw Error(ErrorCode::InvalidConfig, "max_position must be positive");
+  if (c.max_position > (1LL << 31) - 1) throw Error(ErrorCode::InvalidConfig, "max_position exceeds int32 device range");
+  if (dtype != F32 && dtype != BF16) throw Error(ErrorCode::InvalidConfig, "dtype must be f32 or bf16");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(ErrorCode::CudaError, "no CUDA device: the Prompt Cache engine has no CPU fallback");
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  w_ = std::make_unique<Weights>();
+  ws_ = std::make_unique<Workspace>();
+  ws_->d = c.hidden;
+  ws_->V = c.vocab_size;
+  ws_->dt = dtype;
+
+  const int d = c.hidden;
+  const size_t es = dtype == F32 ? 4 : 2;
+  const float ws = 1.0f / std::sqrt(static_cast<float>(d));
+  const float ws2 = 1.0f / std::sqrt(static_cast<float>(4 * d));
+  const size_t Vd = static_cast<size_t>(c.vocab_size) * d;
+  // weight init (reference model.cpp:191-218): same tensor names, scales, streams
+  w_->embed = static_cast<float*>(w_->alloc(Vd * 4));
+  kern::init_uniform(F32, w_->embed, Vd, stream_seed("embed", c.seed), 0.1f, stream_);
+  w_->unembed = w_->alloc(Vd * es);
+  kern::init_uniform(dtype, w_->unembed, Vd, stream_seed("unembed", c.seed), ws, stream_);
+  const size_t dd = static_cast<size_t>(d) * d;
+  for (int l = 0; l < c.n_layers; ++l) {
+    char* qkv = static_cast<char*>(w_->alloc(3 * dd * es));
+    kern::init_uniform(dtype, qkv, dd, stream_seed(tname(l, "wq"), c.seed), ws, stream_);
+    kern::init_uniform(dtype, qkv + dd * es, dd, stream_seed(tname(l, "wk"), c.seed), ws, stream_);
+    kern::init_uniform(dtype, qkv + 2 * dd * es, dd, stream_seed(tname(l, "wv"), c.seed), ws, stream_);
+    w_->wqkv.push_back(qkv);
+    void* wo = w_->alloc(dd * es);
+    kern::init_uniform(dtype, wo, dd, stream_seed(tname(l, "wo"), c.seed), ws, stream_);
+    w_->wo.push_back(wo);
+    void* w1 = w_->alloc(4 * dd * es);
+    kern::init_uniform(dtype, w1, 4 * dd, stream_seed(tname(l, "w1"), c.seed), ws, stream_);
+    w_->w1.push_back(w1);
+    void* w2 = w_->alloc(4 * dd * es);
+    kern::init_uniform(dtype, w2, 4 * dd, stream_seed(tname(l, "w2"), c.seed), ws2, stream_);
+    w_->w2.push_back(w2);
+  }
+  if (c.pos_encoding == PosEncoding::Rope) {  // model.cpp:220-230, glibc fp64 table
+    const int half = c.head_dim / 2;
+    const size_t cnt = static_cast<size_t>(c.max_position) * half;
+    std::vector<double> cs(cnt), sn(cnt);
+    for (int64_t p = 0; p < c.max_position; ++p)
+      for (int i = 0; i < half; ++i) {
+        double theta = std::pow(10000.0, -2.0 * i / c.head_dim);
+        cs[p * half + i] = std::cos(static_cast<double>(p) * theta);
+        sn[p * half + i] = std::sin(static_cast<double>(p) * theta);
+      }
+    if (dtype == F32) {
+      w_->cos64 = static_cast<double*>(w_->alloc(cnt * 8));
+      w_->sin64 = static_cast<double*>(w_->alloc(cnt * 8));
+      CK(cudaMemcpy(w_->cos64, cs.data(), cnt * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(w_->sin64, sn.data(), cnt * 8, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float> c32(cnt), s32(cnt);
+      for (size_t i = 0; i < cnt; ++i) {
+        c32[i] = static_cast<float>(cs[i]);
+        s32[i] = static_cast<float>(sn[i]);
+      }
+      w_->cos32 = static_cast<float*>(w_->alloc(cnt * 4));
+      w_->sin32 = static_cast<float*>(w_->alloc(cnt * 4));
+      CK(cudaMemcpy(w_->cos32, c32.data(), cnt * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(w_->sin32, s32.data(), cnt * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  if (c.pos_encoding == PosEncoding::Alibi) {  // model.cpp:231-236
+    std::vector<float> sl(c.n_heads);
+    for (int h = 0; h < c.n_heads; ++h) sl[h] = static_cast<float>(std::pow(2.0, -8.0 * (h + 1) / c.n_heads));
+    w_->alibi = static_cast<float*>(w_->alloc(c.n_heads * 4));
+    CK(cudaMemcpy(w_->alibi, sl.data(), c.n_heads * 4, cudaMemcpyHostToDevice));
+  }
+  if (c.pos_encoding == PosEncoding::AbsTable) {  // model.cpp:237-245
+    const size_t cnt = static_cast<size_t>(c.max_position) * d;
+    std::vector<float> t(cnt);
+    for (int64_t p = 0; p < c.max_position; ++p)
+      for (int i = 0; i < d / 2; ++i) {
+        double theta = static_cast<double>(p) / std::pow(10000.0, 2.0 * i / d);
+        t[p * d + 2 * i] = static_cast<float>(std::sin(theta));
+        t[p * d + 2 * i + 1] = static_cast<float>(std::cos(theta));
+      }
+    w_->abs_table = static_cast<float*>(w_->alloc(cnt * 4));
+    CK(cudaMemcpy(w_->abs_table, t.data(), cnt * 4, cudaMemcpyHostToDevice));
+  }
+  CK(cudaStreamSynchronize(stream_));
+}
+
+Model::~Model() {
+  if (stream_) {
+    cudaStreamSynchronize(stream_);
+    cudaStreamDestroy(stream_);
+  }
+}
+
+KVPtr Model::alloc_kv(int64_t cap, bool host) const {
+  auto kv = std::make_shared<KVBlock>();
+  kv->dtype = dtype_;
+  kv->n_layers = cfg_.n_layers;
+  kv->hidden = cfg_.hidden;
+  kv->cap = cap;
+  kv->host = host;
+  if (cap > 0) {
+    if (host) CK(cudaMallocHost(&kv->data, kv->bytes()));
+    else CK(cudaMalloc(&kv->data, kv->bytes()));
+  }
+  return kv;
+}
+
+void Model::copy_rows(const KVBlock& src, KVBlock& dst, int64_t dst_row) const {
+  if (src.rows == 0) return;
+  if (dst_row + src.rows > dst.cap) throw Error(ErrorCode::Internal, "copy_rows: destination too small");
+  const cudaMemcpyKind kind = src.host ? (dst.host ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice)
+                                       : (dst.host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  const size_t rb = src.row_bytes();
+  // every plane is one strided 2-D copy: L*2 rows of src.rows*rb bytes
+  CK(cudaMemcpy2DAsync(dst.data == nullptr ? nullptr : dst.plane(0, 0) + dst_row * rb, dst.plane_bytes(),
+                       src.plane(0, 0), src.plane_bytes(), src.rows * rb, 2 * src.n_layers, kind, stream_));
+}
+
+KVPtr Model::to_host(const KVBlock& src) const {
+  KVPtr h = alloc_kv(src.rows, true);
+  copy_rows(src, *h, 0);
+  h->rows = src.rows;
+  h->positions = src.positions;
+  CK(cudaStreamSynchronize(stream_));
+  return h;
+}
+
+void Model::validate(const int32_t* tokens, const int64_t* positions, int64_t n, const KVBlock& kv) const {
+  for (int64_t i = 0; i < n; ++i) {
+    if (positions[i] < 0 || positions[i] >= cfg_.max_position)
+      throw Error(ErrorCode::PositionOutOfRange, "position " + std::to_string(positions[i]) + " outside [0, " +
+                                                     std::to_string(cfg_.max_position) + ")");
+    if (tokens[i] < 0 || tokens[i] >= cfg_.vocab_size)
+      throw Error(ErrorCode::ShapeMismatch, "token id out of vocab range");
+  }
+  if (kv.n_layers != cfg_.n_layers || kv.hidden != cfg_.hidden || kv.dtype != dtype_)
+    throw Error(ErrorCode::ShapeMismatch, "past KV shape mismatch");
+  if (kv.host) throw Error(ErrorCode::ShapeMismatch, "forward needs a device-resident KV block");
+  if (kv.rows + n > kv.cap) throw Error(ErrorCode::ShapeMismatch, "KV block capacity exceeded");
+}
+
+void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi) {
+  const auto& e = *static_cast<const kern::Epilogue*>(epi);
+  if (dtype_ == BF16 && !force_simt && kern::gemm_tc_supported(M, N, K))
+    kern::gemm_tc(A, W, M, N, K, e, ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->counters, stream_);
+  else
+    kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_);
+  ++launches;
+}
+
+void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBlock& kv, const uint8_t* mask,
+                const int32_t* block_ids, int64_t logit_rows) {
+  CK(cudaSetDevice(device_));
+  validate(tokens, positions, n, kv);
+  if (mask && kv.rows) throw Error(ErrorCode::ShapeMismatch, "masked forward takes no past KV");
+  if (mask)
+    for (int64_t i = 0; i < n; ++i)
+      if (!mask[i * n + i]) throw Error(ErrorCode::ShapeMismatch, "mask diagonal must be true");
+  if (n <= 0) return;
+  logit_rows = std::min(logit_rows, n);
+  forward_tokens.fetch_add(n, std::memory_order_relaxed);
+  const auto& c = cfg_;
+  const int d = c.hidden, H = c.n_heads, hd = c.head_dim;
+  const int64_t P = kv.rows, total = P + n;
+  Workspace& W = *ws_;
+  W.ensure(n, total, logit_rows, mask != nullptr);
+  cudaStream_t s = stream_;
+
+  // stage token ids / int32 positions (positions < max_position < 2^31, checked)
+  int32_t* hi = W.host_ints;
+  for (int64_t i = 0; i < n; ++i) {
+    hi[i] = tokens[i];
+    hi[n + i] = static_cast<int32_t>(positions[i]);
+  }
+  CK(cudaMemcpyAsync(W.tok, hi, n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(W.pos, hi + n, n * 4, cudaMemcpyHostToDevice, s));
+  const bool alibi = c.pos_encoding == PosEncoding::Alibi;
+  if (alibi) {
+    int32_t* kp = hi + 2 * n;
+    for (int64_t j = 0; j < P; ++j) kp[j] = static_cast<int32_t>(kv.positions[j]);
+    for (int64_t i = 0; i < n; ++i) kp[P + i] = static_cast<int32_t>(positions[i]);
+    CK(cudaMemcpyAsync(W.kvpos, kp, total * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (mask) CK(cudaMemcpyAsync(W.mask, mask, n * n, cudaMemcpyHostToDevice, s));
+  if (block_ids) {
+    int32_t* bp = hi + 2 * n + (alibi ? total : 0);
+    std::memcpy(bp, block_ids, n * 4);
+    CK(cudaMemcpyAsync(W.block, bp, n * 4, cudaMemcpyHostToDevice, s));
+  }
+
+  kern::embed(W.tok, W.pos, n, w_->embed, w_->abs_table, d, W.h, s);
+  launches += 1;
+
+  kern::AttnArgs aa;
+  aa.n = n;
+  aa.P = P;
+  aa.H = H;
+  aa.hd = hd;
+  aa.d = d;
+  aa.q = W.q;
+  aa.out = W.attn;
+  aa.mask = mask ? W.mask : nullptr;
+  aa.block_id = block_ids ? W.block : nullptr;
+  aa.alibi = alibi ? w_->alibi : nullptr;
+  aa.kv_pos = alibi ? W.kvpos : nullptr;
+  const bool tc_attn = dtype_ == BF16 && !force_simt && kern::attention_tc_supported(aa);
+  int64_t nq = n;
+  if (!tc_attn) {
+    const size_t per_q = static_cast<size_t>(H) * total * sizeof(double);
+    const size_t budget = 512ull << 20;
+    nq = std::max<int64_t>(1, std::min<int64_t>(n, static_cast<int64_t>(budget / per_q)));
+    W.ensure_attn_scratch(per_q * nq);
+  } else {
+    W.ensure_attn_scratch(64ull << 20);
+  }
+
+  for (int l = 0; l < c.n_layers; ++l) {
+    kern::layernorm(dtype_, W.h, n, d, W.x, s);
+    kern::Epilogue e;
+    e.kind = kern::EPI_QKV;
+    e.d = d;
+    e.q_out = W.q;
+    e.k_out = kv.k(l);
+    e.v_out = kv.v(l);
+    e.kv_row0 = P;
+    e.pos = W.pos;
+    e.rope = c.pos_encoding == PosEncoding::Rope;
+    e.head_dim = hd;
+    e.rope_cos64 = w_->cos64;
+    e.rope_sin64 = w_->sin64;
+    e.rope_cos32 = w_->cos32;
+    e.rope_sin32 = w_->sin32;
+    gemm(W.x, w_->wqkv[l], n, 3 * d, d, &e);
+
+    aa.k = kv.k(l);
+    aa.v = kv.v(l);
+    if (tc_attn) {
+      kern::attention_tc(aa, W.attn_scratch, W.attn_scratch_bytes, s);
+      ++launches;
+    } else {
+      for (int64_t i0 = 0; i0 < n; i0 += nq) {
+        aa.i0 = i0;
+        aa.nq = std::min(nq, n - i0);
+        kern::attention_simt(dtype_, aa, W.attn_scratch, s);
+        ++launches;
+      }
+      aa.i0 = 0;
+      aa.nq = -1;
+    }
+
+    kern::Epilogue eo;
+    eo.kind = kern::EPI_RESID;
+    eo.resid = W.h;
+    gemm(W.attn, w_->wo[l], n, d, d, &eo);
+    kern::layernorm(dtype_, W.h, n, d, W.x, s);
+    kern::Epilogue eg;
+    eg.kind = kern::EPI_GELU;
+    eg.out = W.mid;
+    gemm(W.x, w_->w1[l], n, 4 * d, d, &eg);
+    gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo);
+    launches += 2;
+  }
+  if (logit_rows > 0) {
+    const int64_t r0 = n - logit_rows;
+    kern::layernorm(dtype_, W.h + r0 * d, logit_rows, d, W.x, s);
+    kern::Epilogue ef;
+    ef.kind = kern::EPI_F32;
+    ef.outf = W.logits;
+    ef.ldo = c.vocab_size;
+    gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
+    launches += 1;
+  }
+  kv.rows = total;
+  kv.positions.insert(kv.positions.end(), positions, positions + n);
+}
+
+const float* Model::device_logits() const { return ws_->logits; }
+int32_t* Model::device_argmax() const { return ws_->argmax; }
+
+void Model::argmax_last(int64_t logit_rows) {
+  kern::argmax_rows(ws_->logits, logit_rows, cfg_.vocab_size, ws_->argmax, stream_);
+  ++launches;
+}
+
+// ---------------------------------------------------------------------------
+// Reference-shaped API
+// ---------------------------------------------------------------------------
+ForwardOutput Model::forward(const std::vector<int>& tokens, const std::vector<int64_t>& positions,
+                             const KVBlock* past) {
+  if (tokens.size() != positions.size())
+    throw Error(ErrorCode::ShapeMismatch, "tokens/position_ids length mismatch");
+  if (past && (past->n_layers != cfg_.n_layers || past->hidden != cfg_.hidden || past->dtype != dtype_))
+    throw Error(ErrorCode::ShapeMismatch, "past KV shape mismatch");
+  if (past)
+    for (int64_t p : past->positions)
+      if (p < 0 || p >= cfg_.max_position) throw Error(ErrorCode::PositionOutOfRange, "past position out of range");
+  const int64_t n = static_cast<int64_t>(tokens.size());
+  const int64_t P = past ? past->rows : 0;
+  KVPtr kv = alloc_kv(P + n);
+  if (past) {
+    copy_rows(*past, *kv, 0);
+    kv->rows = P;
+    kv->positions = past->positions;
+  }
+  std::vector<int32_t> t32(tokens.begin(), tokens.end());
+  run(t32.data(), positions.data(), n, *kv, nullptr, nullptr, n);
+  ForwardOutput out;
+  out.seq = n;
+  out.vocab = cfg_.vocab_size;
+  out.logits.resize(static_cast<size_t>(n) * cfg_.vocab_size);
+  if (n) CK(cudaMemcpyAsync(out.logits.data(), ws_->logits, out.logits.size() * 4, cudaMemcpyDeviceToHost, stream_));
+  out.new_kv = alloc_kv(n);
+  if (n) {
+    const size_t rb = kv->row_bytes();
+    CK(cudaMemcpy2DAsync(out.new_kv->plane(0, 0), out.new_kv->plane_bytes(), kv->plane(0, 0) + P * rb,
+                         kv->plane_bytes(), n * rb, 2 * cfg_.n_layers, cudaMemcpyDeviceToDevice, stream_));
+  }
+  out.new_kv->rows = n;
+  out.new_kv->positions = positions;
+  CK(cudaStreamSynchronize(stream_));
+  return out;
+}
+
+ForwardOutput Model::forward_masked(const std::vector<int>& tokens, const std::vector<int64_t>& positions,
+                                    const std::vector<uint8_t>& mask) {
+  const int64_t n = static_cast<int64_t>(tokens.size());
+  if (positions.size() != tokens.size()) throw Error(ErrorCode::ShapeMismatch, "tokens/position_ids length mismatch");
+  if (static_cast<int64_t>(mask.size()) != n * n) throw Error(ErrorCode::ShapeMismatch, "mask must be [seq, seq]");
+  KVPtr kv = alloc_kv(n);
+  std::vector<int32_t> t32(tokens.begin(), tokens.end());
+  run(t32.data(), positions.data(), n, *kv, mask.data(), nullptr, n);
+  ForwardOutput out;
+  out.seq = n;
+  out.vocab = cfg_.vocab_size;
+  out.logits.resize(static_cast<size_t>(n) * cfg_.vocab_size);
+  if (n) CK(cudaMemcpyAsync(out.logits.data(), ws_->logits, out.logits.size() * 4, cudaMemcpyDeviceToHost, stream_));
+  out.new_kv = kv;
+  CK(cudaStreamSynchronize(stream_));
+  return out;
+}
+
+std::vector<int> Model::generate(KVBlock& kv, int last_token, int64_t last_position, int n_steps) {
+  std::vector<int> out;
+  int32_t cur = last_token;
+  int64_t pos = last_position;
+  int32_t* host = nullptr;
+  CK(cudaMallocHost(reinterpret_cast<void**>(&host), 4));
+  try {
+    for (int s = 0; s < n_steps; ++s) {
+      if (kv.rows + 1 > kv.cap) {  // grow: reference KVState::append semantics
+        KVPtr bigger = alloc_kv(std::max<int64_t>(kv.cap * 2, kv.rows + n_steps - s));
+        copy_rows(kv, *bigger, 0);
+        std::swap(kv.data, bigger->data);
+        std::swap(kv.cap, bigger->cap);
+      }
+      run(&cur, &pos, 1, kv, nullptr, nullptr, 1);
+      argmax_last(1);
+      CK(cudaMemcpyAsync(host, ws_->argmax, 4, cudaMemcpyDeviceToHost, stream_));
+      CK(cudaStreamSynchronize(stream_));
+      cur = *host;
+      out.push_back(cur);
+      ++pos;
+    }
+  } catch (...) {
+    cudaFreeHost(host);
+    throw;
+  }
+  cudaFreeHost(host);
+  return out;
+}
+
+uint64_t Model::weight_checksum(const std::string& name) const {
+  // FNV-1a over the fp32 tensor as generated (reference model.cpp:248-267).  The
+  // generator is re-run into a scratch buffer so the check is independent of the
+  // storage dtype (the bf16 model stores RNE of exactly these values).
+  const int d = cfg_.hidden;
+  size_t count = 0;
+  float scale = 1.0f / std::sqrt(static_cast<float>(d));
+  if (name == "embed") {
+    count = static_cast<size_t>(cfg_.vocab_size) * d;
+    scale = 0.1f;
+  } else if (name == "unembed") {
+    count = static_cast<size_t>(cfg_.vocab_size) * d;
+  } else {
+    for (int l = 0; l < cfg_.n_layers && !count; ++l)
+      for (const char* t : {"wq", "wk", "wv", "wo", "w1", "w2"})
+        if (name == tname(l, t)) {
+          count = static_cast<size_t>(d) * d * ((t[1] == '1' || t[1] == '2') ? 4 : 1);
+          if (t[1] == '2') scale = 1.0f / std::sqrt(static_cast<float>(4 * d));
+        }
+  }
+  if (!count) throw Error(ErrorCode::Internal, "unknown tensor \"" + name + "\"");
+  float* tmp = nullptr;
+  CK(cudaMalloc(&tmp, count * 4));
+  kern::init_uniform(F32, tmp, count, stream_seed(name, cfg_.seed), scale, stream_);
+  std::vector<float> h(count);
+  CK(cudaMemcpyAsync(h.data(), tmp, count * 4, cudaMemcpyDeviceToHost, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  cudaFree(tmp);
+  return fnv1a64(h.data(), count * 4);
+}
+
+int argmax_lowest(const float* logits, int n) {
+  int best = 0;
+  for (int i = 1; i < n; ++i)
+    if (logits[i] > logits[best]) best = i;
+  return best;
+}
+
+}  // namespace pcb::model

@@ -1,0 +1,110 @@
+// Device kernel entry points of the Prompt Cache hot path (sm_100a).
+//
+// Data layout in HBM:
+//   weights   W[out][in] row-major (K-major for the tensor cores), bf16 or fp32;
+//             per layer Wqkv fused [3d][d] (q rows, k rows, v rows), Wo [d][d],
+//             W1 [4d][d], W2 [d][4d]; embed fp32 [V][d]; unembed [V][d].
+//   KV block  [L][2][cap][d] (layer, K/V, row, head-interleaved hidden) — the
+//             same layout for store entries and a request's assembled cache, so
+//             KV assembly is one contiguous copy per (module, layer, K/V).
+//   residual  fp32 [n][d]; activations in the model dtype.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pcb::kern {
+
+enum DType : int { F32 = 0, BF16 = 1 };
+
+inline size_t dtype_size(int dt) { return dt == F32 ? 4 : 2; }
+
+enum EpiKind : int {
+  EPI_QKV = 0,     // N = 3d: q -> q_out[m][n]; k,v -> cache rows kv_row0+m; RoPE on q,k
+  EPI_RESID = 1,   // resid[m][n] += acc
+  EPI_GELU = 2,    // out[m][n] = gelu(acc)   (model dtype)
+  EPI_F32 = 3,     // outf[m*ldo + n] = acc   (fp32 logits)
+};
+
+struct Epilogue {
+  int kind = EPI_F32;
+  int d = 0;  // hidden (EPI_QKV)
+  void* q_out = nullptr;
+  void* k_out = nullptr;  // layer K base of the cache, row stride d
+  void* v_out = nullptr;
+  int64_t kv_row0 = 0;
+  const int32_t* pos = nullptr;  // per token (EPI_QKV rope)
+  int rope = 0;                  // apply RoPE
+  int head_dim = 0;
+  const double* rope_cos64 = nullptr;  // [max_pos][hd/2] (F32 path)
+  const double* rope_sin64 = nullptr;
+  const float* rope_cos32 = nullptr;   // (BF16 path)
+  const float* rope_sin32 = nullptr;
+  float* resid = nullptr;
+  void* out = nullptr;
+  float* outf = nullptr;
+  int64_t ldo = 0;
+};
+
+// ---- weights (PCG32 jump-ahead; bit-identical to the reference's fill_uniform) ----
+void init_uniform(int dtype, void* dst, uint64_t count, uint64_t stream_seed, float scale, cudaStream_t s);
+void fill_const(float* dst, uint64_t count, float v, cudaStream_t s);
+
+// ---- small ops ----
+void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table, const float* abs_table,
+           int d, float* h, cudaStream_t s);
+// out = LN(h) (gamma=1, beta=0, eps 1e-5), rows [row0, row0+n)
+void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s);
+void argmax_rows(const float* logits, int64_t rows, int V, int32_t* out, cudaStream_t s);
+
+// ---- GEMM: C[m][n] = sum_k A[m][k] * W[n][k] with a fused epilogue ----
+// SIMT: F32 = fp64 accumulation in the reference's 4-lane order (bit-exact
+// dot products); BF16 = fp32 accumulation (bring-up / odd shapes).
+void gemm_simt(int dtype, const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e,
+               cudaStream_t s);
+// tcgen05 + TMA + TMEM (bf16 in, fp32 accumulate).  Requires K%64==0, N%128==0.
+bool gemm_tc_supported(int64_t M, int N, int K);
+void gemm_tc(const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e, float* workspace,
+             size_t workspace_bytes, int* counters, cudaStream_t s);
+
+// ---- attention over a KV cache ----
+// q [n][d]; K/V layer bases [rows][d]; query i (sequence index P+i) attends keys
+// j <= P+i (sequence-order causality) or, with mask [n][n] (P must be 0), the
+// allowed set.  ALiBi uses per-row positions.
+struct AttnArgs {
+  const void* q = nullptr;
+  const void* k = nullptr;
+  const void* v = nullptr;
+  void* out = nullptr;
+  int64_t n = 0, P = 0;
+  int H = 0, hd = 0, d = 0;
+  const uint8_t* mask = nullptr;
+  const int32_t* block_id = nullptr;   // block-causal (oracle) variant: [P+n]
+  const float* alibi = nullptr;        // [H] or null
+  const int32_t* kv_pos = nullptr;     // [P+n] positions (alibi)
+  int64_t i0 = 0, nq = -1;             // query sub-range [i0, i0+nq) (nq < 0: all n)
+};
+void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s);
+size_t attention_simt_scratch(const AttnArgs& a);
+bool attention_tc_supported(const AttnArgs& a);
+void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s);
+
+// ---- KV assembly: batched contiguous copies (one descriptor per segment) ----
+struct CopySeg {
+  const void* src;
+  void* dst;
+  uint64_t bytes;  // multiple of 16
+};
+// Host planning: fills first_chunk[i] (chunk index where segment i starts) and
+// returns the total chunk count.  Segment bytes must be multiples of 16.
+uint64_t assemble_plan(const CopySeg* segs, int n_segs, uint64_t* first_chunk);
+void assemble(const CopySeg* d_segs, const uint64_t* d_first_chunk, int n_segs, uint64_t n_chunks, cudaStream_t s);
+// Row gather across all 2L planes of a KV block: dst[p][r] = src[p][map[r]],
+// used for the decode working cache (reference assemble_working, engine.cpp:65-97).
+void gather_map(const void* src, int64_t src_cap, void* dst, int64_t dst_cap, const int32_t* d_map, int64_t rows,
+                int64_t row_bytes, int planes, cudaStream_t s);
+
+// Convert between storage types (fp32 <-> bf16) for host interchange.
+void convert(int src_dtype, const void* src, int dst_dtype, void* dst, uint64_t count, cudaStream_t s);
+
+}  // namespace pcb::kern
