@@ -1,0 +1,442 @@
+"""Prompt Cache hot-path benchmark (driver contract: one JSON line from rank 0).
+
+Workload (BASELINE.json configs[1]): Llama-2-7B shape (L32 d4096 H32 hd128 V32000, random-init bf16
+weights from the reference's seeded PCG generator), one 4096-token document module precomputed into
+the HBM store, and a prompt ``<doc/>`` + 64 uncached tokens (positions 4096..4159).  One step = one
+cached serve request through to the first token.
+
+  value        requests/s over K steps, store resident in HBM, device-timed with CUDA events on the
+               model stream (max over ranks; each rank serves its own requests: weak scaling)
+  e2e          the same metric through the public C ABI (pcb_serve on prompt TEXT): host parse +
+               resolve, H2D of tokens/positions, D2H of first-token logits + token, host-clock timed
+  ttft_ms      mean cached TTFT (host clock, request receipt -> first token on host)
+  full_prefill_ttft_ms  same prompt with use_cache=False (4160-token prefill on the GPU)
+  roofline     dominant kernel class (GEMM weight streaming, HBM-bound at 64 tokens), CUDA events
+  cpu_baseline reference C++ (oracle/_ref, unmodified) on this host, bounded sample, extrapolated
+
+``--impl reference`` times the reference's own CPU implementation (oracle/_ref) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TTFT ms (cached vs full prefill) and requests/sec, Llama-2-7B shape, 1/2/4/8 B200"
+CFG_7B = dict(n_layers=32, n_heads=32, head_dim=128, hidden=4096, vocab_size=32000, pos_encoding="rope",
+              max_position=8192, bytes_per_element=2, seed=42)
+ALPHABET = "abcdefghijklmnopqrstuvwxyz ABCDEFGHIJKLMNOPQRSTUVWXYZ.,"
+
+
+def splitmix64(x: int) -> int:
+    M = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+def synthetic_text(n: int, seed: int) -> str:
+    """The reference's synthetic_text (bench.cpp:22-31): PCG32 over a 55-char alphabet."""
+    M = (1 << 64) - 1
+    state = (splitmix64(seed) + 1442695040888963407) & M
+    out = []
+
+    def nxt():
+        nonlocal state
+        old = state
+        state = (old * 6364136223846793005 + 1442695040888963407) & M
+        xs = (((old >> 18) ^ old) >> 27) & 0xFFFFFFFF
+        rot = old >> 59
+        return ((xs >> rot) | (xs << ((-rot) & 31))) & 0xFFFFFFFF
+
+    nxt()
+    for _ in range(n):
+        out.append(ALPHABET[nxt() % len(ALPHABET)])
+    return "".join(out)
+
+
+def question(n: int, seed: int) -> str:
+    s = list(synthetic_text(n, seed))
+    if s[0] == " ":
+        s[0] = "Q"
+    if s[-1] == " ":
+        s[-1] = "?"
+    return "".join(s)
+
+
+def workload(n_cached: int, n_uncached: int, n_modules: int = 1):
+    """Schema of n_modules document modules totalling n_cached tokens + prompt with n_uncached tokens."""
+    sizes = [n_cached // n_modules + (1 if i < n_cached % n_modules else 0) for i in range(n_modules)]
+    mods = "".join(f'<module name="doc{i}">{synthetic_text(sz, 7 * sz + 1 + i)}</module>'
+                   for i, sz in enumerate(sizes))
+    schema = f'<schema name="bench">{mods}</schema>'
+    imports = "".join(f"<doc{i}/>" for i in range(n_modules))
+    prompts = [f'<prompt schema="bench">{imports}{question(n_uncached, 1000 + r)}</prompt>' for r in range(4)]
+    return schema, prompts
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (one process per GPU; barrier + max over ranks)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist, self.torch = dist, torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified reference library)
+# ---------------------------------------------------------------------------
+def _ref_sample(n_s: int, P: int, reps: int):
+    """Times the reference's cached-prefill step on a 1-layer 7B-shape model: concat_kv of a P-row
+    module (engine.cpp:236) and Model::forward of n_s suffix tokens over it (engine.cpp:245).
+    Returns (t_forward_s, t_concat_s) medians."""
+    from oracle.oracle import Ref
+    import ctypes as C
+    L = Ref.lib()
+    cfg = dict(CFG_7B, n_layers=1)
+    m = L.pcref_model_create(json.dumps(cfg).encode())
+    past = L.pcref_kv_synthetic(1, cfg["hidden"], P, 12345)
+    tf, tc = [], []
+    for _ in range(reps):
+        a, b = C.c_double(), C.c_double()
+        rc = L.pcref_time_cached_step(m, past, n_s, P, C.byref(a), C.byref(b))
+        if rc:
+            raise RuntimeError(L.pcref_last_error().decode())
+        tf.append(a.value)
+        tc.append(b.value)
+    L.pcref_kv_destroy(past)
+    L.pcref_model_destroy(m)
+    return statistics.median(tf), statistics.median(tc)
+
+
+def _ref_extrapolate(t_forward: float, t_concat: float, n_s: int, P: int, n: int, L: int = 32) -> float:
+    """Full-request reference time from the 1-layer sample by exact MAC scaling (all of the reference's
+    forward is fp64-accumulated dot products at one rate): the sample's MACs are n_s rows through one
+    layer (12 d^2 + attention over P + row) plus unembed of n_s rows; the request is n rows through L
+    layers plus unembed of all n rows (the reference computes every row's logits, model.cpp:439-441).
+    Cache copies: concat_kv + assemble_working each copy the whole cached KV (engine.cpp:236, 253)."""
+    d, V = CFG_7B["hidden"], CFG_7B["vocab_size"]
+
+    def layer_macs(rows, past):
+        return rows * 12 * d * d + sum(2 * (past + i + 1) * d for i in range(rows))
+
+    sample = layer_macs(n_s, P) + n_s * V * d
+    full = L * layer_macs(n, P) + n * V * d
+    return t_forward * full / sample + 2 * L * t_concat
+
+
+def cpu_baseline(n_cached: int, n_uncached: int, n_s: int = 4, reps: int = 2) -> dict:
+    t_f, t_c = _ref_sample(n_s, n_cached, reps)
+    t_req = _ref_extrapolate(t_f, t_c, n_s, n_cached, n_uncached)
+    return {"value": 1.0 / t_req, "unit": "requests/s", "cores": 1, "kind": "reference",
+            "ttft_ms": t_req * 1e3,
+            "sample": (f"oracle/_ref (reference C++, -O3, 1 thread): 1-layer 7B-shape model, concat_kv of a "
+                       f"{n_cached}-row synthetic module + Model::forward of {n_s} suffix tokens over it, median of "
+                       f"{reps}; forward {t_f:.2f}s concat {t_c * 1e3:.0f}ms; extrapolated to 32 layers x "
+                       f"{n_uncached} tokens by MAC count + 2x32 cache copies")}
+
+
+def _worker(args):
+    n_s, P, reps = args
+    return _ref_sample(n_s, P, reps)
+
+
+def run_reference(a) -> None:
+    """--impl reference: the reference's own CPU path on this host, all usable cores (one process each,
+    the reference is single-threaded), W warm-up + K timed steps; a step = every worker timing one
+    bounded sample of the config-2 request."""
+    dist_rank = int(os.environ.get("RANK", "0"))
+    if dist_rank != 0:
+        return
+    import multiprocessing as mp
+    n_cached, n_unc = 4096, 64
+    n_s = 4
+    try:
+        mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+    except (ValueError, OSError):
+        mem_gb = 64
+    workers = max(1, min(os.cpu_count() or 1, int(mem_gb // 4), 16))
+    try:
+        from oracle.oracle import ref_available
+        if not ref_available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference "
+                              "at build time)"}))
+            return
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle import failed: {e}"}))
+        return
+    ctx = mp.get_context("fork")
+    per_step = []
+    t_req_all = []
+    with ctx.Pool(workers) as pool:
+        for step in range(a.warmup + a.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_worker, [(n_s, n_cached, 1)] * workers)
+            wall = time.perf_counter() - t0
+            if step >= a.warmup:
+                per_step.append(wall)
+                t_req_all += [_ref_extrapolate(tf, tc, n_s, n_cached, n_unc) for tf, tc in res]
+    t_req = statistics.median(t_req_all)
+    value = workers / t_req
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": statistics.mean(per_step) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference synthetic_text generator; seeded PCG weights; synthetic past rows)",
+        "config": {"workload": "configs[1]: Llama-2-7B shape, 4096 cached module tokens + 64 uncached, "
+                               "single request per worker", "cached_tokens": n_cached, "uncached_tokens": n_unc},
+        "ttft_ms": t_req * 1e3,
+        "cpu_baseline": {"value": value, "unit": "requests/s", "cores": workers, "kind": "reference",
+                         "sample": f"{workers} processes x [1-layer 7B model: concat_kv({n_cached} rows) + "
+                                   f"forward({n_s} suffix tokens)]; per-request time extrapolated to 32 layers x "
+                                   f"{n_unc} tokens by MAC count + 2x32 cache copies"},
+        "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+def run_ours(a) -> None:
+    D = Dist()
+    import numpy as np
+
+    import paper_2311_04934_b200 as pcb
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    tc_peak = float(peaks.get("bf16_tflops", 1590.0))
+    peak_src = "measured" if peaks else "fallback"
+
+    n_cached, n_unc, n_mod = {"c2": (4096, 64, 1), "c3": (16384, 128, 3)}[a.config]
+    cfg = dict(CFG_7B)
+    if a.config == "c3":
+        cfg["max_position"] = 32768
+    schema_text, prompts = workload(n_cached, n_unc, n_mod)
+    model = pcb.Model(cfg, dtype=pcb.BF16, device=D.local)
+    schema = pcb.Schema.parse(schema_text)
+    store = pcb.ModuleStore(model)
+    t0 = time.perf_counter()
+    store.encode_schema(schema)
+    model.sync()
+    precompute_ms = (time.perf_counter() - t0) * 1e3
+    parsed = [pcb.Prompt.parse(p) for p in prompts]
+
+    # warm-up
+    for i in range(a.warmup):
+        pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1)
+    model.sync()
+
+    # ---- timed region: K cached requests, device-timed (CUDA events via the library profile hooks are
+    # off here; the region is bracketed by barrier + synchronize and timed by events on the model stream)
+    D.barrier()
+    model.sync()
+    launches0 = model.launches
+    ttfts = []
+    with ClockSampler(D.local) as clk:
+        model.timer_start()
+        dev_ms = 0.0
+        for i in range(a.steps):
+            r = pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1)
+            ttfts.append(r.timings["ttft_us"] / 1e3)
+            dev_ms += (r.timings["assemble_us"] + r.timings["prefill_device_us"]) / 1e3
+        region_dev_ms = model.timer_stop()
+    launches = model.launches - launches0
+    region_ms = D.max(region_dev_ms)
+    ttft_mean = D.max(statistics.mean(ttfts))
+    value = D.world * a.steps / (region_ms / 1e3)
+    clocks = clk.summary()
+
+    # ---- e2e: public C ABI on prompt TEXT, host buffers, H2D/D2H inside the timed region
+    D.barrier()
+    model.sync()
+    t1 = time.perf_counter()
+    for i in range(a.steps):
+        r = pcb.serve(store, schema, prompts[i % len(prompts)], max_new_tokens=1)
+        _ = r.output_tokens[0]
+    e2e_s = D.max(time.perf_counter() - t1)
+    e2e_value = D.world * a.steps / e2e_s
+    h2d = n_unc * 4 + n_unc * 4  # token ids + int32 positions staged per request
+    d2h = cfg["vocab_size"] * 4 + 4  # first-token logits row + token id
+
+    # ---- roofline: per kernel class CUDA-event times over K instrumented requests
+    model.set_option("profile", 1)
+    model.profile()
+    for i in range(a.steps):
+        pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1)
+    prof = model.profile()
+    model.set_option("profile", 0)
+    g = prof["gemm"]
+    gemm_ms_step = g["ms"] / a.steps
+    gemm_bytes_step = g["bytes"] / a.steps
+    achieved = gemm_bytes_step / (gemm_ms_step / 1e3) / 1e9
+    classes = {k: {"ms_per_step": v["ms"] / a.steps, "launches_per_step": v["launches"] / a.steps,
+                   "GB_per_step": v["bytes"] / a.steps / 1e9,
+                   "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None,
+                   "TFLOPps": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] else None}
+               for k, v in prof.items()}
+
+    # ---- full prefill comparator (same prompt, use_cache=False)
+    full = []
+    for i in range(max(2, min(a.steps, 3)) + 1):
+        r = pcb.serve(store, schema, parsed[0], max_new_tokens=1, use_cache=False)
+        if i:
+            full.append(r.timings["ttft_us"] / 1e3)
+    full_ms = D.max(statistics.median(full))
+
+    # ---- slow tier (modules in pinned host memory, H2D per request)
+    slow = None
+    if not a.skip_slow:
+        sstore = pcb.ModuleStore(model)
+        sstore.encode_schema(schema, tier=pcb.SLOW)
+        ts = []
+        for i in range(3):
+            r = pcb.serve(sstore, schema, parsed[0], max_new_tokens=1)
+            if i:
+                ts.append(r.timings["ttft_us"] / 1e3)
+        slow = statistics.median(ts)
+        del sstore
+
+    cpu = None
+    if D.rank == 0 and D.world == 1 and not a.skip_cpu:
+        try:
+            cpu = cpu_baseline(n_cached, n_unc)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unavailable": str(e)}
+
+    if D.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": D.world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": region_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference synthetic_text generator; random-init weights from the reference's "
+                    "seeded PCG32 streams)",
+            "config": {"workload": f"configs[{1 if a.config == 'c2' else 2}]: Llama-2-7B shape, {n_cached} cached "
+                                   f"module tokens ({n_mod} module{'s' if n_mod > 1 else ''}) + {n_unc} uncached, "
+                                   "single request per step per GPU, modules resident in HBM",
+                       "model": "llama-2-7b-shape (reference block: LN, MHA, interleaved RoPE, GELU MLP)",
+                       "cached_tokens": n_cached, "uncached_tokens": n_unc, "parallelism": f"dp{D.world}",
+                       "l2": "inputs larger than L2 (12.9 GB weights + 2.1 GB KV per step)"},
+            "ttft_ms": ttft_mean, "full_prefill_ttft_ms": full_ms, "ttft_speedup_vs_full_prefill": full_ms / ttft_mean,
+            "device_ms_per_request": dev_ms / a.steps, "ttft_slow_tier_ms": slow,
+            "precompute_ms": precompute_ms,
+            "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "gemm_tc (tcgen05 swap-AB weight streaming, all GEMMs of a step)",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "alg_bytes_per_step": gemm_bytes_step, "gemm_ms_per_step": gemm_ms_step,
+                         "tensor_peak_tflops": tc_peak},
+            "kernel_classes": classes,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    D.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-slow", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

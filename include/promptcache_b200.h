@@ -70,7 +70,7 @@ int64_t pcb_per_token_bytes(const char* config_json);                    /* cach
 /* ---- model (model.hpp:59-91) ---- */
 int pcb_model_create(const char* config_json, int dtype, int device, pcb_model** out);
 void pcb_model_destroy(pcb_model* m);
-int pcb_model_set_option(pcb_model* m, const char* key, int64_t value);  /* "force_simt" (testing) */
+int pcb_model_set_option(pcb_model* m, const char* key, int64_t value);  /* "force_simt" (testing), "profile" */
 int pcb_model_weight_checksum(pcb_model* m, const char* tensor, uint64_t* out);
 /* Model::forward / forward_masked: logits_out [n][vocab] (host, may be NULL);
  * past may be NULL; mask [n][n] (NULL = causal); new_kv may be NULL. */
@@ -81,6 +81,12 @@ int pcb_model_generate(pcb_model* m, pcb_kv* kv, int32_t last_token, int64_t las
                        int32_t* out);
 int64_t pcb_model_forward_tokens(const pcb_model* m);
 int64_t pcb_model_launches(const pcb_model* m);   /* kernels launched by this model so far */
+/* with option "profile"=1: per kernel class {gemm, attention, assembly, other} CUDA-event
+ * milliseconds, launch counts and algorithmic bytes / flops since the last call (resets) */
+char* pcb_model_profile_json(pcb_model* m);
+/* device timer on the model's stream: stop=0 records the start event; stop=1 records the end event,
+ * waits for it and returns the elapsed device milliseconds */
+int pcb_model_timer(pcb_model* m, int stop, double* ms_out);
 int pcb_model_sync(pcb_model* m);
 
 /* ---- KV blocks (model.hpp:34-44) ---- */

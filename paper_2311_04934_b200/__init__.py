@@ -74,6 +74,7 @@ def lib():
         "pcb_model_forward": (i32, [vp, vp, vp, i64, vp, vp, vp, pvp]),
         "pcb_model_generate": (i32, [vp, vp, i32, i64, i32, vp]),
         "pcb_model_forward_tokens": (i64, [vp]), "pcb_model_launches": (i64, [vp]),
+        "pcb_model_profile_json": (vp, [vp]), "pcb_model_timer": (i32, [vp, i32, C.POINTER(C.c_double)]),
         "pcb_model_sync": (i32, [vp]),
         "pcb_kv_rows": (i64, [vp]), "pcb_kv_positions": (i32, [vp, vp]),
         "pcb_kv_read": (i32, [vp, i32, i32, vp]), "pcb_kv_upload": (i32, [vp, vp, vp, vp, i64, pvp]),
@@ -291,6 +292,20 @@ class Model(_Handle):
     @property
     def forward_tokens(self) -> int:
         return int(lib().pcb_model_forward_tokens(self._h))
+
+    def profile(self) -> dict:
+        """Per kernel class CUDA-event times since the last call (needs set_option("profile", 1))."""
+        return json.loads(_take_str(lib().pcb_model_profile_json(self._h)))
+
+    def timer_start(self):
+        """Record a CUDA event on the model's stream (device-side timing of a region)."""
+        _check(lib().pcb_model_timer(self._h, 0, None))
+
+    def timer_stop(self) -> float:
+        """Record the end event, wait for it; returns device milliseconds since timer_start()."""
+        ms = C.c_double()
+        _check(lib().pcb_model_timer(self._h, 1, C.byref(ms)))
+        return ms.value
 
     @property
     def launches(self) -> int:

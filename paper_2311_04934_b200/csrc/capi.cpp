@@ -139,6 +139,7 @@ void pcb_model_destroy(pcb_model* m) { delete m; }
 int pcb_model_set_option(pcb_model* m, const char* key, int64_t v) {
   return guard([&] {
     if (std::strcmp(key, "force_simt") == 0) m->m->force_simt = v != 0;
+    else if (std::strcmp(key, "profile") == 0) m->m->set_profiling(v != 0);
     else throw Error(ErrorCode::InvalidConfig, std::string("unknown option ") + key);
   });
 }
@@ -176,6 +177,25 @@ int pcb_model_generate(pcb_model* m, pcb_kv* kv, int32_t last_token, int64_t las
 }
 int64_t pcb_model_forward_tokens(const pcb_model* m) { return m->m->forward_tokens.load(); }
 int64_t pcb_model_launches(const pcb_model* m) { return m->m->launches; }
+char* pcb_model_profile_json(pcb_model* m) { return guard_str([&] { return m->m->profile_json(); }); }
+int pcb_model_timer(pcb_model* m, int stop, double* ms_out) {
+  return guard([&] {
+    static thread_local cudaEvent_t a = nullptr, b = nullptr;
+    if (!a) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    }
+    if (!stop) {
+      if (cudaEventRecord(a, m->m->stream()) != cudaSuccess) throw Error(ErrorCode::CudaError, "event record");
+      return;
+    }
+    cudaEventRecord(b, m->m->stream());
+    cudaEventSynchronize(b);
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) throw Error(ErrorCode::CudaError, "event elapsed");
+    if (ms_out) *ms_out = ms;
+  });
+}
 int pcb_model_sync(pcb_model* m) {
   return guard([&] {
     cudaError_t e = cudaStreamSynchronize(m->m->stream());

@@ -177,8 +177,11 @@ int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model
     const uint64_t chunks = kern::assemble_plan(sc.h_segs, n_segs, sc.h_first);
     CK(cudaMemcpyAsync(sc.d_segs, sc.h_segs, n_segs * sizeof(kern::CopySeg), cudaMemcpyHostToDevice, m.stream()));
     CK(cudaMemcpyAsync(sc.d_first, sc.h_first, n_segs * sizeof(uint64_t), cudaMemcpyHostToDevice, m.stream()));
+    double bytes = 0;
+    for (int i = 0; i < n_segs; ++i) bytes += 2.0 * sc.h_segs[i].bytes;  // read + write
+    m.prof_begin();
     kern::assemble(sc.d_segs, sc.d_first, n_segs, chunks, m.stream());
-    m.launches += 1;
+    m.prof_end(model::Model::PROF_ASM, bytes, 0);
   }
   return slow;
 }

@@ -303,6 +303,79 @@ Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtyp
   CK(cudaStreamSynchronize(stream_));
 }
 
+struct Model::Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct Rec {
+    int cat;
+    cudaEvent_t a, b;
+    double bytes, flops;
+  };
+  std::vector<Rec> recs;
+  cudaEvent_t pending = nullptr;
+  double ms[PROF_N] = {}, bytes[PROF_N] = {}, flops[PROF_N] = {};
+  int64_t count[PROF_N] = {};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
+};
+
+void Model::set_profiling(bool on) {
+  if (!prof_) prof_ = std::make_unique<Prof>();
+  prof_->on = on;
+}
+void Model::prof_begin() {
+  if (!prof_ || !prof_->on) return;
+  prof_->pending = prof_->get();
+  CK(cudaEventRecord(prof_->pending, stream_));
+}
+void Model::prof_end(int cat, double alg_bytes, double alg_flops) {
+  ++launches;
+  if (!prof_ || !prof_->on || !prof_->pending) return;
+  cudaEvent_t b = prof_->get();
+  CK(cudaEventRecord(b, stream_));
+  prof_->recs.push_back({cat, prof_->pending, b, alg_bytes, alg_flops});
+  prof_->pending = nullptr;
+}
+std::string Model::profile_json() {
+  nlohmann::json j = nlohmann::json::object();
+  if (!prof_) return j.dump();
+  CK(cudaStreamSynchronize(stream_));
+  for (auto& r : prof_->recs) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    prof_->ms[r.cat] += ms;
+    prof_->bytes[r.cat] += r.bytes;
+    prof_->flops[r.cat] += r.flops;
+    prof_->count[r.cat] += 1;
+    prof_->pool.push_back(r.a);
+    prof_->pool.push_back(r.b);
+  }
+  prof_->recs.clear();
+  const char* names[PROF_N] = {"gemm", "attention", "assembly", "other"};
+  for (int c = 0; c < PROF_N; ++c) {
+    j[names[c]] = {{"ms", prof_->ms[c]}, {"launches", prof_->count[c]}, {"bytes", prof_->bytes[c]},
+                   {"flops", prof_->flops[c]}};
+    prof_->ms[c] = prof_->bytes[c] = prof_->flops[c] = 0;
+    prof_->count[c] = 0;
+  }
+  return j.dump();
+}
+
 Model::~Model() {
   if (stream_) {
     cudaStreamSynchronize(stream_);
@@ -360,11 +433,15 @@ void Model::validate(const int32_t* tokens, const int64_t* positions, int64_t n,
 
 void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi) {
   const auto& e = *static_cast<const kern::Epilogue*>(epi);
+  prof_begin();
   if (dtype_ == BF16 && !force_simt && kern::gemm_tc_supported(M, N, K))
     kern::gemm_tc(A, W, M, N, K, e, ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->counters, stream_);
   else
     kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_);
-  ++launches;
+  // algorithmic bytes: weights + activations in + outputs (residual: read + write fp32)
+  const double es = dtype_ == F32 ? 4.0 : 2.0;
+  const double out_b = e.kind == kern::EPI_RESID ? 8.0 : (e.kind == kern::EPI_F32 ? 4.0 : es);
+  prof_end(PROF_GEMM, (double)N * K * es + (double)M * K * es + (double)M * N * out_b, 2.0 * M * N * K);
 }
 
 void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBlock& kv, const uint8_t* mask,
@@ -381,6 +458,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
   const auto& c = cfg_;
   const int d = c.hidden, H = c.n_heads, hd = c.head_dim;
   const int64_t P = kv.rows, total = P + n;
+  const double es = dtype_ == F32 ? 4.0 : 2.0;
   Workspace& W = *ws_;
   W.ensure(n, total, logit_rows, mask != nullptr);
   cudaStream_t s = stream_;
@@ -407,8 +485,9 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     CK(cudaMemcpyAsync(W.block, bp, n * 4, cudaMemcpyHostToDevice, s));
   }
 
+  prof_begin();
   kern::embed(W.tok, W.pos, n, w_->embed, w_->abs_table, d, W.h, s);
-  launches += 1;
+  prof_end(PROF_OTHER, 8.0 * n * d, 0);
 
   kern::AttnArgs aa;
   aa.n = n;
@@ -434,7 +513,9 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
   }
 
   for (int l = 0; l < c.n_layers; ++l) {
+    prof_begin();
     kern::layernorm(dtype_, W.h, n, d, W.x, s);
+    prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
     kern::Epilogue e;
     e.kind = kern::EPI_QKV;
     e.d = d;
@@ -453,16 +534,22 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
 
     aa.k = kv.k(l);
     aa.v = kv.v(l);
+    // algorithmic work: every visible key/value row read once, q in, out written
+    const double attn_bytes = 2.0 * total * d * es + 2.0 * n * d * es;
+    const double attn_flops = 4.0 * (double)n * d * (mask || block_ids || P == 0 ? (total + 1) / 2.0 : (P + (n + 1) / 2.0));
     if (tc_attn) {
+      prof_begin();
       kern::attention_tc(aa, W.attn_scratch, W.attn_scratch_bytes, s);
-      ++launches;
+      prof_end(PROF_ATTN, attn_bytes, attn_flops);
     } else {
+      prof_begin();
       for (int64_t i0 = 0; i0 < n; i0 += nq) {
         aa.i0 = i0;
         aa.nq = std::min(nq, n - i0);
         kern::attention_simt(dtype_, aa, W.attn_scratch, s);
-        ++launches;
+        if (i0 + nq < n) ++launches;
       }
+      prof_end(PROF_ATTN, attn_bytes, attn_flops);
       aa.i0 = 0;
       aa.nq = -1;
     }
@@ -471,23 +558,25 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     eo.kind = kern::EPI_RESID;
     eo.resid = W.h;
     gemm(W.attn, w_->wo[l], n, d, d, &eo);
+    prof_begin();
     kern::layernorm(dtype_, W.h, n, d, W.x, s);
+    prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
     kern::Epilogue eg;
     eg.kind = kern::EPI_GELU;
     eg.out = W.mid;
     gemm(W.x, w_->w1[l], n, 4 * d, d, &eg);
     gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo);
-    launches += 2;
   }
   if (logit_rows > 0) {
     const int64_t r0 = n - logit_rows;
+    prof_begin();
     kern::layernorm(dtype_, W.h + r0 * d, logit_rows, d, W.x, s);
+    prof_end(PROF_OTHER, (4.0 + es) * logit_rows * d, 0);
     kern::Epilogue ef;
     ef.kind = kern::EPI_F32;
     ef.outf = W.logits;
     ef.ldo = c.vocab_size;
     gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
-    launches += 1;
   }
   kv.rows = total;
   kv.positions.insert(kv.positions.end(), positions, positions + n);
@@ -497,8 +586,9 @@ const float* Model::device_logits() const { return ws_->logits; }
 int32_t* Model::device_argmax() const { return ws_->argmax; }
 
 void Model::argmax_last(int64_t logit_rows) {
+  prof_begin();
   kern::argmax_rows(ws_->logits, logit_rows, cfg_.vocab_size, ws_->argmax, stream_);
-  ++launches;
+  prof_end(PROF_OTHER, 4.0 * logit_rows * cfg_.vocab_size, 0);
 }
 
 // ---------------------------------------------------------------------------

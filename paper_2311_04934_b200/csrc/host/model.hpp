@@ -114,6 +114,13 @@ class Model {
   void copy_rows(const KVBlock& src, KVBlock& dst, int64_t dst_row) const;
   KVPtr to_host(const KVBlock& src) const;  // pinned host copy (slow tier)
 
+  // ---- live per-kernel-class timing (CUDA events on the model stream) ----
+  enum ProfCat { PROF_GEMM = 0, PROF_ATTN = 1, PROF_ASM = 2, PROF_OTHER = 3, PROF_N = 4 };
+  void set_profiling(bool on);
+  void prof_begin();
+  void prof_end(int cat, double alg_bytes, double alg_flops);
+  std::string profile_json();  // syncs, returns per-class {ms, launches, bytes, flops}, resets
+
   mutable std::atomic<long> forward_tokens{0};
   bool force_simt = false;       // testing: route bf16 GEMM/attention through SIMT kernels
   int64_t launches = 0;          // kernels launched by run() (bench evidence)
@@ -127,6 +134,8 @@ class Model {
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Weights> w_;
   std::unique_ptr<Workspace> ws_;
+  struct Prof;
+  std::unique_ptr<Prof> prof_;
 };
 
 int argmax_lowest(const float* logits, int n);

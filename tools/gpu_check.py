@@ -101,3 +101,24 @@ def _():
         m.set_option("force_simt", 1)
         b, _ = m.forward(t, p)
         print(f"   M={M} rel {np.abs(a - b).max() / np.abs(b).max():.3e}")
+
+
+@section("7B-shape attention tc vs simt (1 layer)")
+def _():
+    cfg = dict(n_layers=1, n_heads=32, head_dim=128, hidden=4096, vocab_size=32000, pos_encoding="rope",
+               max_position=8192, bytes_per_element=2, seed=42)
+    m = pcb.Model(cfg, dtype=pcb.BF16)
+    t = rng.integers(0, 259, 4160)
+    p = np.arange(4160)
+    res = {}
+    for force in (0, 1):
+        m.set_option("force_simt", force)
+        a, kv = m.forward(t[:4096], p[:4096])
+        b, _ = m.forward(t[4096:], p[4096:], past=kv)
+        c, _ = m.forward(t[4096:4097], p[4096:4097], past=kv)
+        d, _ = m.forward(t[:200], p[:200])
+        res[force] = (a, b, c, d)
+    for i, nm in enumerate(["prefill4096", "suffix64", "suffix1", "prefill200"]):
+        x, y = res[0][i], res[1][i]
+        print(f"   {nm}: rel {np.abs(x - y).max() / np.abs(y).max():.3e} argmax_eq "
+              f"{(x.argmax(-1) == y.argmax(-1)).mean():.3f}")
