@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <functional>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -200,6 +201,76 @@ int pcb_model_sync(pcb_model* m) {
   return guard([&] {
     cudaError_t e = cudaStreamSynchronize(m->m->stream());
     if (e != cudaSuccess) throw Error(ErrorCode::CudaError, cudaGetErrorString(e));
+  });
+}
+
+// ---- kernel microbenchmarks (tuning aid; random bf16 operands on the device) ----
+int pcb_debug_kernel_bench(const char* which, int64_t a0, int64_t a1, int64_t a2, int iters, double* us_out) {
+  return guard([&] {
+    cudaStream_t s;
+    cudaStreamCreate(&s);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<void*> bufs;
+    auto alloc = [&](size_t bytes) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) throw Error(ErrorCode::CudaError, "bench alloc");
+      bufs.push_back(p);
+      return p;
+    };
+    std::function<void()> run;
+    float* ws = static_cast<float*>(alloc(64ull << 20));
+    int* ctr = static_cast<int*>(alloc(65536 * 4));
+    cudaMemset(ctr, 0, 65536 * 4);
+    if (std::strcmp(which, "gemm") == 0) {  // a0 = M tokens, a1 = N, a2 = K
+      void* X = alloc(a0 * a2 * 2);
+      void* W = alloc(a1 * a2 * 2);
+      float* R = static_cast<float*>(alloc(a0 * a1 * 4));
+      kern::init_uniform(kern::BF16, X, a0 * a2, 1, 1.0f, s);
+      kern::init_uniform(kern::BF16, W, a1 * a2, 2, 0.02f, s);
+      kern::Epilogue e;
+      e.kind = std::getenv("PCB_GEMM_EPI_NONE") ? kern::EPI_NONE : kern::EPI_RESID;
+      e.resid = R;
+      run = [=] { kern::gemm_tc(X, W, a0, static_cast<int>(a1), static_cast<int>(a2), e, ws, 64ull << 20, ctr, s); };
+    } else if (std::strcmp(which, "attn") == 0) {  // a0 = n queries, a1 = P past, a2 = heads (hd 128)
+      const int H = static_cast<int>(a2), d = H * 128;
+      const int64_t tot = a0 + a1;
+      void* q = alloc(a0 * d * 2);
+      void* k = alloc(tot * d * 2);
+      void* v = alloc(tot * d * 2);
+      void* o = alloc(a0 * d * 2);
+      kern::init_uniform(kern::BF16, q, a0 * d, 3, 1.0f, s);
+      kern::init_uniform(kern::BF16, k, tot * d, 4, 1.0f, s);
+      kern::init_uniform(kern::BF16, v, tot * d, 5, 1.0f, s);
+      kern::AttnArgs a;
+      a.q = q;
+      a.k = k;
+      a.v = v;
+      a.out = o;
+      a.n = a0;
+      a.P = a1;
+      a.H = H;
+      a.hd = 128;
+      a.d = d;
+      run = [=] { kern::attention_tc(a, ws, 64ull << 20, s); };
+    } else {
+      throw Error(ErrorCode::InvalidConfig, "unknown kernel bench");
+    }
+    for (int i = 0; i < 3; ++i) run();
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < iters; ++i) run();
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *us_out = ms * 1000.0 / iters;
+    cudaError_t err = cudaGetLastError();
+    for (void* p : bufs) cudaFree(p);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    if (err != cudaSuccess) throw Error(ErrorCode::CudaError, cudaGetErrorString(err));
   });
 }
 

@@ -112,6 +112,7 @@ struct Weights {
   float *cos32 = nullptr, *sin32 = nullptr;
   float* alibi = nullptr;
   float* abs_table = nullptr;
+  bool packed = false;  // bf16 GEMM weights in the tcgen05 tile layout
   std::vector<void*> owned;
   ~Weights() {
     for (void* p : owned) cudaFree(p);
@@ -236,24 +237,35 @@ Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtyp
   // weight init (reference model.cpp:191-218): same tensor names, scales, streams
   w_->embed = static_cast<float*>(w_->alloc(Vd * 4));
   kern::init_uniform(F32, w_->embed, Vd, stream_seed("embed", c.seed), 0.1f, stream_);
-  w_->unembed = w_->alloc(Vd * es);
-  kern::init_uniform(dtype, w_->unembed, Vd, stream_seed("unembed", c.seed), ws, stream_);
-  const size_t dd = static_cast<size_t>(d) * d;
+  // bf16 GEMM weights are stored pre-packed for the tcgen05 kernel (kernels.cuh
+  // packed_index); fp32 weights stay row-major for the exact SIMT path.
+  w_->packed = dtype == BF16 && kern::weight_packable(3 * d, d) && kern::weight_packable(4 * d, d) &&
+               kern::weight_packable(d, 4 * d) && kern::weight_packable(c.vocab_size, d);
+  void* staging = nullptr;
+  if (w_->packed) CK(cudaMalloc(&staging, std::max<size_t>(4 * static_cast<size_t>(d) * d, Vd) * es));
+  // generate the fp32 stream of each named part into rows [row0, row0 + rows) of an [N][K] matrix
+  auto make = [&](int N, int K, std::initializer_list<std::pair<std::string, float>> parts) {
+    void* dst = w_->alloc(static_cast<size_t>(N) * K * es);
+    char* gen = static_cast<char*>(w_->packed ? staging : dst);
+    const size_t part = static_cast<size_t>(N) * K / parts.size();
+    size_t off = 0;
+    for (auto& [name, scale] : parts) {
+      kern::init_uniform(dtype, gen + off * es, part, stream_seed(name, c.seed), scale, stream_);
+      off += part;
+    }
+    if (w_->packed) kern::pack_weight_bf16(staging, dst, N, K, stream_);
+    return dst;
+  };
+  w_->unembed = make(c.vocab_size, d, {{"unembed", ws}});
   for (int l = 0; l < c.n_layers; ++l) {
-    char* qkv = static_cast<char*>(w_->alloc(3 * dd * es));
-    kern::init_uniform(dtype, qkv, dd, stream_seed(tname(l, "wq"), c.seed), ws, stream_);
-    kern::init_uniform(dtype, qkv + dd * es, dd, stream_seed(tname(l, "wk"), c.seed), ws, stream_);
-    kern::init_uniform(dtype, qkv + 2 * dd * es, dd, stream_seed(tname(l, "wv"), c.seed), ws, stream_);
-    w_->wqkv.push_back(qkv);
-    void* wo = w_->alloc(dd * es);
-    kern::init_uniform(dtype, wo, dd, stream_seed(tname(l, "wo"), c.seed), ws, stream_);
-    w_->wo.push_back(wo);
-    void* w1 = w_->alloc(4 * dd * es);
-    kern::init_uniform(dtype, w1, 4 * dd, stream_seed(tname(l, "w1"), c.seed), ws, stream_);
-    w_->w1.push_back(w1);
-    void* w2 = w_->alloc(4 * dd * es);
-    kern::init_uniform(dtype, w2, 4 * dd, stream_seed(tname(l, "w2"), c.seed), ws2, stream_);
-    w_->w2.push_back(w2);
+    w_->wqkv.push_back(make(3 * d, d, {{tname(l, "wq"), ws}, {tname(l, "wk"), ws}, {tname(l, "wv"), ws}}));
+    w_->wo.push_back(make(d, d, {{tname(l, "wo"), ws}}));
+    w_->w1.push_back(make(4 * d, d, {{tname(l, "w1"), ws}}));
+    w_->w2.push_back(make(d, 4 * d, {{tname(l, "w2"), ws2}}));
+  }
+  if (staging) {
+    CK(cudaStreamSynchronize(stream_));
+    cudaFree(staging);
   }
   if (c.pos_encoding == PosEncoding::Rope) {  // model.cpp:220-230, glibc fp64 table
     const int half = c.head_dim / 2;
@@ -434,10 +446,10 @@ void Model::validate(const int32_t* tokens, const int64_t* positions, int64_t n,
 void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi) {
   const auto& e = *static_cast<const kern::Epilogue*>(epi);
   prof_begin();
-  if (dtype_ == BF16 && !force_simt && kern::gemm_tc_supported(M, N, K))
+  if (w_->packed && !force_simt && kern::gemm_tc_supported(M, N, K))
     kern::gemm_tc(A, W, M, N, K, e, ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->counters, stream_);
   else
-    kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_);
+    kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_, w_->packed);
   // algorithmic bytes: weights + activations in + outputs (residual: read + write fp32)
   const double es = dtype_ == F32 ? 4.0 : 2.0;
   const double out_b = e.kind == kern::EPI_RESID ? 8.0 : (e.kind == kern::EPI_F32 ? 4.0 : es);

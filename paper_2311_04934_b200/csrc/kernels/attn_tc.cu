@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tO = tmem + BKV;
+  pdl_trigger();
+  pdl_wait();  // Q/K/V come from the QKV GEMM (and assembly) just before
 
   if (warp == 0) {
     if (elect_one() && nb > 0) {
@@ -245,6 +247,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 // Merge split partials in split order: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
 template <int HD>
 __global__ void k_attn_combine(AttnParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t qi = blockIdx.x;
   const int h = blockIdx.y, x = threadIdx.x;
   float M = -INFINITY;
@@ -311,11 +315,9 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   CUtensorMap tk = tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
   CUtensorMap tv = tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
   dim3 grid(q_tiles, a.H, splits);
-  k_attn_tc<HD><<<grid, kAttnThreads, Sm::kBytes, s>>>(tq, tk, tv, p);
-  PCB_CUDA(cudaGetLastError());
+  launch_k(k_attn_tc<HD>, grid, dim3(kAttnThreads), Sm::kBytes, s, 1, tq, tk, tv, p);
   if (splits > 1) {
-    k_attn_combine<HD><<<dim3(static_cast<unsigned>(a.n), a.H), HD, 0, s>>>(p);
-    PCB_CUDA(cudaGetLastError());
+    launch_k(k_attn_combine<HD>, dim3(static_cast<unsigned>(a.n), a.H), dim3(HD), 0, s, 1, p);
   }
 }
 

@@ -4,8 +4,10 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "kernels.cuh"
 
@@ -31,6 +33,47 @@ __device__ __forceinline__ float gelu_ref(float xf) {
   double x3 = __dmul_rn(__dmul_rn(__dmul_rn(0.044715, x), x), x);
   double t = __dmul_rn(0.7978845608028654, __dadd_rn(x, x3));
   return (float)__dmul_rn(__dmul_rn(0.5, x), __dadd_rn(1.0, tanh(t)));
+}
+
+// ---- programmatic dependent launch (PDL) ----
+// Every kernel of the forward chain is launched with programmatic stream
+// serialization: it may start (barrier init, TMEM alloc, weight prefetch) while
+// its predecessor drains, and calls pdl_wait() before touching memory the
+// predecessor produces (or that an earlier kernel still reads).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PCB_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster_z,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[na].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  ++na;
+  if (cluster_z > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = cluster_z;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 __device__ __forceinline__ float gelu_fast(float x) {

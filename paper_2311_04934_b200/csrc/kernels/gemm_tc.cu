@@ -1,18 +1,26 @@
 // tcgen05 GEMM for the bf16 hot path: C[m][n] = sum_k X[m][k] * W[n][k] with
 // the epilogue fused (RoPE + K/V cache write, residual add, GELU, fp32 logits).
 //
-// Orientation ("swap AB"): the weight tile is the MMA A operand (M = 128 weight
-// rows per CTA) and the token tile the B operand (N = BN tokens), so a 64-token
-// suffix still issues full-height 128xBNx16 UMMAs and the kernel streams weights
-// — the HBM-bound quantity at small token counts.
-//   warp 0     TMA producer (one elected lane): W tile [128 x 64] + X tile [BN x 64]
+// Design (B200-first):
+//  * Weights live in HBM pre-packed as 128x64 bf16 tiles, each tile stored as the
+//    exact 128-byte-swizzled shared-memory image the UMMA descriptor expects, tiles
+//    of one 128-row block contiguous along K.  A tile is one 16 KB cp.async.bulk:
+//    the weight stream is a handful of long sequential reads per SM.
+//  * "Swap AB": the weight tile is the MMA A operand (M = 128 weight rows), the
+//    token tile the B operand (N = BN tokens), so a 64-token suffix still issues
+//    full-height 128xBNx16 UMMAs.
+//  * Persistent stream-K: one CTA per SM; the (tile, k-block) units are split into
+//    equal contiguous ranges, so every SM streams the same number of weight bytes
+//    (the HBM-bound quantity at small token counts).  A tile cut
+//    between CTAs is finished by the CTA holding its last k-block, which adds the
+//    other CTAs' fp32 partials in CTA order (deterministic) before the epilogue.
+//  * Two TMEM accumulators: the epilogue of one tile overlaps the MMAs of the next.
+//   warp 0     producer: W tile (bulk copy) + X tile (TMA 2-D) per k-block
 //   warp 1     TMEM allocator + MMA issuer (one elected lane)
 //   warps 2-5  epilogue: tcgen05.ld (lane = weight row, column = token) -> fused op
-// Split-K over CTAs fills all 148 SMs when (N/128) x token tiles is small; the
-// partial sums meet in an L2-resident workspace and the last-arriving CTA of a
-// tile adds them in split order (deterministic) before running the epilogue.
 #include <cuda.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -67,23 +75,64 @@ CUtensorMap tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// Epilogue on one thread's weight row n for 16 consecutive tokens.
+// Weight packing: row-major [N][K] bf16 -> tiles [N/128][K/64] of 16 KB, each the
+// SW128 K-major smem image (row r at r*128 B, 16-byte chunk c at (c ^ (r & 7))).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void epi_chunk(const Epilogue& e, int n, int N, int64_t m0, int64_t M, float* v) {
+__host__ __device__ inline uint64_t packed_offset_bytes(int n, int k, int K) { return packed_index(n, k, K) * 2; }
+
+__global__ void k_pack(const uint4* __restrict__ src, uint8_t* __restrict__ dst, int N, int K) {
+  const int64_t chunks = static_cast<int64_t>(N) * (K / 8);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = static_cast<int>(i / (K / 8)), k = static_cast<int>(i % (K / 8)) * 8;
+    *reinterpret_cast<uint4*>(dst + packed_offset_bytes(n, k, K)) = src[i];
+  }
+}
+
+bool weight_packable(int N, int K) { return N % 128 == 0 && K % 64 == 0 && K >= 64; }
+
+void pack_weight_bf16(const void* src, void* dst, int N, int K, cudaStream_t s) {
+  k_pack<<<592, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint8_t*>(dst), N, K);
+  PCB_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Epilogue on one thread's weight row n for 16 consecutive tokens [m0, m0+16),
+// split into a prefetch (global loads that do not depend on the accumulator:
+// residual rows, RoPE cos/sin) and the apply step, so the loads of the next
+// chunk are in flight while the current one is processed.
+// ---------------------------------------------------------------------------
+struct EpiPre {
+  float a[16], b[16];
+};
+
+__device__ __forceinline__ void epi_prefetch(const Epilogue& e, int n, int N, int64_t m0, int64_t M, EpiPre& p) {
+  if (e.kind == EPI_RESID) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) p.a[j] = (m0 + j < M) ? e.resid[(m0 + j) * N + n] : 0.f;
+  } else if (e.kind == EPI_QKV) {
+    const int seg = n / e.d, c = n - seg * e.d;
+    if (seg < 2 && e.rope) {
+      const int half = e.head_dim >> 1, pi = (c % e.head_dim) >> 1;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int64_t pos = (m0 + j < M) ? e.pos[m0 + j] : 0;
+        p.a[j] = e.rope_cos32[pos * half + pi];
+        p.b[j] = e.rope_sin32[pos * half + pi];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_chunk(const Epilogue& e, int n, int N, int64_t m0, int64_t M, float* v,
+                                          const EpiPre& pre) {
   if (e.kind == EPI_QKV) {
     const int seg = n / e.d, c = n - seg * e.d;
     const bool rot = seg < 2 && e.rope;
-    const int half = e.head_dim >> 1, pi = (c % e.head_dim) >> 1;
     const bool odd = c & 1;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       float pv = __shfl_xor_sync(0xffffffffu, v[j], 1);  // partner column n^1 lives in lane^1
-      int64_t m = m0 + j;
-      if (rot && m < M) {
-        int64_t p = e.pos[m];
-        float cs = e.rope_cos32[p * half + pi], sn = e.rope_sin32[p * half + pi];
-        v[j] = odd ? (pv * sn + v[j] * cs) : (v[j] * cs - pv * sn);
-      }
+      if (rot) v[j] = odd ? (pv * pre.b[j] + v[j] * pre.a[j]) : (v[j] * pre.a[j] - pv * pre.b[j]);
     }
     __nv_bfloat16* dst = seg == 0 ? static_cast<__nv_bfloat16*>(e.q_out)
                                   : static_cast<__nv_bfloat16*>(seg == 1 ? e.k_out : e.v_out) + e.kv_row0 * e.d;
@@ -92,12 +141,13 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int n, int N, int64
       if (m0 + j < M) dst[(m0 + j) * e.d + c] = __float2bfloat16_rn(v[j]);
     return;
   }
+  if (e.kind == EPI_NONE) return;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int64_t m = m0 + j;
     if (m >= M) break;
     if (e.kind == EPI_RESID) {
-      e.resid[m * N + n] += v[j];
+      e.resid[m * N + n] = pre.a[j] + v[j];
     } else if (e.kind == EPI_GELU) {
       static_cast<__nv_bfloat16*>(e.out)[m * N + n] = __float2bfloat16_rn(gelu_fast(v[j]));
     } else {
@@ -106,173 +156,271 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int n, int N, int64
   }
 }
 
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 constexpr int kThreads = 192;
+constexpr int kWTile = 128 * 64 * 2;  // one packed weight tile
 
 template <int BN, int STAGES>
-struct GemmSmem {
-  static constexpr int kA = 128 * 64 * 2;  // weight tile
-  static constexpr int kB = BN * 64 * 2;   // token tile
-  static constexpr int kStage = kA + kB;
-  static constexpr int kBytes = STAGES * kStage + 1024 /*barriers*/ + 1024 /*align*/;
+struct SkSmem {
+  static constexpr int kStage = kWTile + BN * 128;
+  static constexpr int kBytes = STAGES * kStage + 1024 + 1024;
+  static constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
 };
+
+struct SkArgs {
+  const uint8_t* w;  // packed weights
+  int64_t M;
+  int N, K, kbs, m_tiles;
+  int64_t units;
+  int epoch;
+  float* ws;  // [gridDim.x][128][BN] partial tiles
+  int* flags; // [gridDim.x] epoch flags
+  const uint8_t* x_bulk_probe = nullptr;
+};
+
+__device__ __forceinline__ int64_t unit_begin(int c, int64_t U, int C) { return static_cast<int64_t>(c) * U / C; }
+
+// CTA whose unit range contains unit g
+__device__ __forceinline__ int cta_of(int64_t g, int64_t U, int C) {
+  int c = static_cast<int>((g * C) / U);
+  while (c + 1 < C && unit_begin(c + 1, U, C) <= g) ++c;
+  while (c > 0 && unit_begin(c, U, C) > g) --c;
+  return c;
+}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int64_t M, int N,
-              int K, int splits, Epilogue e, float* __restrict__ ws, int* __restrict__ counters) {
-  using S = GemmSmem<BN, STAGES>;
+    k_gemm_sk(const __grid_constant__ CUtensorMap tmX, SkArgs a, Epilogue e) {
+  using S = SkSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
-  const int n0 = n_tile * 128;
-  const int64_t m0 = static_cast<int64_t>(m_tile) * BN;
-  const int total_kb = K / 64;
-  const int kb0 = static_cast<int>(static_cast<int64_t>(split) * total_kb / splits);
-  const int kb1 = static_cast<int>(static_cast<int64_t>(split + 1) * total_kb / splits);
-  constexpr uint32_t kCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  const int C = gridDim.x, c = blockIdx.x;
+  const int64_t g0 = unit_begin(c, a.units, C), g1 = unit_begin(c + 1, a.units, C);
+  const int kbs = a.kbs;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmW);
     tma_prefetch(&tmX);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kCols);
+  if (warp == 1) tmem_alloc(tmem_slot, S::kCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream once
       const uint64_t pol_x = policy_evict_last();   // activations are re-read by every CTA
-      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+      auto w_src = [&](int64_t g) {
+        const int64_t t = g / kbs;
+        const int kb = static_cast<int>(g - t * kbs);
+        const int n_tile = static_cast<int>(t / a.m_tiles);
+        return a.w + (static_cast<int64_t>(n_tile) * kbs + kb) * kWTile;
+      };
+      auto x_coords = [&](int64_t g, int& kx, int& my) {
+        const int64_t t = g / kbs;
+        kx = static_cast<int>(g - t * kbs) * 64;
+        my = static_cast<int>(t % a.m_tiles) * BN;
+      };
+      // Weights do not depend on the previous kernel: start streaming them before
+      // waiting on it (programmatic dependent launch), then the activations.
+      const int pre = static_cast<int>((g1 - g0) < STAGES ? (g1 - g0) : STAGES);
+      for (int it = 0; it < pre; ++it) {
+        mbar_expect_tx(&full[it], S::kStage);
+        bulk_load(smem + it * S::kStage, w_src(g0 + it), kWTile, &full[it], pol_w);
+      }
+      pdl_wait();
+      for (int it = 0; it < pre; ++it) {
+        int kx, my;
+        x_coords(g0 + it, kx, my);
+        tma_load_2d_hint(smem + it * S::kStage + kWTile, &tmX, &full[it], kx, my, pol_x);
+      }
+      int it = pre;
+      for (int64_t g = g0 + pre; g < g1; ++g, ++it) {
         const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * S::kStage;
+        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * S::kStage;
         mbar_expect_tx(&full[s], S::kStage);
-        tma_load_2d_hint(sa, &tmW, &full[s], kb * 64, n0, pol_w);
-        tma_load_2d_hint(sa + S::kA, &tmX, &full[s], kb * 64, static_cast<int>(m0), pol_x);
+        bulk_load(st, w_src(g), kWTile, &full[s], pol_w);
+        int kx, my;
+        x_coords(g, kx, my);
+        if (a.x_bulk_probe)  // timing probe: activation tile as one bulk copy (values meaningless)
+          bulk_load(st + kWTile, a.x_bulk_probe + (static_cast<int64_t>(kx) / 64 * a.m_tiles + my / BN) * (BN * 128),
+                    BN * 128, &full[s], pol_x);
+        else
+          tma_load_2d_hint(st + kWTile, &tmX, &full[s], kx, my, pol_x);
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
-      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int it = 0, seg = 0;
+      for (int64_t g = g0; g < g1; ++seg) {
+        const int64_t t = g / kbs;
+        const int64_t ge = min(g1, (t + 1) * kbs);
+        const int buf = seg & 1;
+        mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a = smem_u32(smem + s * S::kStage);
-        const uint32_t b = a + S::kA;
+        const uint32_t acc = tmem + buf * BN;
+        for (int64_t u = g; u < ge; ++u, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t wa = smem_u32(smem + s * S::kStage), xb = wa + kWTile;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16(tmem, sw128_kmajor_desc(a + k * 32), sw128_kmajor_desc(b + k * 32), idesc,
-                    (kb > kb0 || k > 0) ? 1u : 0u);
-        umma_commit(&empty[s]);
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(acc, sw128_kmajor_desc(wa + k * 32), sw128_kmajor_desc(xb + k * 32), idesc,
+                      (u > g || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[buf]);
+        g = ge;
       }
-      umma_commit(tmem_full);
     }
   } else {
     // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4 ----
     const int q = warp & 3;
     const int row = q * 32 + lane;  // weight row within the tile
-    const int n = n0 + row;
-    const int et = threadIdx.x - 64;  // 0..127
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int et = threadIdx.x - 64;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    pdl_wait();  // the epilogue reads / writes activations of earlier kernels
     float v[16];
-    if (splits == 1) {
+    int seg = 0;
+    for (int64_t g = g0; g < g1; ++seg) {
+      const int64_t t = g / kbs;
+      const int64_t tb = t * kbs, te = (t + 1) * kbs;
+      const int64_t ge = min(g1, te);
+      const int n_tile = static_cast<int>(t / a.m_tiles), m_tile = static_cast<int>(t % a.m_tiles);
+      const int n = n_tile * 128 + row;
+      const int64_t m0 = static_cast<int64_t>(m_tile) * BN;
+      const int buf = seg & 1;
+      const uint32_t acc = tmem + buf * BN + lane_off;
+      EpiPre cur, nxt;
+      if (g == tb) epi_prefetch(e, n, a.N, m0, a.M, cur);  // before the accumulator is ready
+      mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      if (g > tb) {
+        // tile started in an earlier CTA (this is our first segment): park the
+        // partial for the owner (the CTA holding the tile's first k-block)
+        float* dst = a.ws + (static_cast<int64_t>(c) * 128 + row) * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        tmem_ld16(taddr + c, v);
-        if (m0 + c < M) epi_chunk(e, n, N, m0 + c, M, v);
-      }
-    } else {
-      const int tile = m_tile * gridDim.x + n_tile;
-      float* mine = ws + (static_cast<int64_t>(tile) * splits + split) * (BN * 128);
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        tmem_ld16(taddr + c, v);
+        for (int cc = 0; cc < BN; cc += 16) {
+          tmem_ld16(acc + cc, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) mine[(c + j) * 128 + row] = v[j];
-      }
-      __threadfence();
-      named_bar(1, 128);
-      if (et == 0) *last_flag = (atomicAdd(&counters[tile], 1) == splits - 1);
-      named_bar(1, 128);
-      if (*last_flag) {
-        __threadfence();
-        const float* base = ws + static_cast<int64_t>(tile) * splits * (BN * 128);
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 16) {
-          if (m0 + c >= M) break;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float acc = 0.f;
-            for (int s2 = 0; s2 < splits; ++s2) acc += __ldcg(base + s2 * (BN * 128) + (c + j) * 128 + row);
-            v[j] = acc;
-          }
-          epi_chunk(e, n, N, m0 + c, M, v);
+          for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
-        if (et == 0) counters[tile] = 0;
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
+        __threadfence();
+        named_bar(1, 128);
+        if (et == 0) st_release(a.flags + c, a.epoch);
+      } else {
+        // owner (or sole CTA) of tile t: add the later CTAs' partials (their first
+        // segments, finished long before this, our last segment) in CTA order
+        const int c_last = ge < te ? cta_of(te - 1, a.units, C) : c;
+        if (c_last > c) {
+          for (int p = c + 1 + et; p <= c_last; p += 128)
+            while (ld_acquire(a.flags + p) < a.epoch) {
+            }
+          named_bar(1, 128);
+        }
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 16) {
+          if (m0 + cc >= a.M) break;  // warp-uniform
+          if (cc + 16 < BN && m0 + cc + 16 < a.M) epi_prefetch(e, n, a.N, m0 + cc + 16, a.M, nxt);
+          tmem_ld16(acc + cc, v);
+          for (int p = c + 1; p <= c_last; ++p) {
+            const float* src = a.ws + (static_cast<int64_t>(p) * 128 + row) * BN + cc;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              const float4 f = __ldcg(reinterpret_cast<const float4*>(src + j));
+              v[j] += f.x;
+              v[j + 1] += f.y;
+              v[j + 2] += f.z;
+              v[j + 3] += f.w;
+            }
+          }
+          epi_chunk(e, n, a.N, m0 + cc, a.M, v, cur);
+          cur = nxt;
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
       }
+      g = ge;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kCols);
+  if (warp == 1) tmem_dealloc(tmem, S::kCols);
 }
 
-bool gemm_tc_supported(int64_t M, int N, int K) { return M >= 1 && N % 128 == 0 && K % 64 == 0 && K >= 64; }
+bool gemm_tc_supported(int64_t M, int N, int K) { return M >= 1 && weight_packable(N, K); }
 
-CUtensorMap tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// one launch counter for every instantiation: all of them share a model's flag array
+static std::atomic<int> g_sk_epoch{0};
 
 template <int BN, int STAGES>
-static void launch(const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e, float* ws,
-                   size_t ws_bytes, int* counters, cudaStream_t s, int sms) {
-  using Sm = GemmSmem<BN, STAGES>;
+static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, const Epilogue& e, float* ws,
+                      size_t ws_bytes, int* flags, cudaStream_t s, int sms) {
+  using Sm = SkSmem<BN, STAGES>;
   static bool attr = [] {
-    PCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
+    PCB_CUDA(cudaFuncSetAttribute(k_gemm_sk<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
     return true;
   }();
   (void)attr;
-  const int n_tiles = N / 128;
-  const int m_tiles = static_cast<int>((M + BN - 1) / BN);
-  const int tiles = n_tiles * m_tiles;
-  const int kbs = K / 64;
-  // CTAs resident per SM given the shared-memory footprint
-  const int per_sm = std::max(1, (227 * 1024) / Sm::kBytes);
-  const int slots = sms * per_sm;
-  int splits = 1;
-  if (tiles < slots) {
-    splits = std::min(kbs / 2 > 0 ? kbs / 2 : 1, std::max(1, slots / tiles));
-    splits = std::max(1, std::min(splits, 16));
-  }
-  while (splits > 1 && static_cast<size_t>(tiles) * splits * BN * 128 * sizeof(float) > ws_bytes) --splits;
-  CUtensorMap tw = tmap_bf16_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), 128);
+  SkArgs a;
+  a.w = static_cast<const uint8_t*>(Wp);
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.kbs = K / 64;
+  a.m_tiles = static_cast<int>((M + BN - 1) / BN);
+  a.units = static_cast<int64_t>(N / 128) * a.m_tiles * a.kbs;
+  a.ws = ws;
+  a.flags = flags;
+  a.epoch = ++g_sk_epoch;
+  if (std::getenv("PCB_GEMM_XBULK_PROBE")) a.x_bulk_probe = static_cast<const uint8_t*>(A);
+  int C = static_cast<int>(std::min<int64_t>(sms, a.units));
+  if (const char* ov = std::getenv("PCB_GEMM_CTAS")) C = std::max(1, std::min(C, std::atoi(ov)));  // tuning
+  if (static_cast<size_t>(C) * 128 * BN * sizeof(float) > ws_bytes) throw std::runtime_error("gemm workspace too small");
   CUtensorMap tx = tmap_bf16_2d(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), BN);
-  dim3 grid(n_tiles, m_tiles, splits);
-  k_gemm_tc<BN, STAGES><<<grid, kThreads, Sm::kBytes, s>>>(tw, tx, M, N, K, splits, e, ws, counters);
-  PCB_CUDA(cudaGetLastError());
+  launch_k(k_gemm_sk<BN, STAGES>, dim3(C), dim3(kThreads), Sm::kBytes, s, 1, tx, a, e);
 }
 
-void gemm_tc(const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e, float* ws, size_t ws_bytes,
-             int* counters, cudaStream_t s) {
+void gemm_tc(const void* A, const void* Wp, int64_t M, int N, int K, const Epilogue& e, float* ws, size_t ws_bytes,
+             int* flags, cudaStream_t s) {
   if (M <= 0) return;
   static int sms = [] {
     int dev = 0, v = 148;
@@ -280,11 +428,11 @@ void gemm_tc(const void* A, const void* W, int64_t M, int N, int K, const Epilog
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  if (M <= 16) launch<16, 5>(A, W, M, N, K, e, ws, ws_bytes, counters, s, sms);
-  else if (M <= 32) launch<32, 5>(A, W, M, N, K, e, ws, ws_bytes, counters, s, sms);
-  else if (M <= 64) launch<64, 4>(A, W, M, N, K, e, ws, ws_bytes, counters, s, sms);
-  else if (M <= 128) launch<128, 4>(A, W, M, N, K, e, ws, ws_bytes, counters, s, sms);
-  else launch<256, 4>(A, W, M, N, K, e, ws, ws_bytes, counters, s, sms);
+  if (M <= 16) launch_sk<16, 10>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
+  else if (M <= 32) launch_sk<32, 10>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
+  else if (M <= 64) launch_sk<64, 8>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
+  else if (M <= 128) launch_sk<128, 6>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
+  else launch_sk<256, 4>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
 }
 
 }  // namespace pcb::kern

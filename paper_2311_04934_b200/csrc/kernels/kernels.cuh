@@ -24,6 +24,7 @@ enum EpiKind : int {
   EPI_RESID = 1,   // resid[m][n] += acc
   EPI_GELU = 2,    // out[m][n] = gelu(acc)   (model dtype)
   EPI_F32 = 3,     // outf[m*ldo + n] = acc   (fp32 logits)
+  EPI_NONE = 4,    // discard (timing probes only)
 };
 
 struct Epilogue {
@@ -57,15 +58,27 @@ void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table
 void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s);
 void argmax_rows(const float* logits, int64_t rows, int V, int32_t* out, cudaStream_t s);
 
+// ---- packed bf16 weights (the tcgen05 GEMM's HBM layout) ----
+// W[n][k] lives in 128x64 tiles [N/128][K/64], 16 KB each, each tile the SW128
+// K-major shared-memory image: row r at r*128 B, 16-byte chunk c at (c ^ (r & 7)).
+__host__ __device__ inline uint64_t packed_index(int n, int k, int K) {
+  const int tn = n >> 7, r = n & 127, tk = k >> 6, kk = k & 63;
+  const int c = kk >> 3, e = kk & 7;
+  return ((static_cast<uint64_t>(tn) * (K >> 6) + tk) * 16384ull + r * 128 + ((c ^ (r & 7)) << 4)) / 2 + e;
+}
+bool weight_packable(int N, int K);
+void pack_weight_bf16(const void* src_rowmajor, void* dst_packed, int N, int K, cudaStream_t s);
+
 // ---- GEMM: C[m][n] = sum_k A[m][k] * W[n][k] with a fused epilogue ----
 // SIMT: F32 = fp64 accumulation in the reference's 4-lane order (bit-exact
-// dot products); BF16 = fp32 accumulation (bring-up / odd shapes).
+// dot products); BF16 = fp32 accumulation (bring-up / odd shapes), W packed or not.
 void gemm_simt(int dtype, const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e,
-               cudaStream_t s);
-// tcgen05 + TMA + TMEM (bf16 in, fp32 accumulate).  Requires K%64==0, N%128==0.
+               cudaStream_t s, bool w_packed = false);
+// tcgen05 persistent stream-K GEMM (bf16 in, fp32 accumulate) over PACKED weights.
+// Requires K%64==0, N%128==0.  workspace >= 148*128*256*4 bytes; flags >= #SMs ints (zeroed once).
 bool gemm_tc_supported(int64_t M, int N, int K);
-void gemm_tc(const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e, float* workspace,
-             size_t workspace_bytes, int* counters, cudaStream_t s);
+void gemm_tc(const void* A, const void* W_packed, int64_t M, int N, int K, const Epilogue& e, float* workspace,
+             size_t workspace_bytes, int* flags, cudaStream_t s);
 
 // ---- attention over a KV cache ----
 // q [n][d]; K/V layer bases [rows][d]; query i (sequence index P+i) attends keys

@@ -81,6 +81,8 @@ void fill_const(float* d, uint64_t n, float v, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 __global__ void k_embed(const int32_t* tok, const int32_t* pos, const float* table, const float* abs_table, int d,
                         float* h) {
+  pdl_trigger();
+  pdl_wait();
   int64_t i = blockIdx.x;
   const float* e = table + static_cast<int64_t>(tok[i]) * d;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
@@ -92,7 +94,7 @@ __global__ void k_embed(const int32_t* tok, const int32_t* pos, const float* tab
 void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table, const float* abs_table, int d,
            float* h, cudaStream_t s) {
   if (n <= 0) return;
-  k_embed<<<static_cast<unsigned>(n), 256, 0, s>>>(tok, pos, table, abs_table, d, h);
+  launch_k(k_embed, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, tok, pos, table, abs_table, d, h);
   PCB_CUDA(cudaGetLastError());
 }
 
@@ -101,6 +103,8 @@ void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void k_layernorm(const float* h, int d, T* out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double red[32];
   const float* row = h + static_cast<int64_t>(blockIdx.x) * d;
   auto block_sum = [&](double v) {
@@ -128,9 +132,10 @@ __global__ void k_layernorm(const float* h, int d, T* out) {
 void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s) {
   if (n <= 0) return;
   if (dtype == F32)
-    k_layernorm<float><<<static_cast<unsigned>(n), 256, 0, s>>>(h, d, static_cast<float*>(out));
+    launch_k(k_layernorm<float>, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, h, d, static_cast<float*>(out));
   else
-    k_layernorm<__nv_bfloat16><<<static_cast<unsigned>(n), 256, 0, s>>>(h, d, static_cast<__nv_bfloat16*>(out));
+    launch_k(k_layernorm<__nv_bfloat16>, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, h, d,
+             static_cast<__nv_bfloat16*>(out));
   PCB_CUDA(cudaGetLastError());
 }
 
@@ -138,6 +143,8 @@ void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStrea
 // argmax_lowest (model.cpp:457-462): ties break to the lowest index.
 // ---------------------------------------------------------------------------
 __global__ void k_argmax(const float* logits, int V, int32_t* out) {
+  pdl_trigger();
+  pdl_wait();
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -174,7 +181,7 @@ __global__ void k_argmax(const float* logits, int V, int32_t* out) {
 }
 void argmax_rows(const float* logits, int64_t rows, int V, int32_t* out, cudaStream_t s) {
   if (rows <= 0) return;
-  k_argmax<<<static_cast<unsigned>(rows), 1024, 0, s>>>(logits, V, out);
+  launch_k(k_argmax, dim3(static_cast<unsigned>(rows)), dim3(1024), 0, s, 1, logits, V, out);
   PCB_CUDA(cudaGetLastError());
 }
 
@@ -239,7 +246,13 @@ __device__ __forceinline__ void epi_pair(const Epilogue& e, int64_t m, int n, in
 constexpr int TM = 16, TN = 32, TK = 32;
 
 template <typename T, bool EXACT>
-__global__ void k_gemm_simt(const T* __restrict__ A, const T* __restrict__ W, int64_t M, int N, int K, Epilogue e) {
+__global__ void k_gemm_simt(const T* __restrict__ A, const T* __restrict__ W, int64_t M, int N, int K, Epilogue e,
+                            bool w_packed) {
+  pdl_trigger();
+  pdl_wait();
+  auto widx = [&](int64_t n, int64_t k) -> int64_t {
+    return w_packed ? static_cast<int64_t>(packed_index(static_cast<int>(n), static_cast<int>(k), K)) : n * K + k;
+  };
   __shared__ float sA[TM][TK + 1];
   __shared__ float sW[TN][TK + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -258,7 +271,7 @@ __global__ void k_gemm_simt(const T* __restrict__ A, const T* __restrict__ W, in
     for (int idx = tid; idx < TN * TK; idx += 256) {
       int r = idx / TK, c = idx % TK;
       int gn = blockIdx.x * TN + r;
-      sW[r][c] = (gn < N && k0 + c < K4) ? ld_f(W, (int64_t)gn * K + k0 + c) : 0.f;
+      sW[r][c] = (gn < N && k0 + c < K4) ? ld_f(W, widx(gn, k0 + c)) : 0.f;
     }
     __syncthreads();
     const int kmax = min(TK, K4 - k0);
@@ -276,8 +289,8 @@ __global__ void k_gemm_simt(const T* __restrict__ A, const T* __restrict__ W, in
   if (m >= M || n0 >= N) return;
   for (int k = K4; k < K; ++k) {  // reference tail goes to lane 0
     Acc x = ld_f(A, m * K + k);
-    a0[0] += x * (Acc)ld_f(W, (int64_t)n0 * K + k);
-    a1[0] += x * (Acc)ld_f(W, (int64_t)(n0 + 1) * K + k);
+    a0[0] += x * (Acc)ld_f(W, widx(n0, k));
+    a1[0] += x * (Acc)ld_f(W, widx(n0 + 1, k));
   }
   float v0 = static_cast<float>((a0[0] + a0[1]) + (a0[2] + a0[3]));
   float v1 = static_cast<float>((a1[0] + a1[1]) + (a1[2] + a1[3]));
@@ -285,16 +298,16 @@ __global__ void k_gemm_simt(const T* __restrict__ A, const T* __restrict__ W, in
 }
 
 void gemm_simt(int dtype, const void* A, const void* W, int64_t M, int N, int K, const Epilogue& e,
-               cudaStream_t s) {
+               cudaStream_t s, bool w_packed) {
   if (M <= 0) return;
   dim3 grid((N + TN - 1) / TN, static_cast<unsigned>((M + TM - 1) / TM));
   dim3 block(16, 16);
   if (dtype == F32)
-    k_gemm_simt<float, true><<<grid, block, 0, s>>>(static_cast<const float*>(A), static_cast<const float*>(W), M, N,
-                                                    K, e);
+    launch_k(k_gemm_simt<float, true>, grid, block, 0, s, 1, static_cast<const float*>(A), static_cast<const float*>(W),
+             M, N, K, e, false);
   else
-    k_gemm_simt<__nv_bfloat16, false><<<grid, block, 0, s>>>(static_cast<const __nv_bfloat16*>(A),
-                                                             static_cast<const __nv_bfloat16*>(W), M, N, K, e);
+    launch_k(k_gemm_simt<__nv_bfloat16, false>, grid, block, 0, s, 1, static_cast<const __nv_bfloat16*>(A),
+             static_cast<const __nv_bfloat16*>(W), M, N, K, e, w_packed);
   PCB_CUDA(cudaGetLastError());
 }
 
@@ -306,6 +319,8 @@ void gemm_simt(int dtype, const void* A, const void* W, int64_t M, int N, int K,
 // ---------------------------------------------------------------------------
 template <typename T, bool EXACT>
 __global__ void k_attn_simt(AttnArgs a, float inv_sqrt, float* scratch_f) {
+  pdl_trigger();
+  pdl_wait();
   using Acc = typename std::conditional<EXACT, double, float>::type;
   const int h = blockIdx.x;
   const int64_t i = a.i0 + blockIdx.y;
@@ -379,9 +394,9 @@ void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s
   dim3 grid(a.H, static_cast<unsigned>(nq));
   float inv_sqrt = 1.0f / sqrtf(static_cast<float>(a.hd));
   if (dtype == F32)
-    k_attn_simt<float, true><<<grid, 128, 0, s>>>(a, inv_sqrt, scratch);
+    launch_k(k_attn_simt<float, true>, grid, dim3(128), 0, s, 1, a, inv_sqrt, scratch);
   else
-    k_attn_simt<__nv_bfloat16, false><<<grid, 128, 0, s>>>(a, inv_sqrt, scratch);
+    launch_k(k_attn_simt<__nv_bfloat16, false>, grid, dim3(128), 0, s, 1, a, inv_sqrt, scratch);
   PCB_CUDA(cudaGetLastError());
 }
 
@@ -408,6 +423,8 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
 
 __global__ void __launch_bounds__(256) k_assemble(const CopySeg* __restrict__ segs, const uint64_t* __restrict__ first_chunk,
                                                   int n_segs, uint64_t n_chunks) {
+  pdl_trigger();
+  pdl_wait();
   for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     int lo = 0, hi = n_segs - 1;  // last segment with first_chunk <= c
     while (lo < hi) {
@@ -448,7 +465,7 @@ void assemble(const CopySeg* d_segs, const uint64_t* d_first_chunk, int n_segs, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(sms) * 8);
-  k_assemble<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_segs, d_first_chunk, n_segs, n_chunks);
+  launch_k(k_assemble, dim3(static_cast<unsigned>(grid)), dim3(256), 0, s, 1, d_segs, d_first_chunk, n_segs, n_chunks);
   PCB_CUDA(cudaGetLastError());
 }
 
