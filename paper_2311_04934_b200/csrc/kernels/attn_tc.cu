@@ -2,15 +2,18 @@
 // against a range of key rows of the assembled cache (reference model.cpp:401-427:
 // causal by sequence order, query i sees keys j <= P + i).
 //
-//   warp 0     TMA: Q tile once, then K/V blocks of 64 keys (2-stage ring)
-//   warp 1     TMEM alloc + MMA issue: S = Q K^T (M=128, N=64, K=hd) into TMEM,
-//              then O_blk = P V (M=128, N=hd, K=64; V as an MN-major operand)
-//   warps 2-5  softmax: one thread per query row (TMEM lane), online max/sum in
-//              fp32, P -> swizzled smem (bf16), O accumulated in registers
-// Suffix prefill (few queries, long cache) splits the key range across CTAs so
-// all SMs stream the KV; a combine kernel merges the (O, m, l) partials in split
-// order (deterministic).  Prefill (P = 0) tiles queries and skips key blocks above
-// the causal diagonal.
+//   warp 0     TMA: Q tile once, then K/V blocks of 64 keys (KV_STAGES-deep ring)
+//   warp 1     TMEM alloc + MMA issue: S_j = Q K_j^T (M=128, N=64, K=hd) into one of
+//              two TMEM score buffers, O += P_j V_j (M=128, N=hd, K=64; V is an
+//              MN-major operand) accumulated in TMEM across all blocks
+//   warps 2-5  softmax: one thread per query row (TMEM lane); online max/sum in
+//              fp32, P_j -> swizzled smem (bf16)
+// Pipelining: QK^T of block j+1 runs while the softmax of block j executes (two
+// score buffers).  The running max is rescaled lazily: O (in TMEM) is corrected
+// only when a row's max grows by more than 2^8, so the common step never touches O.
+// Suffix prefill (few queries, long cache) splits the key range across CTAs so all
+// SMs stream the KV; a combine kernel merges the (O, m, l) partials in split order
+// (deterministic).  Prefill (P = 0) tiles queries and skips blocks above the diagonal.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -23,29 +26,57 @@ CUtensorMap tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, uint32_t
 
 namespace {
 
-constexpr int BQ = 128, BKV = 64, kAttnThreads = 192;
+constexpr int BQ = 128, BKV = 64, kAttnThreads = 192, KV_STAGES = 3;
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain: stale max tolerated up to 2^8
 
 template <int HD>
 struct AttnSmem {
   static constexpr int kAtoms = HD / 64;
-  static constexpr int kQ = BQ * HD * 2;        // Q tile
-  static constexpr int kKV = BKV * HD * 2;      // one K (or V) block
-  static constexpr int kStage = 2 * kKV;        // K + V
-  static constexpr int kP = BQ * BKV * 2;       // probabilities (bf16)
-  static constexpr int kBytes = kQ + 2 * kStage + kP + 1024 + 1024;
-  static constexpr uint32_t kTmemCols = HD + BKV <= 256 ? 256 : 512;
+  static constexpr int kQ = BQ * HD * 2;
+  static constexpr int kKV = BKV * HD * 2;
+  static constexpr int kStage = 2 * kKV;  // K + V
+  static constexpr int kP = BQ * BKV * 2;  // one P buffer (two are used)
+  static constexpr int kBytes = kQ + KV_STAGES * kStage + 2 * kP + 1024 + 1024;
+  static constexpr uint32_t kTmemCols = 2 * BKV + HD <= 256 ? 256 : 512;
 };
 
 struct AttnParams {
   int64_t n, P, total;
   int H, d;
   int splits;
-  int64_t blocks_total;  // key blocks for the whole (causal) range of tile 0
-  float scale_log2;      // log2(e) / sqrt(hd)
+  float scale_log2;  // log2(e) / sqrt(hd)
   __nv_bfloat16* out;
-  float* part_o;  // [H][splits][BQ][HD]
-  float* part_ml; // [H][splits][BQ][2]
+  float* part_o;   // [H][splits][BQ][HD]
+  float* part_ml;  // [H][splits][BQ][2]
+  int kv_head_major;
+  int64_t kv_rows;  // rows per head plane (head-major layout)
+  unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
 };
+
+__device__ __forceinline__ void probe(const AttnParams& p, int ev, int it) {
+  if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && it < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg[ev * 64 + it] = t;
+  }
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -56,22 +87,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + S::kQ;
-  uint8_t* sP = sKV + 2 * S::kStage;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + S::kP);
+  uint8_t* sP = sKV + KV_STAGES * S::kStage;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * S::kP);
   uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* p_full = bar + 6;
-  uint64_t* o_full = bar + 7;
-  uint64_t* o_free = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* kv_full = bar + 1;                // [KV_STAGES]
+  uint64_t* kv_empty = kv_full + KV_STAGES;   // [KV_STAGES]
+  uint64_t* s_full = kv_empty + KV_STAGES;    // [2] score buffer b holds blocks it with it&1 == b
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 1;             // [2] PV of blocks it with it&1 == b completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q_tile = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, split = blockIdx.z;  // heaviest tiles first
   const int64_t q0 = static_cast<int64_t>(q_tile) * BQ;
-  // causal key range of this tile: keys [0, min(total, P + q0 + BQ))
-  const int64_t key_end = min(p.total, p.P + q0 + BQ);
+  const int64_t key_end = min(p.total, p.P + q0 + BQ);  // causal key range of this tile
   const int64_t nblk = (key_end + BKV - 1) / BKV;
   const int64_t b0 = nblk * split / p.splits, b1 = nblk * (split + 1) / p.splits;
   const int nb = static_cast<int>(b1 - b0);
@@ -81,14 +110,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < KV_STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(s_full, 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
     mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
-    mbar_init(o_free, 128);
+    mbar_init(&pv_done[0], 1);
+    mbar_init(&pv_done[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, S::kTmemCols);
@@ -96,9 +126,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + BKV;
+  const uint32_t tO = tmem + 2 * BKV;  // S buffers at columns [0, 64) and [64, 128)
   pdl_trigger();
-  pdl_wait();  // Q/K/V come from the QKV GEMM (and assembly) just before
+  pdl_wait();  // Q/K/V come from the QKV GEMM (and the assembly) just before
 
   if (warp == 0) {
     if (elect_one() && nb > 0) {
@@ -106,14 +136,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int a = 0; a < S::kAtoms; ++a)
         tma_load_2d(sQ + a * (BQ * 128), &tmQ, q_full, h * HD + a * 64, static_cast<int>(q0));
       for (int it = 0; it < nb; ++it) {
-        const int s = it & 1;
-        mbar_wait(&kv_empty[s], ((it >> 1) & 1) ^ 1);
+        const int s = it % KV_STAGES;
+        mbar_wait(&kv_empty[s], ((it / KV_STAGES) & 1) ^ 1);
+        probe(p, 4, it);
         uint8_t* st = sKV + s * S::kStage;
         const int j0 = static_cast<int>((b0 + it) * BKV);
         mbar_expect_tx(&kv_full[s], S::kStage);
+        // head-interleaved cache [rows][H*hd]: x = h*hd + a*64, y = key row;
+        // head-major cache [H][rows][hd]:     x = a*64,        y = h*rows + key row
+        const int kx = p.kv_head_major ? 0 : h * HD;
+        const int ky = p.kv_head_major ? static_cast<int>(h * p.kv_rows + j0) : j0;
         for (int a = 0; a < S::kAtoms; ++a) {
-          tma_load_2d(st + a * (BKV * 128), &tmK, &kv_full[s], h * HD + a * 64, j0);
-          tma_load_2d(st + S::kKV + a * (BKV * 128), &tmV, &kv_full[s], h * HD + a * 64, j0);
+          tma_load_2d(st + a * (BKV * 128), &tmK, &kv_full[s], kx + a * 64, ky);
+          tma_load_2d(st + S::kKV + a * (BKV * 128), &tmV, &kv_full[s], kx + a * 64, ky);
         }
       }
     }
@@ -124,77 +159,110 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
       mbar_wait(q_full, 0);
       auto issue_qk = [&](int it) {
-        const int s = it & 1;
-        mbar_wait(&kv_full[s], (it >> 1) & 1);
+        const int s = it % KV_STAGES;
+        mbar_wait(&kv_full[s], (it / KV_STAGES) & 1);
+        probe(p, 5, it);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sKV + s * S::kStage);
+        const uint32_t tS = tmem + (it & 1) * BKV;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const int a = k >> 2, kk = k & 3;
           umma_bf16(tS, sw128_kmajor_desc(q_addr + a * (BQ * 128) + kk * 32),
                     sw128_kmajor_desc(k_addr + a * (BKV * 128) + kk * 32), idS, k > 0 ? 1u : 0u);
         }
-        umma_commit(s_full);
+        umma_commit(&s_full[it & 1]);
       };
       issue_qk(0);
       for (int it = 0; it < nb; ++it) {
-        const int s = it & 1;
-        mbar_wait(p_full, it & 1);  // P(it) in smem, S(it) consumed
-        tc_fence_after();
+        // S(it+1) goes to the other buffer; its previous content S(it-1) was consumed
+        // before p_full(it-1), which the previous iteration waited for.
         if (it + 1 < nb) issue_qk(it + 1);
-        if (it > 0) mbar_wait(o_free, (it - 1) & 1);
+        mbar_wait(p_full, it & 1);  // P(it) in smem (and any O correction done)
+        probe(p, 2, it);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sKV + s * S::kStage + S::kKV);
+        const uint32_t v_addr = smem_u32(sKV + (it % KV_STAGES) * S::kStage + S::kKV);
+        const uint32_t pb = p_addr + (it & 1) * S::kP;
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16(tO, sw128_kmajor_desc(p_addr + k * 32), sw128_mnmajor_desc(v_addr + k * 2048, BKV * 128, 1024),
-                    idO, k > 0 ? 1u : 0u);
-        umma_commit(o_full);
-        umma_commit(&kv_empty[s]);
+          umma_bf16(tO, sw128_kmajor_desc(pb + k * 32), sw128_mnmajor_desc(v_addr + k * 2048, BKV * 128, 1024),
+                    idO, (it > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&pv_done[it & 1]);
+        umma_commit(&kv_empty[it % KV_STAGES]);
+        probe(p, 3, it);
       }
     }
   } else {
     // ---- softmax warps: query row = TMEM lane ----
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
-    const int64_t qi = q0 + r;             // query index within the n new rows
-    const int64_t limit = p.P + qi;        // last visible key (sequence order)
+    const int64_t qi = q0 + r;       // query index within the n new rows
+    const int64_t limit = p.P + qi;  // last visible key (sequence order)
     const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
-    float o[HD];
-#pragma unroll
-    for (int x = 0; x < HD; ++x) o[x] = 0.f;
     float m = -INFINITY, l = 0.f;
     for (int it = 0; it < nb; ++it) {
       const int64_t j0 = (b0 + it) * BKV;
-      mbar_wait(s_full, it & 1);
+      mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+      if (threadIdx.x == 64) probe(p, 0, it);
       tc_fence_after();
       float sv[BKV];
+      {
+        uint32_t raw[BKV];
 #pragma unroll
-      for (int c = 0; c < BKV; c += 16) tmem_ld16(tS + lane_off + c, sv + c);
-      float bm = -INFINITY;
+        for (int c = 0; c < BKV; c += 16) tmem_ld16_nowait(tmem + (it & 1) * BKV + lane_off + c, raw + c);
+        tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < BKV; ++c) {
-        sv[c] = (j0 + c <= limit) ? sv[c] * p.scale_log2 : -INFINITY;
-        bm = fmaxf(bm, sv[c]);
+        for (int c = 0; c < BKV; ++c) sv[c] = __uint_as_float(raw[c]);
       }
-      const float mn = fmaxf(m, bm);
-      const float alpha = (mn == -INFINITY) ? 1.f : exp2f(m - mn);
+      if (threadIdx.x == 64) probe(p, 6, it);
+      // scores stay raw (unscaled); the 1/sqrt(hd) * log2(e) factor is folded into
+      // one FFMA per element in front of ex2.approx
+      if (j0 + BKV - 1 > limit) {  // diagonal block only
+#pragma unroll
+        for (int c = 0; c < BKV; ++c)
+          if (j0 + c > limit) sv[c] = -INFINITY;
+      }
+      float bm = sv[0];
+#pragma unroll
+      for (int c = 1; c < BKV; ++c) bm = fmaxf(bm, sv[c]);
+      // lazy max update: move the reference max only when it grows by > 2^8
+      const bool grow = bm > m + kRescaleThreshold / p.scale_log2 || (m == -INFINITY && bm > -INFINITY);
+      if (__any_sync(0xffffffffu, grow) && it > 0) {
+        // O holds blocks < it: wait for PV(it-1), then scale the rows that grow
+        mbar_wait(&pv_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        tc_fence_after();
+        const float f = grow ? fast_exp2((m - bm) * p.scale_log2) : 1.f;  // m = -inf -> 0
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 16) {
+          float ov[16];
+          tmem_ld16(tO + lane_off + c, ov);
+#pragma unroll
+          for (int x = 0; x < 16; ++x) ov[x] *= f;
+          tmem_st16(tO + lane_off + c, ov);
+        }
+        tmem_st_wait();
+      }
+      if (grow) {
+        l *= fast_exp2((m - bm) * p.scale_log2);
+        m = bm;
+      }
+      const float mb = (m == -INFINITY) ? 0.f : m * p.scale_log2;  // all scores -inf when m is
       float bsum = 0.f;
       uint32_t packed[BKV / 2];
 #pragma unroll
       for (int c = 0; c < BKV; c += 2) {
-        float p0 = (mn == -INFINITY) ? 0.f : exp2f(sv[c] - mn);
-        float p1 = (mn == -INFINITY) ? 0.f : exp2f(sv[c + 1] - mn);
+        const float p0 = fast_exp2(fmaf(sv[c], p.scale_log2, -mb));
+        const float p1 = fast_exp2(fmaf(sv[c + 1], p.scale_log2, -mb));
+        bsum += p0 + p1;
         __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-        // the denominator sums the bf16-rounded weights actually fed to the MMA
-        float2 f2 = __bfloat1622float2(b2);
-        bsum += f2.x + f2.y;
         packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
       }
-      l = l * alpha + bsum;
-      m = mn;
-      // P row r -> 128-byte swizzled smem row (16-byte chunk c at c ^ (r & 7))
-      uint8_t* prow = sP + r * 128;
+      l += bsum;
+      if (threadIdx.x == 64) probe(p, 7, it);
+      // P buffer it&1 is free once PV(it-2) completed
+      if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
+      if (threadIdx.x == 64) probe(p, 8, it);
+      uint8_t* prow = sP + (it & 1) * S::kP + r * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint4 v = make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
@@ -203,39 +271,43 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(p_full);
-#pragma unroll
-      for (int x = 0; x < HD; ++x) o[x] *= alpha;
-      mbar_wait(o_full, it & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HD; c += 16) {
-        float ob[16];
-        tmem_ld16(tO + lane_off + c, ob);
-#pragma unroll
-        for (int x = 0; x < 16; ++x) o[c + x] += ob[x];
-      }
-      tc_fence_before();
-      mbar_arrive(o_free);
+      if (threadIdx.x == 64) probe(p, 1, it);
     }
-    if (qi < p.n && nb > 0) {
+    if (nb > 0) {
+      mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+      tc_fence_after();
       if (p.splits == 1) {
         const float inv = 1.f / l;
         __nv_bfloat16* dst = p.out + qi * p.d + h * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 16) {
+          float ov[16];
+          tmem_ld16(tO + lane_off + c, ov);
+          if (qi < p.n) {
+            uint4 w[2];
+            __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w);
 #pragma unroll
-        for (int x = 0; x < HD; x += 8) {
-          uint4 v;
-          __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-          for (int y = 0; y < 4; ++y) b[y] = __floats2bfloat162_rn(o[x + 2 * y] * inv, o[x + 2 * y + 1] * inv);
-          *reinterpret_cast<uint4*>(dst + x) = v;
+            for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
+            *reinterpret_cast<uint4*>(dst + c) = w[0];
+            *reinterpret_cast<uint4*>(dst + c + 8) = w[1];
+          }
         }
       } else {
         const int64_t slot = (static_cast<int64_t>(h) * p.splits + split) * BQ + r;
         float* po = p.part_o + slot * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 16) {
+          float ov[16];
+          tmem_ld16(tO + lane_off + c, ov);
+          if (qi < p.n)
 #pragma unroll
-        for (int x = 0; x < HD; x += 4) *reinterpret_cast<float4*>(po + x) = make_float4(o[x], o[x + 1], o[x + 2], o[x + 3]);
-        p.part_ml[slot * 2] = m;
-        p.part_ml[slot * 2 + 1] = l;
+            for (int x = 0; x < 16; x += 4)
+              *reinterpret_cast<float4*>(po + c + x) = make_float4(ov[x], ov[x + 1], ov[x + 2], ov[x + 3]);
+        }
+        if (qi < p.n) {
+          p.part_ml[slot * 2] = m;
+          p.part_ml[slot * 2 + 1] = l;
+        }
       }
     }
   }
@@ -292,8 +364,8 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   p.out = static_cast<__nv_bfloat16*>(a.out);
   const int q_tiles = static_cast<int>((a.n + BQ - 1) / BQ);
   const int64_t nblk0 = (std::min<int64_t>(p.total, a.P + BQ) + BKV - 1) / BKV;  // tile 0 key blocks
-  // one CTA per SM (the fp32 O row lives in registers); pick the split count that
-  // minimises (waves x blocks per CTA) for single-tile (suffix) launches
+  // one CTA per SM; for single-tile (suffix) launches pick the split count that
+  // minimises waves x blocks per CTA (+ a per-split fixed cost)
   const int base = q_tiles * a.H;
   int splits = 1;
   if (q_tiles == 1 && base < 2 * sms) {
@@ -301,23 +373,51 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
     for (int s2 = 1; s2 <= std::max<int64_t>(1, std::min<int64_t>(nblk0 / 2, 32)); ++s2) {
       const size_t need = static_cast<size_t>(a.H) * s2 * BQ * (HD + 2) * sizeof(float);
       if (s2 > 1 && need > scratch_bytes) break;
-      const int64_t cost = ((static_cast<int64_t>(base) * s2 + sms - 1) / sms) * ((nblk0 + s2 - 1) / s2) * 16 + s2;
+      const int64_t waves = (static_cast<int64_t>(base) * s2 + sms - 1) / sms;
+      const int64_t cost = waves * ((nblk0 + s2 - 1) / s2 + 6) * 16 + s2;
       if (best < 0 || cost < best) {
         best = cost;
         splits = s2;
       }
     }
   }
+  if (const char* ov = std::getenv("PCB_ATTN_SPLITS")) splits = std::max(1, std::atoi(ov));  // tuning
   p.splits = splits;
   p.part_o = scratch;
   p.part_ml = scratch + static_cast<size_t>(a.H) * splits * BQ * HD;
   CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), BQ);
-  CUtensorMap tk = tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
-  CUtensorMap tv = tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+  p.kv_head_major = std::getenv("PCB_ATTN_HM_PROBE") ? 1 : 0;  // timing probe (values meaningless)
+  p.kv_rows = p.total;
+  static unsigned long long* dbg = nullptr;
+  const bool probe_on = std::getenv("PCB_ATTN_DBG") != nullptr;  // timeline probe of CTA 0 (debug)
+  if (probe_on) {
+    if (!dbg) PCB_CUDA(cudaMallocManaged(&dbg, 12 * 64 * sizeof(unsigned long long)));
+    std::memset(dbg, 0, 12 * 64 * sizeof(unsigned long long));
+    p.dbg = dbg;
+  }
+  CUtensorMap tk = p.kv_head_major
+                       ? tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
+                       : tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+  CUtensorMap tv = p.kv_head_major
+                       ? tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
+                       : tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
   dim3 grid(q_tiles, a.H, splits);
   launch_k(k_attn_tc<HD>, grid, dim3(kAttnThreads), Sm::kBytes, s, 1, tq, tk, tv, p);
-  if (splits > 1) {
-    launch_k(k_attn_combine<HD>, dim3(static_cast<unsigned>(a.n), a.H), dim3(HD), 0, s, 1, p);
+  if (splits > 1) launch_k(k_attn_combine<HD>, dim3(static_cast<unsigned>(a.n), a.H), dim3(HD), 0, s, 1, p);
+  if (probe_on) {
+    PCB_CUDA(cudaDeviceSynchronize());
+    const unsigned long long t0 = dbg[4 * 64];
+    std::fprintf(stderr, "attn probe (ns from first load): it | kv_empty->load  kv_full(MMA)  s_full(softmax)  p_arrive  p_full(MMA)  pv_issued\n");
+    for (int it = 0; it < 16; ++it)
+      std::fprintf(stderr, "%2d | %8lld %8lld %8lld %8lld %8lld %8lld\n", it, (long long)(dbg[4 * 64 + it] - t0),
+                   (long long)(dbg[5 * 64 + it] - t0), (long long)(dbg[0 * 64 + it] - t0),
+                   (long long)(dbg[1 * 64 + it] - t0), (long long)(dbg[2 * 64 + it] - t0),
+                   (long long)(dbg[3 * 64 + it] - t0));
+    std::fprintf(stderr, "softmax detail: it | s_full  ld_done  exp_done  pvdone_wait  arrive\n");
+    for (int it = 0; it < 16; ++it)
+      std::fprintf(stderr, "%2d | %8lld %8lld %8lld %8lld %8lld\n", it, (long long)(dbg[0 * 64 + it] - t0),
+                   (long long)(dbg[6 * 64 + it] - t0), (long long)(dbg[7 * 64 + it] - t0),
+                   (long long)(dbg[8 * 64 + it] - t0), (long long)(dbg[1 * 64 + it] - t0));
   }
 }
 
