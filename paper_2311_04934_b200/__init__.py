@@ -268,6 +268,8 @@ class Model(_Handle):
         t = np.ascontiguousarray(tokens, np.int32)
         p = np.ascontiguousarray(positions, np.int64)
         n = len(t)
+        if len(p) != n:  # reference model.cpp:312-313
+            raise PromptCacheError(9, "ShapeMismatch: tokens/position_ids length mismatch")
         logits = np.zeros((n, self.vocab), np.float32)
         mk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
         kv = C.c_void_p()

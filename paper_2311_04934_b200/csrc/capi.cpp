@@ -20,6 +20,13 @@ using namespace pcb;
 
 struct pcb_schema {
   engine::Schema s;
+  bool planned = false;  // an unexpanded schema (chat tags kept) has no layout plan
+  std::string plan_error;
+  int plan_code = 0;
+  const engine::Schema& P() const {
+    if (!planned) throw pcb::Error(static_cast<pcb::ErrorCode>(plan_code), plan_error);
+    return s;
+  }
 };
 struct pcb_prompt {
   pml::PromptDoc p;
@@ -73,11 +80,17 @@ char* guard_str(F&& f) {
   return out;
 }
 
-engine::Schema make_schema(pml::SchemaDoc doc) {
-  engine::Schema s;
-  s.plan = layout::plan_layout(doc);
-  s.doc = std::move(doc);
-  return s;
+pcb_schema* make_schema(pml::SchemaDoc doc) {
+  auto* b = new pcb_schema;
+  try {
+    b->s.plan = layout::plan_layout(doc);
+    b->planned = true;
+  } catch (const Error& e) {
+    b->plan_error = e.what();
+    b->plan_code = static_cast<int>(e.code());
+  }
+  b->s.doc = std::move(doc);
+  return b;
 }
 }  // namespace
 
@@ -93,16 +106,16 @@ int pcb_schema_parse(const char* pml_text, int expand, pcb_schema** out) {
   return guard([&] {
     pml::SchemaDoc d = pml::parse_schema(pml_text);
     if (expand) d = pml::expand_chat_tags(d, pml::ChatTemplate::llama2());
-    *out = new pcb_schema{make_schema(std::move(d))};
+    *out = make_schema(std::move(d));
   });
 }
 int pcb_schema_from_ast(const char* ast, pcb_schema** out) {
-  return guard([&] { *out = new pcb_schema{make_schema(pml::schema_from_ast_json(ast))}; });
+  return guard([&] { *out = make_schema(pml::schema_from_ast_json(ast)); });
 }
 void pcb_schema_destroy(pcb_schema* s) { delete s; }
 char* pcb_schema_to_ast(const pcb_schema* s) { return guard_str([&] { return pml::schema_to_ast_json(s->s.doc); }); }
 char* pcb_schema_serialize(const pcb_schema* s) { return guard_str([&] { return pml::serialize(s->s.doc); }); }
-char* pcb_schema_plan_json(const pcb_schema* s) { return guard_str([&] { return s->s.plan.to_json(); }); }
+char* pcb_schema_plan_json(const pcb_schema* s) { return guard_str([&] { return s->P().plan.to_json(); }); }
 int pcb_prompt_parse(const char* text, pcb_prompt** out) {
   return guard([&] { *out = new pcb_prompt{pml::parse_prompt(text)}; });
 }
@@ -116,7 +129,7 @@ char* pcb_validate(const pcb_prompt* p, const pcb_schema* s) {
   return guard_str([&] { return pml::validate_prompt(p->p, s->s.doc).to_json(); });
 }
 char* pcb_resolve(const pcb_prompt* p, const pcb_schema* s) {
-  return guard_str([&] { return layout::resolve_prompt(p->p, s->s.plan).to_json(); });
+  return guard_str([&] { return layout::resolve_prompt(p->p, s->P().plan).to_json(); });
 }
 
 // ---- config ----
@@ -140,6 +153,8 @@ void pcb_model_destroy(pcb_model* m) { delete m; }
 int pcb_model_set_option(pcb_model* m, const char* key, int64_t v) {
   return guard([&] {
     if (std::strcmp(key, "force_simt") == 0) m->m->force_simt = v != 0;
+    else if (std::strcmp(key, "force_simt_gemm") == 0) m->m->force_simt_gemm = v != 0;
+    else if (std::strcmp(key, "force_simt_attn") == 0) m->m->force_simt_attn = v != 0;
     else if (std::strcmp(key, "profile") == 0) m->m->set_profiling(v != 0);
     else throw Error(ErrorCode::InvalidConfig, std::string("unknown option ") + key);
   });
@@ -349,18 +364,18 @@ int pcb_store_set_capacity(pcb_store* s, int tier, int64_t bytes) {
   return guard([&] { s->s->set_capacity(tier_of(tier), bytes); });
 }
 int pcb_store_encode_module(pcb_store* s, const pcb_schema* sc, const char* name, int tier) {
-  return guard([&] { s->s->insert(cache::encode_module(s->s->model(), sc->s.plan, name, tier_of(tier))); });
+  return guard([&] { s->s->insert(cache::encode_module(s->s->model(), sc->P().plan, name, tier_of(tier))); });
 }
 int pcb_store_encode_schema(pcb_store* s, const pcb_schema* sc, int tier, int* count) {
   return guard([&] {
-    int c = cache::encode_schema(s->s->model(), sc->s.plan, *s->s, tier_of(tier));
+    int c = cache::encode_schema(s->s->model(), sc->P().plan, *s->s, tier_of(tier));
     if (count) *count = c;
   });
 }
 int pcb_store_encode_scaffold(pcb_store* s, const pcb_schema* sc, const char* members_json, int tier) {
   return guard([&] {
     std::vector<std::string> members = nlohmann::json::parse(members_json);
-    s->s->insert(cache::encode_scaffold(s->s->model(), sc->s.plan, members, tier_of(tier)));
+    s->s->insert(cache::encode_scaffold(s->s->model(), sc->P().plan, members, tier_of(tier)));
   });
 }
 int pcb_store_lookup(pcb_store* s, const char* schema, const char* name, pcb_kv** out) {
@@ -383,7 +398,7 @@ int pcb_serve(pcb_store* s, const pcb_schema* sc, const pcb_prompt* p, int max_n
     req.max_new_tokens = max_new;
     req.use_cache = use_cache != 0;
     req.use_scaffolds = use_scaffolds != 0;
-    *out = new pcb_response{engine::serve(req, sc->s, *s->s)};
+    *out = new pcb_response{engine::serve(req, sc->P(), *s->s)};
   });
 }
 int pcb_oracle_serve(pcb_model* m, const pcb_schema* sc, const pcb_prompt* p, int max_new, pcb_response** out) {
@@ -391,7 +406,7 @@ int pcb_oracle_serve(pcb_model* m, const pcb_schema* sc, const pcb_prompt* p, in
     engine::ServeRequest req;
     req.prompt = p->p;
     req.max_new_tokens = max_new;
-    *out = new pcb_response{engine::oracle_serve(req, sc->s, *m->m)};
+    *out = new pcb_response{engine::oracle_serve(req, sc->P(), *m->m)};
   });
 }
 char* pcb_response_json(const pcb_response* r) { return guard_str([&] { return r->r.to_json(); }); }

@@ -145,6 +145,11 @@ struct Workspace {
     for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)mask, (void*)h, x, q,
                     attn, mid, (void*)logits, (void*)gemm_ws, (void*)counters, (void*)attn_scratch})
       if (p) cudaFree(p);
+    for (auto& e : staged)
+      if (e) {
+        cudaEventSynchronize(e);
+        cudaEventDestroy(e);
+      }
     if (host_ints) cudaFreeHost(host_ints);
   }
   template <typename T>
@@ -190,11 +195,25 @@ struct Workspace {
     }
     int64_t need_ints = 3 * n + rows + 16;
     if (need_ints > host_ints_cap) {
+      for (int sl = 0; sl < 2; ++sl)
+        if (staged[sl]) CK(cudaEventSynchronize(staged[sl]));
       if (host_ints) cudaFreeHost(host_ints);
-      CK(cudaMallocHost(reinterpret_cast<void**>(&host_ints), need_ints * 4));
+      CK(cudaMallocHost(reinterpret_cast<void**>(&host_ints), 2 * need_ints * 4));
       host_ints_cap = need_ints;
     }
   }
+  // Pinned staging for the per-call token / position uploads: two slots, each
+  // reused only after the async H2D copies that read it have executed (the host
+  // can run far ahead of the stream, e.g. back-to-back module precomputes).
+  cudaEvent_t staged[2] = {nullptr, nullptr};
+  int slot = 0;
+  int32_t* acquire_staging() {
+    slot ^= 1;
+    if (!staged[slot]) CK(cudaEventCreateWithFlags(&staged[slot], cudaEventDisableTiming));
+    else CK(cudaEventSynchronize(staged[slot]));
+    return host_ints + slot * host_ints_cap;
+  }
+  void release_staging(cudaStream_t s) { CK(cudaEventRecord(staged[slot], s)); }
   void ensure_attn_scratch(size_t bytes) {
     if (bytes > attn_scratch_bytes) {
       regrow(attn_scratch, bytes);
@@ -446,7 +465,7 @@ void Model::validate(const int32_t* tokens, const int64_t* positions, int64_t n,
 void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi) {
   const auto& e = *static_cast<const kern::Epilogue*>(epi);
   prof_begin();
-  if (w_->packed && !force_simt && kern::gemm_tc_supported(M, N, K))
+  if (w_->packed && !force_simt && !force_simt_gemm && kern::gemm_tc_supported(M, N, K))
     kern::gemm_tc(A, W, M, N, K, e, ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->counters, stream_);
   else
     kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_, w_->packed);
@@ -476,7 +495,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
   cudaStream_t s = stream_;
 
   // stage token ids / int32 positions (positions < max_position < 2^31, checked)
-  int32_t* hi = W.host_ints;
+  int32_t* hi = W.acquire_staging();
   for (int64_t i = 0; i < n; ++i) {
     hi[i] = tokens[i];
     hi[n + i] = static_cast<int32_t>(positions[i]);
@@ -496,6 +515,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     std::memcpy(bp, block_ids, n * 4);
     CK(cudaMemcpyAsync(W.block, bp, n * 4, cudaMemcpyHostToDevice, s));
   }
+  W.release_staging(s);
 
   prof_begin();
   kern::embed(W.tok, W.pos, n, w_->embed, w_->abs_table, d, W.h, s);
@@ -513,7 +533,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
   aa.block_id = block_ids ? W.block : nullptr;
   aa.alibi = alibi ? w_->alibi : nullptr;
   aa.kv_pos = alibi ? W.kvpos : nullptr;
-  const bool tc_attn = dtype_ == BF16 && !force_simt && kern::attention_tc_supported(aa);
+  const bool tc_attn = dtype_ == BF16 && !force_simt && !force_simt_attn && kern::attention_tc_supported(aa);
   int64_t nq = n;
   if (!tc_attn) {
     const size_t per_q = static_cast<size_t>(H) * total * sizeof(double);

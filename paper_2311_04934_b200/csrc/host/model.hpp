@@ -123,6 +123,8 @@ class Model {
 
   mutable std::atomic<long> forward_tokens{0};
   bool force_simt = false;       // testing: route bf16 GEMM/attention through SIMT kernels
+  bool force_simt_gemm = false;  // testing: SIMT GEMM only
+  bool force_simt_attn = false;  // testing: SIMT attention only
   int64_t launches = 0;          // kernels launched by run() (bench evidence)
 
  private:

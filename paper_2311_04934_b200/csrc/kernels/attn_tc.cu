@@ -333,7 +333,7 @@ __global__ void k_attn_combine(AttnParams p) {
     const int64_t slot = (static_cast<int64_t>(h) * p.splits + s) * BQ + qi;
     const float ls = p.part_ml[slot * 2 + 1];
     if (!(ls > 0.f)) continue;
-    const float w = exp2f(p.part_ml[slot * 2] - M);
+    const float w = exp2f((p.part_ml[slot * 2] - M) * p.scale_log2);  // maxima are raw scores
     num += w * p.part_o[slot * HD + x];
     den += w * ls;
   }

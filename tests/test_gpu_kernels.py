@@ -1,0 +1,92 @@
+"""Full-size (Llama-2-7B shape) properties of the sm_100a kernels where the CPU
+reference is far too slow to run: the tcgen05 GEMM and flash attention against the
+exact SIMT kernels, KV assembly byte-exactness, determinism, and cached serve ==
+block-causal oracle at 7B shape with reduced depth."""
+import numpy as np
+import pytest
+
+import paper_2311_04934_b200 as pcb
+from tests.util import BF16_REL, rel, same_greedy_token
+
+pytestmark = pytest.mark.gpu
+
+L7B = dict(n_layers=2, n_heads=32, head_dim=128, hidden=4096, vocab_size=32000, pos_encoding="rope",
+           max_position=8192, bytes_per_element=2, seed=42)
+
+
+@pytest.fixture(scope="module")
+def m7():
+    return pcb.Model(L7B, dtype=pcb.BF16)
+
+
+def test_tc_path_vs_simt_7b_shape(m7):
+    rng = np.random.default_rng(0)
+    t = rng.integers(0, 259, 4160)
+    p = np.arange(4160)
+    out = {}
+    for simt in (0, 1):
+        m7.set_option("force_simt", simt)
+        a, kv = m7.forward(t[:4096], p[:4096])          # 4096-row prefill (precompute shape)
+        b, _ = m7.forward(t[4096:], p[4096:], past=kv)  # 64-token suffix over the 4096-row cache
+        c, _ = m7.forward(t[:1], p[:1])
+        out[simt] = (a[-1], b, c)
+    m7.set_option("force_simt", 0)
+    for x, y in zip(out[0], out[1]):
+        assert rel(x, y) <= BF16_REL
+        x2, y2 = np.atleast_2d(x), np.atleast_2d(y)
+        assert all(same_greedy_token(a, b) for a, b in zip(x2, y2))
+
+
+@pytest.mark.parametrize("M", [1, 7, 16, 33, 64, 100, 128, 200, 256, 300])
+def test_gemm_token_counts(m7, M):
+    rng = np.random.default_rng(M)
+    t = rng.integers(0, 259, M)
+    p = np.arange(1000, 1000 + M)
+    a, _ = m7.forward(t, p)
+    m7.set_option("force_simt", 1)
+    b, _ = m7.forward(t, p)
+    m7.set_option("force_simt", 0)
+    assert rel(a, b) <= BF16_REL
+
+
+def test_deterministic(m7):
+    rng = np.random.default_rng(5)
+    t = rng.integers(0, 259, 64)
+    p = np.arange(64)
+    a, ka = m7.forward(t, p)
+    b, kb = m7.forward(t, p)
+    assert np.array_equal(a, b) and np.array_equal(ka.k(), kb.k())
+
+
+def test_cached_serve_equals_oracle_7b_shape(m7):
+    # 3 modules (incl. a union and a param), 4K cached rows, 64-token suffix
+    doc = "".join(chr(97 + (i * 7) % 26) for i in range(2000))
+    schema = pcb.Schema.parse(
+        f'<schema name="big"><module name="sys">{doc[:900]}</module><union><module name="u1">{doc[900:1700]}</module>'
+        f'<module name="u2">{doc[100:400]}</module></union><module name="q">Q: <param name="x" len="8"/> '
+        f'{doc[:1200]}</module></schema>')
+    store = pcb.ModuleStore(m7)
+    store.encode_schema(schema)
+    prompt = ('<prompt schema="big"><sys/><u1/><q><x>abc</x></q>' + ("What comes next in the text above" * 2)[:64]
+              + '</prompt>')
+    c = pcb.serve(store, schema, prompt, 4)
+    o = pcb.oracle_serve(m7, schema, prompt, 4)
+    assert rel(c.first_token_logits, o.first_token_logits) <= BF16_REL
+    assert same_greedy_token(c.first_token_logits, o.first_token_logits)
+    assert c.cache_report["cached_token_count"] > 2000
+
+
+def test_assembly_bytes_at_scale(m7):
+    # 3 modules x 1.3K rows at 7B width: byte-exact gather (the assembly kernel)
+    rng = np.random.default_rng(7)
+    kvs = []
+    start = 0
+    for n in (1300, 1400, 1500):
+        k = rng.standard_normal((2, n, 4096)).astype(np.float32)
+        v = rng.standard_normal((2, n, 4096)).astype(np.float32)
+        kvs.append((m7.upload_kv(k, v, np.arange(start, start + n)), k, v))
+        start += n
+    cat = pcb.concat_kv(m7, [x[0] for x in kvs])
+    assert np.array_equal(cat.positions(), np.arange(start))
+    want_k = np.concatenate([x[0].k() for x in kvs], axis=1)
+    assert np.array_equal(cat.k(), want_k)
