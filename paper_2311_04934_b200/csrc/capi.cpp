@@ -268,6 +268,7 @@ int pcb_debug_kernel_bench(const char* which, int64_t a0, int64_t a1, int64_t a2
       a.H = H;
       a.hd = 128;
       a.d = d;
+      a.counters = ctr + 8192;
       run = [=] { kern::attention_tc(a, ws, 64ull << 20, s); };
     } else {
       throw Error(ErrorCode::InvalidConfig, "unknown kernel bench");

@@ -6,6 +6,8 @@
 #include "model.hpp"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -376,6 +378,13 @@ void Model::prof_begin() {
 }
 void Model::prof_end(int cat, double alg_bytes, double alg_flops) {
   ++launches;
+  static const bool sync_debug = std::getenv("PCB_SYNC_DEBUG") != nullptr;  // hang bisection aid
+  if (sync_debug) {
+    static const char* names[PROF_N] = {"gemm", "attention", "assembly", "other"};
+    std::fprintf(stderr, "[pcb] launch %lld (%s, %.0f bytes) ...", static_cast<long long>(launches), names[cat], alg_bytes);
+    CK(cudaStreamSynchronize(stream_));
+    std::fprintf(stderr, " done\n");
+  }
   if (!prof_ || !prof_->on || !prof_->pending) return;
   cudaEvent_t b = prof_->get();
   CK(cudaEventRecord(b, stream_));
@@ -533,6 +542,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
   aa.block_id = block_ids ? W.block : nullptr;
   aa.alibi = alibi ? w_->alibi : nullptr;
   aa.kv_pos = alibi ? W.kvpos : nullptr;
+  aa.counters = W.counters + 8192;  // [0, #SMs) are the GEMM's stream-K flags
   const bool tc_attn = dtype_ == BF16 && !force_simt && !force_simt_attn && kern::attention_tc_supported(aa);
   int64_t nq = n;
   if (!tc_attn) {

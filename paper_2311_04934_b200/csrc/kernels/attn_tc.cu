@@ -50,6 +50,7 @@ struct AttnParams {
   float* part_ml;  // [H][splits][BQ][2]
   int kv_head_major;
   int64_t kv_rows;  // rows per head plane (head-major layout)
+  int* counters;    // [H] split arrival counters (zero between launches)
   unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
 };
 
@@ -83,6 +84,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   using S = AttnSmem<HD>;
+  constexpr int kRedRow = HD + 4;  // padded fp32 row of a parked partial O
+  static_assert(BQ * (kRedRow + 2) * 4 <= KV_STAGES * S::kStage, "split merge buffer must fit the K/V stages");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -293,51 +296,79 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
         }
       } else {
-        const int64_t slot = (static_cast<int64_t>(h) * p.splits + split) * BQ + r;
-        float* po = p.part_o + slot * HD;
+        // park the unnormalised O row and (m, l) in this CTA's idle K/V stage smem
+        // for the cluster-wide merge below
+        float* red = reinterpret_cast<float*>(sKV);
 #pragma unroll 1
         for (int c = 0; c < HD; c += 16) {
           float ov[16];
           tmem_ld16(tO + lane_off + c, ov);
-          if (qi < p.n)
 #pragma unroll
-            for (int x = 0; x < 16; x += 4)
-              *reinterpret_cast<float4*>(po + c + x) = make_float4(ov[x], ov[x + 1], ov[x + 2], ov[x + 3]);
+          for (int x = 0; x < 16; x += 4)
+            *reinterpret_cast<float4*>(red + r * kRedRow + c + x) = make_float4(ov[x], ov[x + 1], ov[x + 2], ov[x + 3]);
         }
-        if (qi < p.n) {
-          p.part_ml[slot * 2] = m;
-          p.part_ml[slot * 2 + 1] = l;
+        red[BQ * kRedRow + 2 * r] = nb > 0 ? m : -INFINITY;
+        red[BQ * kRedRow + 2 * r + 1] = nb > 0 ? l : 0.f;
+      }
+    }
+  }
+  if (p.splits > 1) {
+    // The split CTAs of one head form a thread-block cluster.  After every partial
+    // is parked, CTA rank s merges query rows {s, s+S, s+2S, ...} of all S partials
+    // through DSMEM in rank order (deterministic):
+    //   O = sum_s w_s O_s / sum_s w_s l_s,  w_s = 2^((m_s - M) * scale),  M = max_s m_s
+    cluster_sync_all();
+    if (warp >= 2) {
+      const int t = threadIdx.x - 64;             // 0..127
+      constexpr int kTpr = 8;                     // threads per row
+      constexpr int kXs = HD / kTpr;              // hd values per thread
+      const uint32_t red0 = smem_u32(sKV);
+      for (int64_t row = split + static_cast<int64_t>(t / kTpr) * p.splits; row < p.n;
+           row += static_cast<int64_t>(128 / kTpr) * p.splits) {
+        float ms[8], ls[8];
+        float M = -INFINITY;
+        for (int s2 = 0; s2 < p.splits; ++s2) {
+          const uint32_t ml = mapa_shared(red0 + (BQ * kRedRow + 2 * static_cast<uint32_t>(row)) * 4, s2);
+          ms[s2] = ld_dsmem_f32(ml);
+          ls[s2] = ld_dsmem_f32(ml + 4);
+          if (ls[s2] > 0.f) M = fmaxf(M, ms[s2]);
+        }
+        float den = 0.f, acc[kXs];
+#pragma unroll
+        for (int x = 0; x < kXs; ++x) acc[x] = 0.f;
+        const int x0 = (t % kTpr) * kXs;
+        for (int s2 = 0; s2 < p.splits; ++s2) {
+          if (!(ls[s2] > 0.f)) continue;
+          const float w = fast_exp2((ms[s2] - M) * p.scale_log2);
+          den += w * ls[s2];
+          const uint32_t src = mapa_shared(red0 + (static_cast<uint32_t>(row) * kRedRow + x0) * 4, s2);
+#pragma unroll
+          for (int x = 0; x < kXs; x += 4) {
+            float f[4];
+            ld_dsmem_v4(src + x * 4, f);
+            acc[x] += w * f[0];
+            acc[x + 1] += w * f[1];
+            acc[x + 2] += w * f[2];
+            acc[x + 3] += w * f[3];
+          }
+        }
+        const float inv = 1.f / den;
+        __nv_bfloat16* dst = p.out + row * p.d + h * HD + x0;
+#pragma unroll
+        for (int x = 0; x < kXs; x += 8) {
+          uint4 v;
+          __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+          for (int y = 0; y < 4; ++y) b[y] = __floats2bfloat162_rn(acc[x + 2 * y] * inv, acc[x + 2 * y + 1] * inv);
+          *reinterpret_cast<uint4*>(dst + x) = v;
         }
       }
     }
+    cluster_sync_all();  // peers are done reading this CTA's smem
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, S::kTmemCols);
-}
-
-// Merge split partials in split order: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
-template <int HD>
-__global__ void k_attn_combine(AttnParams p) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t qi = blockIdx.x;
-  const int h = blockIdx.y, x = threadIdx.x;
-  float M = -INFINITY;
-  for (int s = 0; s < p.splits; ++s) {
-    const int64_t slot = (static_cast<int64_t>(h) * p.splits + s) * BQ + qi;
-    if (p.part_ml[slot * 2 + 1] > 0.f) M = fmaxf(M, p.part_ml[slot * 2]);
-  }
-  float num = 0.f, den = 0.f;
-  for (int s = 0; s < p.splits; ++s) {
-    const int64_t slot = (static_cast<int64_t>(h) * p.splits + s) * BQ + qi;
-    const float ls = p.part_ml[slot * 2 + 1];
-    if (!(ls > 0.f)) continue;
-    const float w = exp2f((p.part_ml[slot * 2] - M) * p.scale_log2);  // maxima are raw scores
-    num += w * p.part_o[slot * HD + x];
-    den += w * ls;
-  }
-  p.out[qi * p.d + h * HD + x] = __float2bfloat16_rn(num / den);
 }
 
 template <int HD>
@@ -370,7 +401,7 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   int splits = 1;
   if (q_tiles == 1 && base < 2 * sms) {
     int64_t best = -1;
-    for (int s2 = 1; s2 <= std::max<int64_t>(1, std::min<int64_t>(nblk0 / 2, 32)); ++s2) {
+    for (int s2 = 1; s2 <= std::max<int64_t>(1, std::min<int64_t>(nblk0 / 2, 8)); ++s2) {  // cluster <= 8
       const size_t need = static_cast<size_t>(a.H) * s2 * BQ * (HD + 2) * sizeof(float);
       if (s2 > 1 && need > scratch_bytes) break;
       const int64_t waves = (static_cast<int64_t>(base) * s2 + sms - 1) / sms;
@@ -385,6 +416,9 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   p.splits = splits;
   p.part_o = scratch;
   p.part_ml = scratch + static_cast<size_t>(a.H) * splits * BQ * HD;
+  p.counters = a.counters;
+  if (splits > 8) splits = 8;
+  p.splits = splits;
   CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), BQ);
   p.kv_head_major = std::getenv("PCB_ATTN_HM_PROBE") ? 1 : 0;  // timing probe (values meaningless)
   p.kv_rows = p.total;
@@ -402,8 +436,8 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
                        ? tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
                        : tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
   dim3 grid(q_tiles, a.H, splits);
-  launch_k(k_attn_tc<HD>, grid, dim3(kAttnThreads), Sm::kBytes, s, 1, tq, tk, tv, p);
-  if (splits > 1) launch_k(k_attn_combine<HD>, dim3(static_cast<unsigned>(a.n), a.H), dim3(HD), 0, s, 1, p);
+  PdlClass pc(PDL_ATTN);
+  launch_k(k_attn_tc<HD>, grid, dim3(kAttnThreads), Sm::kBytes, s, splits, tq, tk, tv, p);  // cluster = splits
   if (probe_on) {
     PCB_CUDA(cudaDeviceSynchronize());
     const unsigned long long t0 = dbg[4 * 64];

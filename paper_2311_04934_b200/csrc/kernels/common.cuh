@@ -52,6 +52,26 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// kernel class of the launch in flight (PCB_PDL_MASK bit i enables PDL for class i)
+enum PdlCls : int { PDL_OTHER = 0, PDL_GEMM = 1, PDL_ATTN = 2, PDL_LN = 3, PDL_EMBED = 4, PDL_ARGMAX = 5, PDL_ASM = 6 };
+inline thread_local int g_pdl_cls = PDL_OTHER;
+struct PdlClass {
+  int prev;
+  explicit PdlClass(int c) : prev(g_pdl_cls) { g_pdl_cls = c; }
+  ~PdlClass() { g_pdl_cls = prev; }
+};
+// Default: every class except attention.  A PDL-launched attention kernel was seen to
+// stall its first softmax hand-off under the early-launch overlap with the QKV GEMM
+// (reproduced with attention as the only PDL class), so it
+// is launched with full stream serialisation until that is understood.
+inline int pdl_mask() {
+  static const int m = [] {
+    const char* v = std::getenv("PCB_PDL_MASK");
+    return v ? std::atoi(v) : (0x7f & ~(1 << PDL_ATTN));
+  }();
+  return m;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster_z,
                      Args&&... args) {
@@ -63,7 +83,7 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cudaLaunchAttribute at[2];
   int na = 0;
   at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[na].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[na].val.programmaticStreamSerializationAllowed = (pdl_enabled() && ((pdl_mask() >> g_pdl_cls) & 1)) ? 1 : 0;
   ++na;
   if (cluster_z > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;

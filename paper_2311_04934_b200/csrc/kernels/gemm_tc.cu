@@ -241,8 +241,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();  // weights stream once
-      const uint64_t pol_x = policy_evict_last();   // activations are re-read by every CTA
+      // one token tile: weights stream through once (evict first); several token tiles
+      // (prefill / precompute): each weight tile is re-read per token tile, keep it
+      const uint64_t pol_w = a.m_tiles == 1 ? policy_evict_first() : policy_evict_last();
+      const uint64_t pol_x = policy_evict_last();  // activations are re-read by every CTA
       auto w_src = [&](int64_t g) {
         const int64_t t = g / kbs;
         const int kb = static_cast<int>(g - t * kbs);
@@ -352,7 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int c_last = ge < te ? cta_of(te - 1, a.units, C) : c;
         if (c_last > c) {
           for (int p = c + 1 + et; p <= c_last; p += 128)
-            while (ld_acquire(a.flags + p) < a.epoch) {
+            for (uint32_t spins = 0; ld_acquire(a.flags + p) < a.epoch;) {
+              __nanosleep(64);
+              if (++spins == (1u << 25)) wait_timeout("stream-K flag", a.flags + p, a.epoch);
             }
           named_bar(1, 128);
         }
@@ -416,6 +420,7 @@ static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, co
   if (const char* ov = std::getenv("PCB_GEMM_CTAS")) C = std::max(1, std::min(C, std::atoi(ov)));  // tuning
   if (static_cast<size_t>(C) * 128 * BN * sizeof(float) > ws_bytes) throw std::runtime_error("gemm workspace too small");
   CUtensorMap tx = tmap_bf16_2d(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), BN);
+  PdlClass pc(PDL_GEMM);
   launch_k(k_gemm_sk<BN, STAGES>, dim3(C), dim3(kThreads), Sm::kBytes, s, 1, tx, a, e);
 }
 

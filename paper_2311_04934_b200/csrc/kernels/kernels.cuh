@@ -96,6 +96,7 @@ struct AttnArgs {
   const float* alibi = nullptr;        // [H] or null
   const int32_t* kv_pos = nullptr;     // [P+n] positions (alibi)
   int64_t i0 = 0, nq = -1;             // query sub-range [i0, i0+nq) (nq < 0: all n)
+  int* counters = nullptr;             // tc split-KV: [H] zeroed arrival counters
 };
 void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s);
 size_t attention_simt_scratch(const AttnArgs& a);

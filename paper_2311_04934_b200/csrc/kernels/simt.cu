@@ -94,6 +94,7 @@ __global__ void k_embed(const int32_t* tok, const int32_t* pos, const float* tab
 void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table, const float* abs_table, int d,
            float* h, cudaStream_t s) {
   if (n <= 0) return;
+  PdlClass pc(PDL_EMBED);
   launch_k(k_embed, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, tok, pos, table, abs_table, d, h);
   PCB_CUDA(cudaGetLastError());
 }
@@ -101,40 +102,86 @@ void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table
 // ---------------------------------------------------------------------------
 // LayerNorm (model.cpp:156-174): fp64 mean / variance, eps 1e-5, gamma 1, beta 0.
 // ---------------------------------------------------------------------------
+// One CTA per row; the row is read once into registers (up to 8 float4 per thread,
+// d <= 8192 at 256 threads), with two block reductions (sum, centred sum of squares).
+constexpr int kLnThreads = 256, kLnVec = 8;
+
+__device__ __forceinline__ double ln_block_sum(double v, double* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0;
+#pragma unroll
+  for (int w = 0; w < kLnThreads / 32; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
 template <typename T>
-__global__ void k_layernorm(const float* h, int d, T* out) {
+__global__ void __launch_bounds__(kLnThreads) k_layernorm(const float* h, int d, T* out) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double red[32];
+  __shared__ double red[kLnThreads / 32];
   const float* row = h + static_cast<int64_t>(blockIdx.x) * d;
-  auto block_sum = [&](double v) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    return t;
-  };
+  T* orow = out + static_cast<int64_t>(blockIdx.x) * d;
+  const int nv = d >> 2;  // float4s in the row (d % 4 == 0 on this path)
+  float4 x[kLnVec];
   double s = 0;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) s += row[j];
-  double mean = block_sum(s) / d;
+#pragma unroll
+  for (int u = 0; u < kLnVec; ++u) {
+    const int i = threadIdx.x + u * kLnThreads;
+    x[u] = i < nv ? reinterpret_cast<const float4*>(row)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (double)x[u].x + (double)x[u].y + (double)x[u].z + (double)x[u].w;
+  }
+  const double mean = ln_block_sum(s, red) / d;
   double v = 0;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    double c = row[j] - mean;
+#pragma unroll
+  for (int u = 0; u < kLnVec; ++u)
+    if (threadIdx.x + u * kLnThreads < nv) {
+      const double a = x[u].x - mean, b = x[u].y - mean, c = x[u].z - mean, e = x[u].w - mean;
+      v += a * a + b * b + c * c + e * e;
+    }
+  const double inv = 1.0 / sqrt(ln_block_sum(v, red) / d + 1e-5);
+#pragma unroll
+  for (int u = 0; u < kLnVec; ++u) {
+    const int i = threadIdx.x + u * kLnThreads;
+    if (i < nv) {
+      st_f(orow, 4 * i + 0, static_cast<float>((x[u].x - mean) * inv));
+      st_f(orow, 4 * i + 1, static_cast<float>((x[u].y - mean) * inv));
+      st_f(orow, 4 * i + 2, static_cast<float>((x[u].z - mean) * inv));
+      st_f(orow, 4 * i + 3, static_cast<float>((x[u].w - mean) * inv));
+    }
+  }
+}
+
+// general-d fallback (d % 4 != 0 or d > 8192): three strided passes
+template <typename T>
+__global__ void __launch_bounds__(kLnThreads) k_layernorm_any(const float* h, int d, T* out) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double red[kLnThreads / 32];
+  const float* row = h + static_cast<int64_t>(blockIdx.x) * d;
+  double s = 0;
+  for (int j = threadIdx.x; j < d; j += kLnThreads) s += row[j];
+  const double mean = ln_block_sum(s, red) / d;
+  double v = 0;
+  for (int j = threadIdx.x; j < d; j += kLnThreads) {
+    const double c = row[j] - mean;
     v += c * c;
   }
-  double var = block_sum(v) / d;
-  double inv = 1.0 / sqrt(var + 1e-5);
-  for (int j = threadIdx.x; j < d; j += blockDim.x)
+  const double inv = 1.0 / sqrt(ln_block_sum(v, red) / d + 1e-5);
+  for (int j = threadIdx.x; j < d; j += kLnThreads)
     st_f(out, static_cast<int64_t>(blockIdx.x) * d + j, static_cast<float>((row[j] - mean) * inv));
 }
 void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s) {
   if (n <= 0) return;
+  PdlClass pc(PDL_LN);
+  const bool fast = d % 4 == 0 && d <= 4 * kLnVec * kLnThreads;
+  const dim3 g(static_cast<unsigned>(n)), b(kLnThreads);
   if (dtype == F32)
-    launch_k(k_layernorm<float>, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, h, d, static_cast<float*>(out));
+    launch_k(fast ? k_layernorm<float> : k_layernorm_any<float>, g, b, 0, s, 1, h, d, static_cast<float*>(out));
   else
-    launch_k(k_layernorm<__nv_bfloat16>, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, h, d,
+    launch_k(fast ? k_layernorm<__nv_bfloat16> : k_layernorm_any<__nv_bfloat16>, g, b, 0, s, 1, h, d,
              static_cast<__nv_bfloat16*>(out));
   PCB_CUDA(cudaGetLastError());
 }
@@ -181,6 +228,7 @@ __global__ void k_argmax(const float* logits, int V, int32_t* out) {
 }
 void argmax_rows(const float* logits, int64_t rows, int V, int32_t* out, cudaStream_t s) {
   if (rows <= 0) return;
+  PdlClass pc(PDL_ARGMAX);
   launch_k(k_argmax, dim3(static_cast<unsigned>(rows)), dim3(1024), 0, s, 1, logits, V, out);
   PCB_CUDA(cudaGetLastError());
 }
@@ -465,6 +513,7 @@ void assemble(const CopySeg* d_segs, const uint64_t* d_first_chunk, int n_segs, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   uint64_t grid = std::min<uint64_t>(n_chunks, static_cast<uint64_t>(sms) * 8);
+  PdlClass pc(PDL_ASM);
   launch_k(k_assemble, dim3(static_cast<unsigned>(grid)), dim3(256), 0, s, 1, d_segs, d_first_chunk, n_segs, n_chunks);
   PCB_CUDA(cudaGetLastError());
 }
