@@ -362,6 +362,14 @@ def run_ours(a) -> None:
     gemm_ms_step = g["ms"] / a.steps
     gemm_bytes_step = g["bytes"] / a.steps
     achieved = gemm_bytes_step / (gemm_ms_step / 1e3) / 1e9
+    # DRAM traffic of the same GEMM launches from the committed ncu capture (profiles/)
+    traffic, traffic_src = None, None
+    import glob
+    tr = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), key=os.path.getmtime)
+    if tr and a.config == "c2":
+        with open(tr[-1]) as f:
+            t = json.load(f)
+        traffic, traffic_src = t.get("gemm_dram_bytes_per_step"), os.path.relpath(tr[-1], ROOT)
     classes = {k: {"ms_per_step": v["ms"] / a.steps, "launches_per_step": v["launches"] / a.steps,
                    "GB_per_step": v["bytes"] / a.steps / 1e9,
                    "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None,
@@ -416,7 +424,8 @@ def run_ours(a) -> None:
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "gemm_tc (tcgen05 swap-AB weight streaming, all GEMMs of a step)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": traffic, "traffic_unit": "bytes per step (all GEMM launches)",
+                         "traffic_source": traffic_src, "peak_source": peak_src,
                          "alg_bytes_per_step": gemm_bytes_step, "gemm_ms_per_step": gemm_ms_step,
                          "tensor_peak_tflops": tc_peak},
             "kernel_classes": classes,
