@@ -134,16 +134,22 @@ class ClockSampler:
 # distributed plumbing (one process per GPU; barrier + max over ranks)
 # ---------------------------------------------------------------------------
 class Dist:
-    def __init__(self):
+    """torch.distributed plumbing for the DP replicas: NCCL on the GPU box, gloo in the CPU tests
+    (tests/test_dist.py).  No collective touches the data path: requests are independent."""
+
+    def __init__(self, backend: str = "nccl"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
+        self.backend = backend
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(backend)
             self.dist, self.torch = dist, torch
 
     def barrier(self):
@@ -153,9 +159,15 @@ class Dist:
     def max(self, x: float) -> float:
         if self.world == 1:
             return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+    def requests(self, steps: int, n_prompts: int) -> list:
+        """Request ids this rank serves in the timed region: rank r takes the r-th stride of the
+        global request stream (weak scaling: `steps` requests per rank)."""
+        return [(self.rank * steps + i) % n_prompts for i in range(steps)]
 
     def close(self):
         if self.world > 1:
@@ -328,8 +340,8 @@ def run_ours(a) -> None:
     with ClockSampler(D.local) as clk:
         model.timer_start()
         dev_ms = 0.0
-        for i in range(a.steps):
-            r = pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1)
+        for i in D.requests(a.steps, len(parsed)):
+            r = pcb.serve(store, schema, parsed[i], max_new_tokens=1)
             ttfts.append(r.timings["ttft_us"] / 1e3)
             dev_ms += (r.timings["assemble_us"] + r.timings["prefill_device_us"]) / 1e3
         region_dev_ms = model.timer_stop()
@@ -343,8 +355,8 @@ def run_ours(a) -> None:
     D.barrier()
     model.sync()
     t1 = time.perf_counter()
-    for i in range(a.steps):
-        r = pcb.serve(store, schema, prompts[i % len(prompts)], max_new_tokens=1)
+    for i in D.requests(a.steps, len(prompts)):
+        r = pcb.serve(store, schema, prompts[i], max_new_tokens=1)
         _ = r.output_tokens[0]
     e2e_s = D.max(time.perf_counter() - t1)
     e2e_value = D.world * a.steps / e2e_s
