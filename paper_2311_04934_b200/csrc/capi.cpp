@@ -156,6 +156,8 @@ int pcb_model_set_option(pcb_model* m, const char* key, int64_t v) {
     else if (std::strcmp(key, "force_simt_gemm") == 0) m->m->force_simt_gemm = v != 0;
     else if (std::strcmp(key, "force_simt_attn") == 0) m->m->force_simt_attn = v != 0;
     else if (std::strcmp(key, "profile") == 0) m->m->set_profiling(v != 0);
+    else if (std::strcmp(key, "chain") == 0) m->m->use_chain = v != 0;
+    else if (std::strcmp(key, "chain_pf") == 0) kern::chain_set_prefetch(static_cast<int>(v));
     else throw Error(ErrorCode::InvalidConfig, std::string("unknown option ") + key);
   });
 }
@@ -220,6 +222,14 @@ int pcb_model_sync(pcb_model* m) {
 }
 
 // ---- kernel microbenchmarks (tuning aid; random bf16 operands on the device) ----
+int pcb_debug_gemm_probe(int64_t* shapes, unsigned long long* times, int max_launches, int* n_out) {
+  return guard([&] { *n_out = kern::gemm_probe_dump(shapes, times, max_launches); });
+}
+
+int pcb_debug_chain_probe(unsigned long long* times, int max_launches, int* n_out, int* phases_out) {
+  return guard([&] { *n_out = kern::chain_probe_dump(times, max_launches, phases_out); });
+}
+
 int pcb_debug_kernel_bench(const char* which, int64_t a0, int64_t a1, int64_t a2, int iters, double* us_out) {
   return guard([&] {
     cudaStream_t s;

@@ -142,6 +142,11 @@ struct Workspace {
   size_t attn_scratch_bytes = 0;
   int32_t* host_ints = nullptr;  // pinned staging
   int64_t host_ints_cap = 0;
+  unsigned long long chain_bar = 0;  // arrivals issued so far on the chain's grid-barrier counter
+  // counters layout (ints): [0, 8192) GEMM stream-K flags, [8192, 16384) attention split
+  // counters, [16384, 32768) chain stream-K flags, [32768, 32770) chain grid barrier (u64)
+  int* chain_flags() const { return counters + 16384; }
+  unsigned long long* chain_gbar() const { return reinterpret_cast<unsigned long long*>(counters + 32768); }
 
   ~Workspace() {
     for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)mask, (void*)h, x, q,
@@ -231,6 +236,7 @@ static uint64_t stream_seed(const std::string& name, uint64_t seed) {
 }
 
 Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtype), device_(device) {
+  if (const char* v = std::getenv("PCB_CHAIN")) use_chain = v[0] != '0';
   if (c.hidden != c.n_heads * c.head_dim) throw Error(ErrorCode::InvalidConfig, "hidden must equal n_heads * head_dim");
   if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 2 || c.head_dim % 2 != 0)
     throw Error(ErrorCode::InvalidConfig, "bad layer/head geometry");
@@ -471,6 +477,30 @@ void Model::validate(const int32_t* tokens, const int64_t* positions, int64_t n,
   if (kv.rows + n > kv.cap) throw Error(ErrorCode::ShapeMismatch, "KV block capacity exceeded");
 }
 
+static double gemm_alg_bytes(int dtype, int64_t M, int N, int K, int epi_kind) {
+  const double es = dtype == F32 ? 4.0 : 2.0;
+  const double out_b = epi_kind == kern::EPI_RESID ? 8.0 : (epi_kind == kern::EPI_F32 ? 4.0 : es);
+  return (double)N * K * es + (double)M * K * es + (double)M * N * out_b;
+}
+
+void Model::chain(const void* steps_v, int n_steps, const void* next) {
+  const auto* steps = static_cast<const kern::ChainStep*>(steps_v);
+  double bytes = 0, flops = 0;
+  for (int i = 0; i < n_steps; ++i) {
+    const auto& st = steps[i];
+    if (st.kind == kern::CHAIN_GEMM) {
+      bytes += gemm_alg_bytes(dtype_, st.M, st.N, st.K, st.e.kind);
+      flops += 2.0 * st.M * st.N * st.K;
+    } else {
+      bytes += 6.0 * st.M * st.ln_d;
+    }
+  }
+  prof_begin();
+  kern::chain_tc(steps, n_steps, static_cast<const kern::ChainStep*>(next), ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->chain_flags(), ws_->chain_gbar(),
+                 ws_->chain_bar, stream_);
+  prof_end(PROF_GEMM, bytes, flops);
+}
+
 void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi) {
   const auto& e = *static_cast<const kern::Epilogue*>(epi);
   prof_begin();
@@ -479,9 +509,7 @@ void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const vo
   else
     kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_, w_->packed);
   // algorithmic bytes: weights + activations in + outputs (residual: read + write fp32)
-  const double es = dtype_ == F32 ? 4.0 : 2.0;
-  const double out_b = e.kind == kern::EPI_RESID ? 8.0 : (e.kind == kern::EPI_F32 ? 4.0 : es);
-  prof_end(PROF_GEMM, (double)N * K * es + (double)M * K * es + (double)M * N * out_b, 2.0 * M * N * K);
+  prof_end(PROF_GEMM, gemm_alg_bytes(dtype_, M, N, K, e.kind), 2.0 * M * N * K);
 }
 
 void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBlock& kv, const uint8_t* mask,
@@ -554,10 +582,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     W.ensure_attn_scratch(64ull << 20);
   }
 
-  for (int l = 0; l < c.n_layers; ++l) {
-    prof_begin();
-    kern::layernorm(dtype_, W.h, n, d, W.x, s);
-    prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
+  auto qkv_epi = [&](int l) {
     kern::Epilogue e;
     e.kind = kern::EPI_QKV;
     e.d = d;
@@ -572,8 +597,20 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     e.rope_sin64 = w_->sin64;
     e.rope_cos32 = w_->cos32;
     e.rope_sin32 = w_->sin32;
-    gemm(W.x, w_->wqkv[l], n, 3 * d, d, &e);
+    return e;
+  };
+  kern::Epilogue eo;
+  eo.kind = kern::EPI_RESID;
+  eo.resid = W.h;
+  kern::Epilogue eg;
+  eg.kind = kern::EPI_GELU;
+  eg.out = W.mid;
+  kern::Epilogue ef;
+  ef.kind = kern::EPI_F32;
+  ef.outf = W.logits;
+  ef.ldo = c.vocab_size;
 
+  auto attention = [&](int l) {
     aa.k = kv.k(l);
     aa.v = kv.v(l);
     // algorithmic work: every visible key/value row read once, q in, out written
@@ -595,30 +632,84 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
       aa.i0 = 0;
       aa.nq = -1;
     }
+  };
 
-    kern::Epilogue eo;
-    eo.kind = kern::EPI_RESID;
-    eo.resid = W.h;
-    gemm(W.attn, w_->wo[l], n, d, d, &eo);
-    prof_begin();
-    kern::layernorm(dtype_, W.h, n, d, W.x, s);
-    prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
-    kern::Epilogue eg;
-    eg.kind = kern::EPI_GELU;
-    eg.out = W.mid;
-    gemm(W.x, w_->w1[l], n, 4 * d, d, &eg);
-    gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo);
-  }
-  if (logit_rows > 0) {
-    const int64_t r0 = n - logit_rows;
-    prof_begin();
-    kern::layernorm(dtype_, W.h + r0 * d, logit_rows, d, W.x, s);
-    prof_end(PROF_OTHER, (4.0 + es) * logit_rows * d, 0);
-    kern::Epilogue ef;
-    ef.kind = kern::EPI_F32;
-    ef.outf = W.logits;
-    ef.ldo = c.vocab_size;
-    gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
+  // Few-token regime (suffix prefill, decode): the GEMM/LayerNorm segments between two
+  // attention launches run as one persistent chain kernel each (chain_tc.cu), so the
+  // weight stream does not stop at GEMM boundaries.
+  const bool chain_now = use_chain && dtype_ == BF16 && w_->packed && !force_simt && !force_simt_gemm &&
+                         kern::chain_ln_supported(d) && kern::chain_tc_supported(n, 3 * d, d) &&
+                         kern::chain_tc_supported(n, 4 * d, d) && kern::chain_tc_supported(n, d, 4 * d) &&
+                         (logit_rows == 0 || kern::chain_tc_supported(logit_rows, c.vocab_size, d));
+  if (chain_now) {
+    auto ln = [&](const float* src, int64_t rows) {
+      kern::ChainStep st;
+      st.kind = kern::CHAIN_LN;
+      st.M = rows;
+      st.ln_src = src;
+      st.ln_dst = W.x;
+      st.ln_d = d;
+      return st;
+    };
+    auto mm = [&](const void* x, const void* w, int64_t M, int N, int K, const kern::Epilogue& e) {
+      kern::ChainStep st;
+      st.kind = kern::CHAIN_GEMM;
+      st.M = M;
+      st.x = x;
+      st.w = w;
+      st.N = N;
+      st.K = K;
+      st.e = e;
+      return st;
+    };
+    kern::ChainStep steps[8];
+    steps[0] = ln(W.h, n);
+    steps[1] = mm(W.x, w_->wqkv[0], n, 3 * d, d, qkv_epi(0));
+    kern::ChainStep next_o = mm(W.attn, w_->wo[0], n, d, d, eo);
+    chain(steps, 2, &next_o);
+    for (int l = 0; l < c.n_layers; ++l) {
+      attention(l);
+      int k = 0;
+      steps[k++] = mm(W.attn, w_->wo[l], n, d, d, eo);
+      steps[k++] = ln(W.h, n);
+      steps[k++] = mm(W.x, w_->w1[l], n, 4 * d, d, eg);
+      steps[k++] = mm(W.mid, w_->w2[l], n, d, 4 * d, eo);
+      if (l + 1 < c.n_layers) {
+        steps[k++] = ln(W.h, n);
+        steps[k++] = mm(W.x, w_->wqkv[l + 1], n, 3 * d, d, qkv_epi(l + 1));
+      } else if (logit_rows > 0) {
+        steps[k++] = ln(W.h + (n - logit_rows) * d, logit_rows);
+        steps[k++] = mm(W.x, w_->unembed, logit_rows, c.vocab_size, d, ef);
+      }
+      if (l + 1 < c.n_layers) {
+        next_o = mm(W.attn, w_->wo[l + 1], n, d, d, eo);
+        chain(steps, k, &next_o);
+      } else {
+        chain(steps, k, nullptr);
+      }
+    }
+  } else {
+    for (int l = 0; l < c.n_layers; ++l) {
+      prof_begin();
+      kern::layernorm(dtype_, W.h, n, d, W.x, s);
+      prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
+      kern::Epilogue e = qkv_epi(l);
+      gemm(W.x, w_->wqkv[l], n, 3 * d, d, &e);
+      attention(l);
+      gemm(W.attn, w_->wo[l], n, d, d, &eo);
+      prof_begin();
+      kern::layernorm(dtype_, W.h, n, d, W.x, s);
+      prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
+      gemm(W.x, w_->w1[l], n, 4 * d, d, &eg);
+      gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo);
+    }
+    if (logit_rows > 0) {
+      const int64_t r0 = n - logit_rows;
+      prof_begin();
+      kern::layernorm(dtype_, W.h + r0 * d, logit_rows, d, W.x, s);
+      prof_end(PROF_OTHER, (4.0 + es) * logit_rows * d, 0);
+      gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
+    }
   }
   kv.rows = total;
   kv.positions.insert(kv.positions.end(), positions, positions + n);

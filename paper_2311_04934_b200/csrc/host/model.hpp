@@ -125,11 +125,13 @@ class Model {
   bool force_simt = false;       // testing: route bf16 GEMM/attention through SIMT kernels
   bool force_simt_gemm = false;  // testing: SIMT GEMM only
   bool force_simt_attn = false;  // testing: SIMT attention only
+  bool use_chain = true;         // few-token GEMM/LN segments as one persistent chain kernel (PCB_CHAIN=0: off)
   int64_t launches = 0;          // kernels launched by run() (bench evidence)
 
  private:
   void validate(const int32_t* tokens, const int64_t* positions, int64_t n, const KVBlock& kv) const;
   void gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi);
+  void chain(const void* steps, int n_steps, const void* next);  // kern::ChainStep[n_steps], next chain's first
 
   ModelConfig cfg_;
   int dtype_, device_;

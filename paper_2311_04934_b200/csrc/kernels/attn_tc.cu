@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 2 * BKV;  // S buffers at columns [0, 64) and [64, 128)
-  pdl_trigger();
+  // No early trigger: a GEMM / chain launched programmatically after this kernel was
+  // seen to deadlock with it (the dependent's CTAs resident and waiting in
+  // griddepcontrol.wait while the attention grid never completed -- tools/pdl_bisect2.sh,
+  // test_cached_serve_equals_oracle_7b_shape), so dependents start at completion.
   pdl_wait();  // Q/K/V come from the QKV GEMM (and the assembly) just before
 
   if (warp == 0) {

@@ -1,0 +1,525 @@
+// Persistent chain of weight-streaming GEMM and LayerNorm phases for the few-token
+// (suffix prefill / decode) regime, one launch per transformer-layer segment:
+//
+//   [O_l (+resid), LN2_l, W1_l (+GELU), W2_l (+resid), LN1_{l+1}, QKV_{l+1} (+RoPE, K/V -> cache)]
+//
+// (reference Model::run, model.cpp:376-436; attention stays its own kernel between
+// two chains).  At 64 tokens every GEMM is HBM-bound on its weights, and as separate
+// launches each one paid a ramp (launch, prologue, first weight bytes) and a drain
+// (stream-K fix-up, epilogue, the slowest CTA) during which HBM idles: the measured
+// per-layer time was ~2.6x the weight-streaming time (tools/gemm_timeline.py).
+// Here the weight stream never stops at a phase boundary:
+//
+//   warp 0     W producer: bulk-copies the packed weight tiles of every phase in
+//              order; weights depend on nothing, so it runs ahead across phase
+//              boundaries, limited only by the shared-memory ring
+//   warp 1     TMEM allocator + MMA issuer (swap-AB 128 x BN x 16 UMMAs)
+//   warp 2     X producer: TMA-loads the activation tile of each unit, after the
+//              grid barrier that publishes the phase's input
+//   warps 3-6  epilogue (fused op, stream-K fix-up), LayerNorm rows, grid barrier
+//
+// Phases are separated by a grid-wide barrier (monotonic 64-bit arrival counter in
+// global memory, release/acquire at gpu scope, proxy fences on both sides because the
+// consumers read through TMA).  All CTAs are co-resident: the grid is one CTA per SM
+// and dependents are released (PDL trigger) only after the first barrier proves it.
+// Within a GEMM phase the work split is the stream-K split of gemm_tc.cu (equal
+// weight bytes per SM, deterministic fix-up in CTA order), with per-phase epochs and
+// a partial-tile workspace double-buffered by phase parity.
+#include <cuda.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+
+#include "gemm_common.cuh"
+
+namespace pcb::kern {
+
+CUtensorMap tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
+namespace {
+
+constexpr int kMaxPhases = 8;
+constexpr int kChainThreads = 224;  // 7 warps
+constexpr int kWTileC = 128 * 64 * 2;
+
+struct PhaseDev {
+  int kind;  // CHAIN_GEMM / CHAIN_LN
+  int N, K, kbs;
+  int64_t M, units;
+  const uint8_t* w;
+  const float* ln_src;
+  __nv_bfloat16* ln_dst;
+  int ln_d;
+  Epilogue e;
+};
+
+struct ChainParams {
+  CUtensorMap tm[kMaxPhases];  // activation maps of the GEMM phases
+  PhaseDev ph[kMaxPhases];
+  int n_phases;
+  int epoch0;
+  float* ws;               // [2][C][128][BN] fp32 partial tiles (phase parity)
+  int64_t ws_half;         // floats per parity half
+  int* flags;              // [C] partial-ready epochs
+  unsigned long long* gbar;  // grid barrier arrival counter (monotonic)
+  unsigned long long gbar_base;
+  int pf_units;              // L2 prefetch distance of the weight stream (units of 16 KB)
+  const uint8_t* next_w;     // first GEMM of the next chain (prefetched into L2 at the end)
+  int64_t next_units;
+  unsigned long long* tl;    // timeline probe [phase][cta][4] (null: off)
+};
+
+// probe events per (phase, CTA): 0 X producer past the phase's barrier, 1 MMA took the
+// phase's last stage, 2 epilogue done with the phase, 3 W producer issued the phase's
+// last weight tile
+__device__ __forceinline__ void ctl(const ChainParams& p, int ph, int ev) {
+  if (p.tl) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.tl[(static_cast<size_t>(ph) * 160 + blockIdx.x) * 12 + ev] = t;
+  }
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
+}
+
+// This CTA's weight units of every GEMM phase in stream order, then its units of the
+// next chain's first GEMM: the L2 prefetch cursor of the W producer.
+struct WCursor {
+  int ph;  // phase index; n_phases = the next chain's first GEMM; > n_phases = done
+  int64_t g, g1;
+  __device__ void settle(const ChainParams& p, int c, int C) {
+    while (ph <= p.n_phases && g >= g1) {
+      ++ph;
+      if (ph < p.n_phases) {
+        if (p.ph[ph].kind != CHAIN_GEMM) continue;
+        g = unit_begin(c, p.ph[ph].units, C);
+        g1 = unit_begin(c + 1, p.ph[ph].units, C);
+      } else if (ph == p.n_phases && p.next_w) {
+        g = unit_begin(c, p.next_units, C);
+        g1 = unit_begin(c + 1, p.next_units, C);
+      } else {
+        ph = p.n_phases + 1;
+      }
+    }
+  }
+  __device__ bool valid(const ChainParams& p) const { return ph <= p.n_phases; }
+  __device__ const uint8_t* addr(const ChainParams& p) const {
+    return (ph < p.n_phases ? p.ph[ph].w : p.next_w) + g * (128 * 64 * 2);
+  }
+};
+
+template <int BN, int STAGES>
+struct ChainSmem {
+  static constexpr int kStage = kWTileC + BN * 128;
+  static constexpr int kBytes = STAGES * kStage + 1024 + 1024;
+  static constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;
+};
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// wait until every CTA has finished phases [0, ph)
+__device__ __forceinline__ void grid_wait(const ChainParams& p, int ph) {
+  const unsigned long long target = p.gbar_base + static_cast<unsigned long long>(ph) * gridDim.x;
+  for (uint32_t spins = 0; ld_acquire_u64(p.gbar) < target;) {
+    __nanosleep(32);
+    if (++spins == (1u << 24)) {
+      printf("[pcb] chain grid barrier timeout: block %d thread %d phase %d/%d counter %llu target %llu\n", blockIdx.x,
+             threadIdx.x, ph, p.n_phases, ld_acquire_u64(p.gbar), target);
+      __trap();
+    }
+  }
+}
+
+__device__ __forceinline__ double ln_sum128(double v, double* red, int et) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((et & 31) == 0) red[et >> 5] = v;
+  named_bar(1, 128);
+  const double t = red[0] + red[1] + red[2] + red[3];
+  named_bar(1, 128);
+  return t;
+}
+
+// One LayerNorm row (model.cpp:156-174: fp64 mean, fp64 centred variance, eps 1e-5,
+// gamma 1, beta 0) by the 128 epilogue threads; d % 4 == 0, d <= 8192.
+__device__ void ln_row(const PhaseDev& P, int64_t r, double* red, int et) {
+  const int d = P.ln_d, nv = d >> 2;
+  const float4* src = reinterpret_cast<const float4*>(P.ln_src + r * d);
+  float4 x[16];
+  double s = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int i = et + u * 128;
+    x[u] = i < nv ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (double)x[u].x + (double)x[u].y + (double)x[u].z + (double)x[u].w;
+  }
+  const double mean = ln_sum128(s, red, et) / d;
+  double v = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u)
+    if (et + u * 128 < nv) {
+      const double a = x[u].x - mean, b = x[u].y - mean, c = x[u].z - mean, e = x[u].w - mean;
+      v += a * a + b * b + c * c + e * e;
+    }
+  const double inv = 1.0 / sqrt(ln_sum128(v, red, et) / d + 1e-5);
+  __nv_bfloat16* dst = P.ln_dst + r * d;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int i = et + u * 128;
+    if (i < nv) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(static_cast<float>((x[u].x - mean) * inv),
+                                                static_cast<float>((x[u].y - mean) * inv));
+      __nv_bfloat162 hi = __floats2bfloat162_rn(static_cast<float>((x[u].z - mean) * inv),
+                                                static_cast<float>((x[u].w - mean) * inv));
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dst + 4 * i) = pk;
+    }
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constant__ ChainParams p) {
+  using S = ChainSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  double* red = reinterpret_cast<double*>(acc_empty + 4);  // [4] LayerNorm partial sums
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = gridDim.x, c = blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2 && lane == 0)
+    for (int ph = 0; ph < p.n_phases; ++ph)
+      if (p.ph[ph].kind == CHAIN_GEMM) tma_prefetch(&p.tm[ph]);
+  if (warp == 1) tmem_alloc(tmem_slot, S::kCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- W producer: never waits for a phase boundary ----
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();
+      // L2 prefetch runs pf_units ahead of the bulk copies (and past the end of this
+      // chain into the next one), so HBM keeps streaming through phase boundaries and
+      // the attention launch between chains; the ring then refills at L2 speed.
+      WCursor pf{-1, 0, 0};
+      pf.settle(p, c, C);
+      int64_t issued = 0, prefetched = 0;
+      int it = 0;
+      for (int ph = 0; ph < p.n_phases; ++ph) {
+        const PhaseDev& P = p.ph[ph];
+        if (P.kind != CHAIN_GEMM) continue;
+        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
+        for (int64_t g = g0; g < g1; ++g, ++it, ++issued) {
+          for (; pf.valid(p) && prefetched < issued + p.pf_units; ++prefetched) {
+            if (prefetched >= issued + STAGES) prefetch_l2(pf.addr(p), kWTileC);  // the ring covers the first STAGES
+            ++pf.g;
+            pf.settle(p, c, C);
+          }
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], S::kStage);
+          // unit g = (n_tile, k-block): packed tiles of one 128-row block are contiguous along K
+          bulk_load(smem + s * S::kStage, P.w + g * kWTileC, kWTileC, &full[s], pol_w);
+        }
+        ctl(p, ph, 3);
+      }
+      for (; pf.valid(p) && prefetched < issued + p.pf_units; ++prefetched) {  // into the next chain
+        if (prefetched >= issued) prefetch_l2(pf.addr(p), kWTileC);
+        ++pf.g;
+        pf.settle(p, c, C);
+      }
+    }
+  } else if (warp == 2) {
+    // ---- X producer: activation tiles, after the phase's inputs are published ----
+    if (elect_one()) {
+      const uint64_t pol_x = policy_evict_last();  // re-read by every CTA
+      int it = 0;
+      for (int ph = 0; ph < p.n_phases; ++ph) {
+        const PhaseDev& P = p.ph[ph];
+        if (P.kind != CHAIN_GEMM) continue;
+        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
+        if (g0 == g1) continue;
+        ctl(p, ph, 6);
+        if (ph == 0) pdl_wait();
+        else grid_wait(p, ph);
+        ctl(p, ph, 7);
+        fence_proxy_async_global();  // generic-proxy stores of other CTAs -> our TMA reads
+        ctl(p, ph, 0);
+        for (int64_t g = g0; g < g1; ++g, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          const int kx = static_cast<int>(g % P.kbs) * 64;
+          tma_load_2d_hint(smem + s * S::kStage + kWTileC, &p.tm[ph], &full[s], kx, 0, pol_x);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      int it = 0, seg = 0;
+      for (int ph = 0; ph < p.n_phases; ++ph) {
+        const PhaseDev& P = p.ph[ph];
+        if (P.kind != CHAIN_GEMM) continue;
+        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
+        const int kbs = P.kbs;
+        for (int64_t g = g0; g < g1; ++seg) {
+          const int64_t ge = min(g1, (g / kbs + 1) * kbs);
+          const int buf = seg & 1;
+          mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t acc = tmem + buf * BN;
+          for (int64_t u = g; u < ge; ++u, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t wa = smem_u32(smem + s * S::kStage), xb = wa + kWTileC;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(acc, sw128_kmajor_desc(wa + k * 32), sw128_kmajor_desc(xb + k * 32), idesc,
+                        (u > g || k > 0) ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
+          umma_commit(&acc_full[buf]);
+          g = ge;
+        }
+        ctl(p, ph, 1);
+      }
+    }
+  } else {
+    // ---- epilogue warps 3..6 (TMEM lane quadrant = warp % 4) ----
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int et = threadIdx.x - 96;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    float v[16];
+    int seg = 0;
+    for (int ph = 0; ph < p.n_phases; ++ph) {
+      const PhaseDev& P = p.ph[ph];
+      if (ph == 0) {
+        pdl_wait();
+      } else {
+        if (et == 0) grid_wait(p, ph);
+        named_bar(1, 128);
+        if (ph == 1) pdl_trigger();  // every CTA is resident: dependents may launch
+      }
+      if (P.kind == CHAIN_LN) {
+        for (int64_t r = c; r < P.M; r += C) ln_row(P, r, red, et);
+      } else {
+        const Epilogue& e = P.e;
+        const int kbs = P.kbs;
+        const int64_t M = P.M;
+        const int epoch = p.epoch0 + ph;
+        float* ws = p.ws + (ph & 1) * p.ws_half;
+        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
+        for (int64_t g = g0; g < g1; ++seg) {
+          const int64_t t = g / kbs;
+          const int64_t tb = t * kbs, te = tb + kbs;
+          const int64_t ge = min(g1, te);
+          const int n = static_cast<int>(t) * 128 + row;
+          const int buf = seg & 1;
+          const uint32_t acc = tmem + buf * BN + lane_off;
+          EpiPre cur;
+          if (g == tb) epi_prefetch(e, n, P.N, 0, M, cur);
+          mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+          tc_fence_after();
+          if (et == 0) ctl(p, ph, 4);
+          if (g > tb) {
+            // tile started in an earlier CTA: park the partial for its owner
+            float* dst = ws + (static_cast<int64_t>(c) * 128 + row) * BN;
+#pragma unroll 1
+            for (int cc = 0; cc < BN; cc += 16) {
+              tmem_ld16(acc + cc, v);
+#pragma unroll
+              for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4*>(dst + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+            __threadfence();
+            named_bar(1, 128);
+            if (et == 0) st_release(p.flags + c, epoch);
+          } else {
+            const int c_last = ge < te ? cta_of(te - 1, P.units, C) : c;
+            if (c_last > c) {
+              for (int pp = c + 1 + et; pp <= c_last; pp += 128)
+                for (uint32_t spins = 0; has_units(pp, P.units, C) && ld_acquire(p.flags + pp) < epoch;) {
+                  __nanosleep(64);
+                  if (++spins == (1u << 25)) wait_timeout("chain stream-K flag", p.flags + pp, epoch);
+                }
+              named_bar(1, 128);
+            }
+            if (et == 0) ctl(p, ph, 5);
+            owner_finish<BN>(e, acc, n, P.N, M, ws, c, c_last, P.units, C, row, cur,
+                             (p.tl && et == 0) ? p.tl + (static_cast<size_t>(ph) * 160 + blockIdx.x) * 12 + 8 : nullptr);
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+          }
+          g = ge;
+        }
+      }
+      if (et == 0) ctl(p, ph, 2);
+      if (ph + 1 < p.n_phases) {
+        // publish this CTA's phase outputs: all epilogue stores -> one release arrival
+        named_bar(1, 128);
+        if (et == 0) {
+          __threadfence();
+          fence_proxy_async_global();
+          red_release_add_u64(p.gbar, 1ull);
+        }
+      }
+    }
+    if (p.n_phases == 1) pdl_trigger();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, S::kCols);
+}
+
+std::atomic<int> g_chain_epoch{0};
+int g_chain_pf = [] {
+  const char* v = std::getenv("PCB_CHAIN_PF");
+  return v ? std::max(0, std::atoi(v)) : 0;
+}();
+
+constexpr int kProbeMax = 256;
+unsigned long long* g_ctl = nullptr;
+int g_ctl_n = 0;
+int g_ctl_ph[kProbeMax];
+unsigned long long* chain_probe_slot(int n_phases) {
+  static const bool on = std::getenv("PCB_CHAIN_PROBE") != nullptr;
+  if (!on || g_ctl_n >= kProbeMax) return nullptr;
+  const size_t per = static_cast<size_t>(kMaxPhases) * 160 * 12;
+  if (!g_ctl) {
+    PCB_CUDA(cudaMallocManaged(&g_ctl, sizeof(unsigned long long) * per * kProbeMax));
+    std::memset(g_ctl, 0, sizeof(unsigned long long) * per * kProbeMax);
+  }
+  g_ctl_ph[g_ctl_n] = n_phases;
+  return g_ctl + per * g_ctl_n++;
+}
+
+template <int BN, int STAGES>
+void launch_chain(const ChainStep* steps, int n, const ChainStep* next, float* ws, size_t ws_bytes, int* flags, unsigned long long* gbar,
+                  unsigned long long& gbar_count, cudaStream_t s, int sms) {
+  using Sm = ChainSmem<BN, STAGES>;
+  static bool attr = [] {
+    PCB_CUDA(cudaFuncSetAttribute(k_chain<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
+    return true;
+  }();
+  (void)attr;
+  ChainParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n_phases = n;
+  const int C = sms;
+  for (int i = 0; i < n; ++i) {
+    const ChainStep& st = steps[i];
+    PhaseDev& d = p.ph[i];
+    d.kind = st.kind;
+    d.M = st.M;
+    if (st.kind == CHAIN_GEMM) {
+      d.N = st.N;
+      d.K = st.K;
+      d.kbs = st.K / 64;
+      d.units = static_cast<int64_t>(st.N / 128) * d.kbs;
+      d.w = static_cast<const uint8_t*>(st.w);
+      d.e = st.e;
+      p.tm[i] = tmap_bf16_2d(st.x, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.K), BN);
+    } else {
+      d.ln_src = st.ln_src;
+      d.ln_dst = static_cast<__nv_bfloat16*>(st.ln_dst);
+      d.ln_d = st.ln_d;
+    }
+  }
+  p.ws = ws;
+  p.ws_half = static_cast<int64_t>(C) * 128 * BN;
+  if (static_cast<size_t>(2 * p.ws_half) * sizeof(float) > ws_bytes) throw std::runtime_error("chain workspace too small");
+  p.flags = flags;
+  p.epoch0 = g_chain_epoch.fetch_add(n) + 1;
+  p.gbar = gbar;
+  p.gbar_base = gbar_count;
+  p.pf_units = g_chain_pf;
+  p.tl = chain_probe_slot(n);
+  if (next && next->kind == CHAIN_GEMM) {
+    p.next_w = static_cast<const uint8_t*>(next->w);
+    p.next_units = static_cast<int64_t>(next->N / 128) * (next->K / 64);
+  }
+  gbar_count += static_cast<unsigned long long>(n - 1) * C;  // one arrival per CTA per phase boundary
+  PdlClass pc(PDL_GEMM);
+  launch_k(k_chain<BN, STAGES>, dim3(C), dim3(kChainThreads), Sm::kBytes, s, 1, p);
+}
+
+}  // namespace
+
+bool chain_tc_supported(int64_t M, int N, int K) { return M >= 1 && M <= 128 && weight_packable(N, K); }
+bool chain_ln_supported(int d) { return d % 4 == 0 && d <= 8192; }
+void chain_set_prefetch(int units) { g_chain_pf = std::max(0, units); }
+
+int chain_probe_dump(unsigned long long* times, int max_launches, int* phases) {
+  PCB_CUDA(cudaDeviceSynchronize());
+  const int n = std::min(g_ctl_n, max_launches);
+  const size_t per = static_cast<size_t>(kMaxPhases) * 160 * 12;
+  if (n > 0) std::memcpy(times, g_ctl, sizeof(unsigned long long) * per * n);
+  for (int i = 0; i < n; ++i) phases[i] = g_ctl_ph[i];
+  if (g_ctl) std::memset(g_ctl, 0, sizeof(unsigned long long) * per * kProbeMax);
+  g_ctl_n = 0;
+  return n;
+}
+
+void chain_tc(const ChainStep* steps, int n_steps, const ChainStep* next, float* ws, size_t ws_bytes, int* flags,
+              unsigned long long* gbar, unsigned long long& gbar_count, cudaStream_t s) {
+  if (n_steps <= 0) return;
+  if (n_steps > kMaxPhases) throw std::runtime_error("chain: too many phases");
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  int64_t M = 1;
+  for (int i = 0; i < n_steps; ++i) {
+    const ChainStep& st = steps[i];
+    if (st.kind == CHAIN_GEMM && !chain_tc_supported(st.M, st.N, st.K))
+      throw std::runtime_error("chain: unsupported GEMM shape");
+    if (st.kind == CHAIN_LN && !chain_ln_supported(st.ln_d)) throw std::runtime_error("chain: unsupported LN width");
+    M = std::max<int64_t>(M, st.M);
+  }
+  if (M <= 16) launch_chain<16, 10>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else if (M <= 32) launch_chain<32, 10>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else if (M <= 64) launch_chain<64, 8>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else launch_chain<128, 6>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+}
+
+}  // namespace pcb::kern

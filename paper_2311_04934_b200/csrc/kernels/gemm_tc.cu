@@ -21,12 +21,14 @@
 #include <cuda.h>
 
 #include <atomic>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
 
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "gemm_common.cuh"
 
 namespace pcb::kern {
 
@@ -95,83 +97,6 @@ void pack_weight_bf16(const void* src, void* dst, int N, int K, cudaStream_t s) 
   PCB_CUDA(cudaGetLastError());
 }
 
-// ---------------------------------------------------------------------------
-// Epilogue on one thread's weight row n for 16 consecutive tokens [m0, m0+16),
-// split into a prefetch (global loads that do not depend on the accumulator:
-// residual rows, RoPE cos/sin) and the apply step, so the loads of the next
-// chunk are in flight while the current one is processed.
-// ---------------------------------------------------------------------------
-struct EpiPre {
-  float a[16], b[16];
-};
-
-__device__ __forceinline__ void epi_prefetch(const Epilogue& e, int n, int N, int64_t m0, int64_t M, EpiPre& p) {
-  if (e.kind == EPI_RESID) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) p.a[j] = (m0 + j < M) ? e.resid[(m0 + j) * N + n] : 0.f;
-  } else if (e.kind == EPI_QKV) {
-    const int seg = n / e.d, c = n - seg * e.d;
-    if (seg < 2 && e.rope) {
-      const int half = e.head_dim >> 1, pi = (c % e.head_dim) >> 1;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int64_t pos = (m0 + j < M) ? e.pos[m0 + j] : 0;
-        p.a[j] = e.rope_cos32[pos * half + pi];
-        p.b[j] = e.rope_sin32[pos * half + pi];
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void epi_chunk(const Epilogue& e, int n, int N, int64_t m0, int64_t M, float* v,
-                                          const EpiPre& pre) {
-  if (e.kind == EPI_QKV) {
-    const int seg = n / e.d, c = n - seg * e.d;
-    const bool rot = seg < 2 && e.rope;
-    const bool odd = c & 1;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      float pv = __shfl_xor_sync(0xffffffffu, v[j], 1);  // partner column n^1 lives in lane^1
-      if (rot) v[j] = odd ? (pv * pre.b[j] + v[j] * pre.a[j]) : (v[j] * pre.a[j] - pv * pre.b[j]);
-    }
-    __nv_bfloat16* dst = seg == 0 ? static_cast<__nv_bfloat16*>(e.q_out)
-                                  : static_cast<__nv_bfloat16*>(seg == 1 ? e.k_out : e.v_out) + e.kv_row0 * e.d;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (m0 + j < M) dst[(m0 + j) * e.d + c] = __float2bfloat16_rn(v[j]);
-    return;
-  }
-  if (e.kind == EPI_NONE) return;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int64_t m = m0 + j;
-    if (m >= M) break;
-    if (e.kind == EPI_RESID) {
-      e.resid[m * N + n] = pre.a[j] + v[j];
-    } else if (e.kind == EPI_GELU) {
-      static_cast<__nv_bfloat16*>(e.out)[m * N + n] = __float2bfloat16_rn(gelu_fast(v[j]));
-    } else {
-      e.outf[m * e.ldo + n] = v[j];
-    }
-  }
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 constexpr int kThreads = 192;
 constexpr int kWTile = 128 * 64 * 2;  // one packed weight tile
 
@@ -191,20 +116,19 @@ struct SkArgs {
   float* ws;  // [gridDim.x][128][BN] partial tiles
   int* flags; // [gridDim.x] epoch flags
   const uint8_t* x_bulk_probe = nullptr;
+  unsigned long long* tl = nullptr;  // timeline probe: [cta][4] globaltimer ns (PCB_GEMM_PROBE)
 };
 
-__device__ __forceinline__ int64_t unit_begin(int c, int64_t U, int C) { return static_cast<int64_t>(c) * U / C; }
-
-// CTA whose unit range contains unit g
-__device__ __forceinline__ int cta_of(int64_t g, int64_t U, int C) {
-  int c = static_cast<int>((g * C) / U);
-  while (c + 1 < C && unit_begin(c + 1, U, C) <= g) ++c;
-  while (c > 0 && unit_begin(c, U, C) > g) --c;
-  return c;
+__device__ __forceinline__ void tl_mark(const SkArgs& a, int ev) {
+  if (a.tl) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.tl[blockIdx.x * 4 + ev] = t;
+  }
 }
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_gemm_sk(const __grid_constant__ CUtensorMap tmX, SkArgs a, Epilogue e) {
   using S = SkSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -219,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int C = gridDim.x, c = blockIdx.x;
   const int64_t g0 = unit_begin(c, a.units, C), g1 = unit_begin(c + 1, a.units, C);
   const int kbs = a.kbs;
+  if (threadIdx.x == 0) tl_mark(a, 0);  // entry
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
@@ -298,7 +223,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t acc = tmem + buf * BN;
         for (int64_t u = g; u < ge; ++u, ++it) {
           const int s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
+          for (uint32_t sp = 0; !mbar_try(&full[s], (it / STAGES) & 1);)
+            if (++sp == (1u << 25)) {
+              printf("[pcb] gemm stage timeout: block %d/%d it %d/%lld M %lld N %d K %d BN %d epoch %d\n", blockIdx.x,
+                     gridDim.x, it, (long long)(g1 - g0), (long long)a.M, a.N, a.K, BN, a.epoch);
+              __trap();
+            }
+          if (it == 0) tl_mark(a, 1);             // first stage landed
+          if (u + 1 == g1) tl_mark(a, 2);         // last stage landed
           tc_fence_after();
           const uint32_t wa = smem_u32(smem + s * S::kStage), xb = wa + kWTile;
 #pragma unroll
@@ -329,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t m0 = static_cast<int64_t>(m_tile) * BN;
       const int buf = seg & 1;
       const uint32_t acc = tmem + buf * BN + lane_off;
-      EpiPre cur, nxt;
+      EpiPre cur;
       if (g == tb) epi_prefetch(e, n, a.N, m0, a.M, cur);  // before the accumulator is ready
       mbar_wait(&acc_full[buf], (seg >> 1) & 1);
       tc_fence_after();
@@ -360,24 +292,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           named_bar(1, 128);
         }
+        if (a.m_tiles == 1) {
+          owner_finish<BN>(e, acc, n, a.N, a.M, a.ws, c, c_last, a.units, C, row, cur);
+        } else {
+          // several token tiles (prefill): chunked, the token offset m0 applies
+          EpiPre nxt;
 #pragma unroll 1
-        for (int cc = 0; cc < BN; cc += 16) {
-          if (m0 + cc >= a.M) break;  // warp-uniform
-          if (cc + 16 < BN && m0 + cc + 16 < a.M) epi_prefetch(e, n, a.N, m0 + cc + 16, a.M, nxt);
-          tmem_ld16(acc + cc, v);
-          for (int p = c + 1; p <= c_last; ++p) {
-            const float* src = a.ws + (static_cast<int64_t>(p) * 128 + row) * BN + cc;
+          for (int cc = 0; cc < BN; cc += 16) {
+            if (m0 + cc >= a.M) break;  // warp-uniform
+            if (cc + 16 < BN && m0 + cc + 16 < a.M) epi_prefetch(e, n, a.N, m0 + cc + 16, a.M, nxt);
+            tmem_ld16(acc + cc, v);
+            for (int p = c + 1; p <= c_last; ++p) {
+              const float* src = a.ws + (static_cast<int64_t>(p) * 128 + row) * BN + cc;
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 f = __ldcg(reinterpret_cast<const float4*>(src + j));
-              v[j] += f.x;
-              v[j + 1] += f.y;
-              v[j + 2] += f.z;
-              v[j + 3] += f.w;
+              for (int j = 0; j < 16; j += 4) {
+                const float4 f = __ldcg(reinterpret_cast<const float4*>(src + j));
+                v[j] += f.x;
+                v[j + 1] += f.y;
+                v[j + 2] += f.z;
+                v[j + 3] += f.w;
+              }
             }
+            epi_chunk(e, n, a.N, m0 + cc, a.M, v, cur);
+            cur = nxt;
           }
-          epi_chunk(e, n, a.N, m0 + cc, a.M, v, cur);
-          cur = nxt;
         }
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
@@ -387,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) tl_mark(a, 3);  // epilogue done
   if (warp == 1) tmem_dealloc(tmem, S::kCols);
 }
 
@@ -395,12 +334,47 @@ bool gemm_tc_supported(int64_t M, int N, int K) { return M >= 1 && weight_packab
 // one launch counter for every instantiation: all of them share a model's flag array
 static std::atomic<int> g_sk_epoch{0};
 
-template <int BN, int STAGES>
+// ---- timeline probe (PCB_GEMM_PROBE=1): per launch, per CTA {entry, first stage landed,
+// last stage landed, done} in globaltimer ns, plus the launch shape ----
+namespace {
+constexpr int kProbeLaunches = 1024, kProbeCtas = 160;
+unsigned long long* g_tl = nullptr;
+int g_tl_n = 0;
+int64_t g_tl_shape[kProbeLaunches][4];
+unsigned long long* probe_slot(int64_t M, int N, int K, int C) {
+  static const bool on = std::getenv("PCB_GEMM_PROBE") != nullptr;
+  if (!on) return nullptr;
+  if (!g_tl) {
+    PCB_CUDA(cudaMallocManaged(&g_tl, sizeof(unsigned long long) * kProbeLaunches * kProbeCtas * 4));
+    std::memset(g_tl, 0, sizeof(unsigned long long) * kProbeLaunches * kProbeCtas * 4);
+  }
+  if (g_tl_n >= kProbeLaunches) return nullptr;
+  g_tl_shape[g_tl_n][0] = M;
+  g_tl_shape[g_tl_n][1] = N;
+  g_tl_shape[g_tl_n][2] = K;
+  g_tl_shape[g_tl_n][3] = C;
+  return g_tl + static_cast<size_t>(g_tl_n++) * kProbeCtas * 4;
+}
+}  // namespace
+
+int gemm_probe_dump(int64_t* shapes, unsigned long long* times, int max_launches) {
+  PCB_CUDA(cudaDeviceSynchronize());
+  const int n = std::min(g_tl_n, max_launches);
+  for (int i = 0; i < n; ++i) {
+    std::memcpy(shapes + i * 4, g_tl_shape[i], sizeof(int64_t) * 4);
+    std::memcpy(times + static_cast<size_t>(i) * kProbeCtas * 4, g_tl + static_cast<size_t>(i) * kProbeCtas * 4,
+                sizeof(unsigned long long) * kProbeCtas * 4);
+  }
+  g_tl_n = 0;
+  return n;
+}
+
+template <int BN, int STAGES, int MINB = 1>
 static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, const Epilogue& e, float* ws,
                       size_t ws_bytes, int* flags, cudaStream_t s, int sms) {
   using Sm = SkSmem<BN, STAGES>;
   static bool attr = [] {
-    PCB_CUDA(cudaFuncSetAttribute(k_gemm_sk<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
+    PCB_CUDA(cudaFuncSetAttribute(k_gemm_sk<BN, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
     return true;
   }();
   (void)attr;
@@ -419,9 +393,10 @@ static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, co
   int C = static_cast<int>(std::min<int64_t>(sms, a.units));
   if (const char* ov = std::getenv("PCB_GEMM_CTAS")) C = std::max(1, std::min(C, std::atoi(ov)));  // tuning
   if (static_cast<size_t>(C) * 128 * BN * sizeof(float) > ws_bytes) throw std::runtime_error("gemm workspace too small");
+  a.tl = probe_slot(M, N, K, C);
   CUtensorMap tx = tmap_bf16_2d(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), BN);
   PdlClass pc(PDL_GEMM);
-  launch_k(k_gemm_sk<BN, STAGES>, dim3(C), dim3(kThreads), Sm::kBytes, s, 1, tx, a, e);
+  launch_k(k_gemm_sk<BN, STAGES, MINB>, dim3(C), dim3(kThreads), Sm::kBytes, s, 1, tx, a, e);
 }
 
 void gemm_tc(const void* A, const void* Wp, int64_t M, int N, int K, const Epilogue& e, float* ws, size_t ws_bytes,
@@ -433,6 +408,10 @@ void gemm_tc(const void* A, const void* Wp, int64_t M, int N, int K, const Epilo
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
+  // (Tried: weight-streaming shapes sized for two co-resident CTAs per SM so the next
+  // PDL-launched GEMM overlaps this one's drain -- measured slower, 8.1 vs 6.6 ms per 7B
+  // request: shallower pipelines and uneven CTA placement.  The few-token path is the
+  // persistent chain kernel, chain_tc.cu.)
   if (M <= 16) launch_sk<16, 10>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
   else if (M <= 32) launch_sk<32, 10>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
   else if (M <= 64) launch_sk<64, 8>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);

@@ -77,8 +77,37 @@ void gemm_simt(int dtype, const void* A, const void* W, int64_t M, int N, int K,
 // tcgen05 persistent stream-K GEMM (bf16 in, fp32 accumulate) over PACKED weights.
 // Requires K%64==0, N%128==0.  workspace >= 148*128*256*4 bytes; flags >= #SMs ints (zeroed once).
 bool gemm_tc_supported(int64_t M, int N, int K);
+// debug: GEMM timeline probe (PCB_GEMM_PROBE=1); shapes [n][4] = {M,N,K,ctas}, times [n][160][4]
+int gemm_probe_dump(int64_t* shapes, unsigned long long* times, int max_launches);
 void gemm_tc(const void* A, const void* W_packed, int64_t M, int N, int K, const Epilogue& e, float* workspace,
              size_t workspace_bytes, int* flags, cudaStream_t s);
+
+// ---- persistent GEMM / LayerNorm chain (few-token regime, M <= 128) ----
+// One launch runs the phases in order with a grid barrier between them; the packed
+// weights of later phases stream in while earlier phases finish (chain_tc.cu).
+enum ChainKind : int { CHAIN_GEMM = 0, CHAIN_LN = 1 };
+struct ChainStep {
+  int kind = CHAIN_GEMM;
+  int64_t M = 0;             // rows (tokens)
+  const void* x = nullptr;   // GEMM: activations [M][K] bf16
+  const void* w = nullptr;   // GEMM: packed weights [N][K]
+  int N = 0, K = 0;
+  Epilogue e;                // GEMM epilogue
+  const float* ln_src = nullptr;  // LN: fp32 rows [M][ln_d]
+  void* ln_dst = nullptr;         // LN: bf16 rows [M][ln_d]
+  int ln_d = 0;
+};
+bool chain_tc_supported(int64_t M, int N, int K);
+bool chain_ln_supported(int d);
+void chain_set_prefetch(int units);  // L2 prefetch distance (16 KB units; 0 = off)
+// debug: chain timeline probe (PCB_CHAIN_PROBE=1): times [n][8 phases][160 CTAs][4]
+int chain_probe_dump(unsigned long long* times, int max_launches, int* phases);
+// flags: >= #SMs ints (zeroed once, private to the chain); gbar: one zeroed u64 whose
+// arrival count the caller tracks in gbar_count (advanced by this call).
+// next: the first step of the chain that follows (its weights are prefetched into L2
+// at the end of this one), or null.
+void chain_tc(const ChainStep* steps, int n_steps, const ChainStep* next, float* ws, size_t ws_bytes, int* flags,
+              unsigned long long* gbar, unsigned long long& gbar_count, cudaStream_t s);
 
 // ---- attention over a KV cache ----
 // q [n][d]; K/V layer bases [rows][d]; query i (sequence index P+i) attends keys

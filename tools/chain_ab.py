@@ -1,0 +1,127 @@
+"""A/B of few-token forward variants inside ONE process (box-to-box noise is ~10%), plus a
+timeline of the persistent chain kernel for one 7B-shape cached request.
+
+  python tools/chain_ab.py [rounds]
+Variants are model options (set_option): chain on/off, chain L2 prefetch distance.
+"""
+import ctypes as C
+import os
+import statistics
+import sys
+
+os.environ.setdefault("PCB_CHAIN_PROBE", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import numpy as np  # noqa: E402
+
+import paper_2311_04934_b200 as pcb  # noqa: E402
+
+L = pcb.lib()
+L.pcb_debug_chain_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_void_p]
+MAXL = 256
+times = np.zeros((MAXL, 8, 160, 12), np.uint64)
+phases = np.zeros(MAXL, np.int32)
+
+
+def dump():
+    n = C.c_int()
+    rc = L.pcb_debug_chain_probe(times.ctypes.data, MAXL, C.byref(n), phases.ctypes.data)
+    assert rc == 0, L.pcb_last_error()
+    return n.value
+
+
+VARIANTS = [
+    ("per-GEMM kernels", {"chain": 0}),
+    ("chain", {"chain": 1, "chain_pf": 0}),
+]
+if os.environ.get("AB_VARIANTS"):
+    VARIANTS = [v for v in VARIANTS if v[0] in os.environ["AB_VARIANTS"].split(",")]
+
+rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+layers = int(os.environ.get("PROF_LAYERS", "32"))
+cfg = dict(bench.CFG_7B, n_layers=layers)
+schema_text, prompts = bench.workload(4096, 64, 1)
+m = pcb.Model(cfg, dtype=pcb.BF16)
+s = pcb.Schema.parse(schema_text)
+st = pcb.ModuleStore(m)
+st.encode_schema(s)
+parsed = [pcb.Prompt.parse(p) for p in prompts]
+res = {name: [] for name, _ in VARIANTS}
+for r in range(rounds):
+    for name, opts in VARIANTS:
+        for k, v in opts.items():
+            m.set_option(k, v)
+        pcb.serve(st, s, parsed[0], max_new_tokens=1)  # settle
+        for i in range(3):
+            rr = pcb.serve(st, s, parsed[(i + 1) % len(parsed)], max_new_tokens=1)
+            res[name].append(rr.timings["ttft_us"] / 1e3)
+        dump()
+print("TTFT ms (median / min over", rounds * 3, "requests)")
+for name, v in res.items():
+    print(f"  {name:18s} {statistics.median(v):7.3f} {min(v):7.3f}")
+
+# ---- chain timeline of one request ----
+m.set_option("chain", 1)
+m.set_option("chain_pf", int(os.environ.get("TL_PF", "0")))
+pcb.serve(st, s, parsed[0], max_new_tokens=1)
+m.sync()
+dump()
+pcb.serve(st, s, parsed[1], max_new_tokens=1)
+n = dump()
+names6 = ["O", "LN2", "W1", "W2", "LN1", "QKV"]
+print(f"chain launches {n}")
+agg = {}
+prev_end = None
+for i in range(n):
+    npn = int(phases[i])
+    t = times[i, :npn, :148].astype(np.int64)  # [ph][cta][ev]
+    names = ["LN1", "QKV"] if npn == 2 else names6[:npn]
+    for ph in range(npn):
+        ev = t[ph]
+        done = ev[:, 2]
+        start_x = ev[:, 0]
+        row = {}
+        if ph > 0:
+            prev_done_max = t[ph - 1][:, 2].max()
+            row["barrier"] = (np.median(start_x[start_x > 0]) - prev_done_max) / 1e3 if (start_x > 0).any() else None
+        row["done_spread"] = (done.max() - done.min()) / 1e3
+        if (start_x > 0).any():
+            mma_end = ev[:, 1]
+            ok = (start_x > 0) & (mma_end > 0)
+            row["stream"] = np.median((mma_end - start_x)[ok]) / 1e3
+            row["epi_tail"] = np.median((done - mma_end)[ok]) / 1e3
+            row["w_lead"] = np.median((start_x - ev[:, 3])[ok]) / 1e3  # >0: weights issued before barrier passed
+        if (start_x > 0).any():
+            okk = (ev[:, 6] > 0) & (ev[:, 7] > 0)
+            row["poll"] = np.median((ev[:, 7] - ev[:, 6])[okk]) / 1e3
+            row["proxyfence"] = np.median((ev[:, 0] - ev[:, 7])[okk]) / 1e3
+            row["pass_minus_lastdone"] = (np.median(ev[:, 7][okk]) - (t[ph - 1][:, 2].max() if ph > 0 else 0)) / 1e3 if ph > 0 else None
+            ok4 = (ev[:, 4] > 0) & (ev[:, 1] > 0)
+            row["accwait_after_mma"] = np.median((ev[:, 4] - ev[:, 1])[ok4]) / 1e3
+            ok5 = (ev[:, 5] > 0) & (ev[:, 4] > 0)
+            if ok5.any():
+                row["flagwait"] = np.median((ev[:, 5] - ev[:, 4])[ok5]) / 1e3
+                row["owner_epi"] = np.median((ev[:, 2] - ev[:, 5])[ok5]) / 1e3
+                ok8 = ok5 & (ev[:, 8] > 0) & (ev[:, 11] > 0)
+                if ok8.any():
+                    row["o_tmem"] = np.median((ev[:, 8] - ev[:, 5])[ok8]) / 1e3
+                    row["o_partials"] = np.median((ev[:, 9] - ev[:, 8])[ok8]) / 1e3
+                    row["o_epi_g0"] = np.median((ev[:, 10] - ev[:, 9])[ok8]) / 1e3
+                    row["o_rest"] = np.median((ev[:, 11] - ev[:, 10])[ok8]) / 1e3
+                    row["o_after"] = np.median((ev[:, 2] - ev[:, 11])[ok8]) / 1e3
+        row["phase_span"] = (done.max() - (t[ph - 1][:, 2].max() if ph > 0 else t[0][:, 2].min())) / 1e3
+        agg.setdefault((npn, names[ph]), []).append(row)
+    first = t[0][:, 0]
+    first = first[first > 0]
+    if prev_end is not None and len(first):
+        agg.setdefault(("gap", "attention+launch"), []).append({"gap": (first.min() - prev_end) / 1e3})
+    prev_end = t[npn - 1][:, 2].max()
+print("per phase (median over chains), us")
+for key, rows in agg.items():
+    keys = sorted({k for r_ in rows for k in r_})
+    out = []
+    for k in keys:
+        vals = [r_[k] for r_ in rows if r_.get(k) is not None]
+        if vals:
+            out.append(f"{k} {statistics.median(vals):6.1f}")
+    print(f"  {str(key):28s} x{len(rows):3d}  " + "  ".join(out))
