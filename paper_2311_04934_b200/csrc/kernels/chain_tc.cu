@@ -134,7 +134,7 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
 // wait until every CTA has finished phases [0, ph)
 __device__ __forceinline__ void grid_wait(const ChainParams& p, int ph) {
   const unsigned long long target = p.gbar_base + static_cast<unsigned long long>(ph) * gridDim.x;
-  for (uint32_t spins = 0; ld_acquire_u64(p.gbar) < target;) {
+  for (uint32_t spins = 0; ld_relaxed_u64(p.gbar) < target;) {
     __nanosleep(32);
     if (++spins == (1u << 24)) {
       printf("[pcb] chain grid barrier timeout: block %d thread %d phase %d/%d counter %llu target %llu\n", blockIdx.x,
@@ -142,6 +142,7 @@ __device__ __forceinline__ void grid_wait(const ChainParams& p, int ph) {
       __trap();
     }
   }
+  fence_acquire_gpu();
 }
 
 __device__ __forceinline__ double ln_sum128(double v, double* red, int et) {
@@ -369,17 +370,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             }
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
-            __threadfence();
+            // one gpu-scope release by et 0 (st_release) publishes the CTA's partial: bar.sync
+            // orders the other threads' stores before it (cumulativity)
             named_bar(1, 128);
             if (et == 0) st_release(p.flags + c, epoch);
           } else {
             const int c_last = ge < te ? cta_of(te - 1, P.units, C) : c;
             if (c_last > c) {
               for (int pp = c + 1 + et; pp <= c_last; pp += 128)
-                for (uint32_t spins = 0; has_units(pp, P.units, C) && ld_acquire(p.flags + pp) < epoch;) {
+                for (uint32_t spins = 0; has_units(pp, P.units, C) && ld_relaxed(p.flags + pp) < epoch;) {
                   __nanosleep(64);
                   if (++spins == (1u << 25)) wait_timeout("chain stream-K flag", p.flags + pp, epoch);
                 }
+              fence_acquire_gpu();
               named_bar(1, 128);
             }
             if (et == 0) ctl(p, ph, 5);
@@ -454,6 +457,7 @@ void launch_chain(const ChainStep* steps, int n, const ChainStep* next, float* w
       d.K = st.K;
       d.kbs = st.K / 64;
       d.units = static_cast<int64_t>(st.N / 128) * d.kbs;
+      if (!units_fit_u32(d.units, C)) throw std::runtime_error("chain: too many work units for the 32-bit split");
       d.w = static_cast<const uint8_t*>(st.w);
       d.e = st.e;
       p.tm[i] = tmap_bf16_2d(st.x, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.K), BN);

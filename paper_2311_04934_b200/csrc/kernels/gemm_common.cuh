@@ -127,6 +127,19 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Spin-wait reads are relaxed (an acquire load invalidates the SM's whole L1 -- CCTL.IVALL
+// -- on every poll); the waiter issues one acquire fence after the condition holds.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -135,7 +148,13 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 
 
-__device__ __forceinline__ int64_t unit_begin(int c, int64_t U, int C) { return static_cast<int64_t>(c) * U / C; }
+// First unit of CTA c when U units are split evenly over C CTAs.  c * U < 2^32 for every
+// launch (checked on the host: units_fit_u32), so the split uses 32-bit division (a 64-bit
+// divide is a ~100-instruction software routine, and these sit on the phase-end path).
+__device__ __forceinline__ int64_t unit_begin(int c, int64_t U, int C) {
+  return static_cast<int64_t>(static_cast<uint32_t>(c) * static_cast<uint32_t>(U) / static_cast<uint32_t>(C));
+}
+inline bool units_fit_u32(int64_t U, int C) { return U >= 0 && (static_cast<uint64_t>(U) * (C + 1)) < (1ull << 32); }
 
 __device__ __forceinline__ bool has_units(int cc, int64_t U, int C) {
   return unit_begin(cc, U, C) < unit_begin(cc + 1, U, C);

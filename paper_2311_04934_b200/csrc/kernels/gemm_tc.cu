@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
-        __threadfence();
+        // one gpu-scope release by et 0 (st_release) publishes the CTA's partial: bar.sync
+        // orders the other threads' stores before it (cumulativity)
         named_bar(1, 128);
         if (et == 0) st_release(a.flags + c, a.epoch);
       } else {
@@ -286,10 +287,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int c_last = ge < te ? cta_of(te - 1, a.units, C) : c;
         if (c_last > c) {
           for (int p = c + 1 + et; p <= c_last; p += 128)
-            for (uint32_t spins = 0; ld_acquire(a.flags + p) < a.epoch;) {
+            for (uint32_t spins = 0; ld_relaxed(a.flags + p) < a.epoch;) {
               __nanosleep(64);
               if (++spins == (1u << 25)) wait_timeout("stream-K flag", a.flags + p, a.epoch);
             }
+          fence_acquire_gpu();
           named_bar(1, 128);
         }
         if (a.m_tiles == 1) {
@@ -386,6 +388,7 @@ static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, co
   a.kbs = K / 64;
   a.m_tiles = static_cast<int>((M + BN - 1) / BN);
   a.units = static_cast<int64_t>(N / 128) * a.m_tiles * a.kbs;
+  if (!units_fit_u32(a.units, sms)) throw std::runtime_error("gemm: too many work units for the 32-bit split");
   a.ws = ws;
   a.flags = flags;
   a.epoch = ++g_sk_epoch;

@@ -33,6 +33,7 @@ def dump():
 VARIANTS = [
     ("per-GEMM kernels", {"chain": 0}),
     ("chain", {"chain": 1, "chain_pf": 0}),
+
 ]
 if os.environ.get("AB_VARIANTS"):
     VARIANTS = [v for v in VARIANTS if v[0] in os.environ["AB_VARIANTS"].split(",")]

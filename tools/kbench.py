@@ -21,7 +21,10 @@ def bench(which, a0, a1, a2, iters=50):
 if __name__ == "__main__":
     for M, N, K, nm in [(64, 12288, 4096, "qkv"), (64, 4096, 4096, "o"), (64, 16384, 4096, "w1"),
                         (64, 4096, 16384, "w2"), (1, 32000, 4096, "unembed"), (128, 12288, 4096, "qkv128"),
-                        (4160, 12288, 4096, "qkv_prefill"), (4160, 16384, 4096, "w1_prefill")]:
+                        (256, 12288, 4096, "qkv256"), (512, 12288, 4096, "qkv512"), (512, 16384, 4096, "w1_512"),
+                        (512, 4096, 16384, "w2_512"),
+                        (4160, 12288, 4096, "qkv_prefill"), (4160, 16384, 4096, "w1_prefill"),
+                        (4160, 4096, 16384, "w2_prefill")]:
         us = bench("gemm", M, N, K)
         gb = (N * K * 2 + M * K * 2 + M * N * 8) / 1e9
         tf = 2 * M * N * K / 1e12
