@@ -85,6 +85,42 @@ def workload(n_cached: int, n_uncached: int, n_modules: int = 1):
     return schema, prompts
 
 
+def pcg32(seed: int):
+    """Pcg32(splitmix64(seed)) as the reference seeds its generators (bench.cpp:22-31)."""
+    M = (1 << 64) - 1
+    state = (splitmix64(seed) + 1442695040888963407) & M
+    while True:
+        old = state
+        state = (old * 6364136223846793005 + 1442695040888963407) & M
+        xs = (((old >> 18) ^ old) >> 27) & 0xFFFFFFFF
+        rot = old >> 59
+        yield ((xs >> rot) | (xs << ((-rot) & 31))) & 0xFFFFFFFF
+
+
+def workload_c4(n_modules: int = 64, mod_len: int = 256, n_req: int = 256, per_req: int = 8, n_unc: int = 64):
+    """a store of n_modules top-level modules (synthetic_text(mod_len, 1000+i)) and
+    n_req prompts, each importing per_req distinct modules picked by Pcg32(splitmix64(req_id)) (schema
+    order) followed by n_unc uncached tokens.  Returns (schema_text, prompts, picks)."""
+    mods = "".join(f'<module name="m{i}">{synthetic_text(mod_len, 1000 + i)}</module>' for i in range(n_modules))
+    schema = f'<schema name="c4">{mods}</schema>'
+    prompts, picks = [], []
+    for r in range(n_req):
+        g, sel = pcg32(r), []
+        while len(sel) < min(per_req, n_modules):
+            x = next(g) % n_modules
+            if x not in sel:
+                sel.append(x)
+        sel.sort()
+        picks.append(sel)
+        prompts.append(f'<prompt schema="c4">{"".join(f"<m{i}/>" for i in sel)}{question(n_unc, 5000 + r)}</prompt>')
+    return schema, prompts, picks
+
+
+def partition(n: int, rank: int, world: int) -> list:
+    """Requests of one rank (data parallel, no collectives): i = rank, rank + world, ..."""
+    return list(range(rank, n, world))
+
+
 # ---------------------------------------------------------------------------
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------

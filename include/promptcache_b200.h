@@ -114,6 +114,12 @@ int pcb_store_load(pcb_store* s, const char* path);
 /* ---- engine (engine.hpp:50-62) ---- */
 int pcb_serve(pcb_store* s, const pcb_schema* sc, const pcb_prompt* p, int max_new_tokens, int use_cache,
               int use_scaffolds, pcb_response** out);
+// Micro-batched first-token serving (config 4: many requests, differing module
+// combinations): micro_batch requests share one assembly launch and one suffix
+// prefill.  Replaces a loop of engine::serve (reference engine.cpp:187-258) with
+// max_new_tokens = 1; out[i] receives one response handle per prompt.
+int pcb_serve_batch(pcb_store* s, const pcb_schema* sc, const pcb_prompt* const* prompts, int n, int micro_batch,
+                    pcb_response** out);
 int pcb_oracle_serve(pcb_model* m, const pcb_schema* sc, const pcb_prompt* p, int max_new_tokens,
                      pcb_response** out);
 char* pcb_response_json(const pcb_response* r);                       /* ServeResponse::to_json (+device timings) */

@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = [
     "PromptCacheError", "Schema", "Prompt", "Model", "KV", "ModuleStore", "ServeResponse",
-    "serve", "oracle_serve", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
+    "serve", "serve_batch", "oracle_serve", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
     "F32", "BF16", "FAST", "SLOW", "lib", "LIB_PATH",
 ]
 
@@ -89,6 +89,7 @@ def lib():
         "pcb_store_load": (i32, [vp, cp]),
         "pcb_serve": (i32, [vp, vp, vp, i32, i32, i32, pvp]),
         "pcb_oracle_serve": (i32, [vp, vp, vp, i32, pvp]),
+        "pcb_serve_batch": (i32, [vp, vp, pvp, i32, i32, pvp]),
         "pcb_response_json": (vp, [vp]), "pcb_response_tokens": (i32, [vp, vp, i32]),
         "pcb_response_first_logits": (i32, [vp, vp, i32]), "pcb_response_destroy": (None, [vp]),
     }
@@ -401,6 +402,17 @@ def serve(store: ModuleStore, schema: Schema, prompt, max_new_tokens: int = 16, 
     _check(lib().pcb_serve(store.handle, schema.handle, p.handle, max_new_tokens, int(use_cache),
                            int(use_scaffolds), C.byref(h)))
     return ServeResponse._from(h.value, store.model.vocab)
+
+
+def serve_batch(store: ModuleStore, schema: Schema, prompts, micro_batch: int = 4) -> list:
+    """engine::serve_batch: first tokens of many requests, micro_batch requests per assembly
+    launch and suffix prefill."""
+    ps = [_prompt(p) for p in prompts]
+    n = len(ps)
+    arr = (C.c_void_p * max(n, 1))(*[p.handle for p in ps])
+    outs = (C.c_void_p * max(n, 1))()
+    _check(lib().pcb_serve_batch(store.handle, schema.handle, arr, n, micro_batch, outs))
+    return [ServeResponse._from(outs[i], store.model.vocab) for i in range(n)]
 
 
 def oracle_serve(model: Model, schema: Schema, prompt, max_new_tokens: int = 16) -> ServeResponse:

@@ -412,6 +412,18 @@ int pcb_serve(pcb_store* s, const pcb_schema* sc, const pcb_prompt* p, int max_n
     *out = new pcb_response{engine::serve(req, sc->P(), *s->s)};
   });
 }
+int pcb_serve_batch(pcb_store* s, const pcb_schema* sc, const pcb_prompt* const* prompts, int n, int micro_batch,
+                    pcb_response** out) {
+  return guard([&] {
+    std::vector<engine::ServeRequest> reqs(n);
+    for (int i = 0; i < n; ++i) {
+      reqs[i].prompt = prompts[i]->p;
+      reqs[i].max_new_tokens = 1;
+    }
+    std::vector<engine::ServeResponse> r = engine::serve_batch(reqs, sc->P(), *s->s, micro_batch);
+    for (int i = 0; i < n; ++i) out[i] = new pcb_response{std::move(r[i])};
+  });
+}
 int pcb_oracle_serve(pcb_model* m, const pcb_schema* sc, const pcb_prompt* p, int max_new, pcb_response** out) {
   return guard([&] {
     engine::ServeRequest req;

@@ -102,12 +102,21 @@ struct AsmScratch {
     if (!ev[0])
       for (auto& e : ev) CK(cudaEventCreate(&e));
     if (n_segs > cap) {
-      int c = std::max(n_segs, 256);
-      if (h_segs) cudaFreeHost(h_segs);
+      int c = std::max(n_segs, 2 * cap);
+      c = std::max(c, 256);
+      kern::CopySeg* old = h_segs;
+      h_segs = nullptr;
+      if (old) {
+        kern::CopySeg* fresh = nullptr;
+        CK(cudaMallocHost(&fresh, c * sizeof(kern::CopySeg)));
+        std::memcpy(fresh, old, cap * sizeof(kern::CopySeg));  // queued segments survive growth
+        cudaFreeHost(old);
+        h_segs = fresh;
+      }
       if (h_first) cudaFreeHost(h_first);
       if (d_segs) cudaFree(d_segs);
       if (d_first) cudaFree(d_first);
-      CK(cudaMallocHost(&h_segs, c * sizeof(kern::CopySeg)));
+      if (!h_segs) CK(cudaMallocHost(&h_segs, c * sizeof(kern::CopySeg)));
       CK(cudaMallocHost(&h_first, c * sizeof(uint64_t)));
       CK(cudaMalloc(&d_segs, c * sizeof(kern::CopySeg)));
       CK(cudaMalloc(&d_first, c * sizeof(uint64_t)));
@@ -121,7 +130,7 @@ struct AsmScratch {
       CK(cudaMalloc(&d_map, c * 4));
       map_cap = c;
     }
-    if (!h_tok) CK(cudaMallocHost(&h_tok, 64));
+    if (!h_tok) CK(cudaMallocHost(&h_tok, 4096 * 4));
     if (V > logit_cap) {
       if (h_logits) cudaFreeHost(h_logits);
       CK(cudaMallocHost(&h_logits, V * 4));
@@ -147,11 +156,12 @@ void check_disjoint(const std::vector<cache::EntryPtr>& entries) {
 // Gathers the entries' KV rows into `dst` rows [0, sum) — one assembly-kernel
 // launch for every device-resident (fast tier) block; slow-tier blocks are
 // H2D copies issued on the same stream.  Returns #slow entries.
-int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model::KVBlock& dst, AsmScratch& sc) {
+int append_segments(model::Model& m, const std::vector<cache::EntryPtr>& entries, model::KVBlock& dst, AsmScratch& sc,
+                    int& n_segs) {
   const int L = m.config().n_layers;
   const size_t rb = dst.row_bytes();
-  int n_segs = 0, slow = 0;
-  sc.ensure(static_cast<int>(entries.size()) * 2 * L, 0, 0);
+  int slow = 0;
+  sc.ensure(n_segs + static_cast<int>(entries.size()) * 2 * L, 0, 0);
   int64_t row = 0;
   for (auto& e : entries) {
     const model::KVBlock& b = *e->kv;
@@ -173,6 +183,11 @@ int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model
     row += b.rows;
   }
   dst.rows = row;
+  return slow;
+}
+
+// One assembly-kernel launch for every queued device segment.
+void launch_segments(model::Model& m, AsmScratch& sc, int n_segs) {
   if (n_segs) {
     const uint64_t chunks = kern::assemble_plan(sc.h_segs, n_segs, sc.h_first);
     CK(cudaMemcpyAsync(sc.d_segs, sc.h_segs, n_segs * sizeof(kern::CopySeg), cudaMemcpyHostToDevice, m.stream()));
@@ -183,6 +198,14 @@ int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model
     kern::assemble(sc.d_segs, sc.d_first, n_segs, chunks, m.stream());
     m.prof_end(model::Model::PROF_ASM, bytes, 0);
   }
+}
+
+// Gathers the entries' KV rows into `dst` rows [0, sum) with one assembly launch;
+// returns #slow entries.
+int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model::KVBlock& dst, AsmScratch& sc) {
+  int n_segs = 0;
+  const int slow = append_segments(m, entries, dst, sc, n_segs);
+  launch_segments(m, sc, n_segs);
   return slow;
 }
 
@@ -384,6 +407,108 @@ ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::Module
   resp.timings.assemble_us = ms * 1000.0;
   resp.timings.copy_us = slow ? ms * 1000.0 : 0.0;
   return resp;
+}
+
+std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, const Schema& schema,
+                                       cache::ModuleStore& store, int micro_batch) {
+  model::Model& m = store.model();
+  CK(cudaSetDevice(m.device()));
+  const int V = m.config().vocab_size;
+  const layout::LayoutPlan& plan = schema.plan;
+  micro_batch = std::max(1, std::min(micro_batch, 1024));
+  std::vector<ServeResponse> out(reqs.size());
+  for (size_t b0 = 0; b0 < reqs.size(); b0 += micro_batch) {
+    auto t0 = Clock::now();
+    const size_t b1 = std::min(reqs.size(), b0 + micro_batch);
+    struct Item {
+      size_t idx;
+      std::vector<cache::EntryPtr> sel;
+      UncachedPass up;
+      int64_t n_cached = 0;
+    };
+    std::vector<Item> items;
+    for (size_t i = b0; i < b1; ++i) {
+      const ServeRequest& req = reqs[i];
+      // decode past the first token, baselines and scaffolds take the single-request path
+      if (!req.use_cache || req.use_scaffolds || req.max_new_tokens != 1) {
+        out[i] = serve(req, schema, store);
+        continue;
+      }
+      require_valid(req.prompt, schema.doc);
+      layout::ResolvedPrompt resolved = layout::resolve_prompt(req.prompt, plan);
+      Item it;
+      it.idx = i;
+      ServeResponse& resp = out[i];
+      resp.timings.parse_us = us_since(t0);
+      for (const std::string& name : resolved.cached_imports) {
+        cache::EntryPtr e = store.lookup(schema.doc.name, name);
+        const layout::ModuleLayout& ml = plan.at(name);
+        if (!e || e->token_len != static_cast<int64_t>(ml.own_tokens.size()) || e->kv->positions != ml.own_positions) {
+          ++resp.cache_report.modules_missed;
+          store.insert(cache::encode_module(m, plan, name));
+          e = store.lookup(schema.doc.name, name);
+        } else {
+          ++resp.cache_report.modules_hit;
+        }
+        it.sel.push_back(e);
+      }
+      check_disjoint(it.sel);
+      for (auto& e : it.sel) {
+        it.n_cached += e->kv->rows;
+        resp.cache_report.cached_token_count += e->token_len;
+      }
+      it.up = build_uncached(resolved, plan, true);
+      resp.cache_report.uncached_token_count = it.up.prompt_token_count;
+      items.push_back(std::move(it));
+    }
+    if (items.empty()) continue;
+    // one request cache per item, equal capacity (run_batch addresses them by offset)
+    int64_t cap = 0;
+    for (auto& it : items) cap = std::max<int64_t>(cap, it.n_cached + static_cast<int64_t>(it.up.tokens.size()));
+    if (store.batch_arenas.size() < items.size() || (!store.batch_arenas.empty() && store.batch_arenas[0]->cap < cap)) {
+      const int64_t c = std::max<int64_t>(cap, store.batch_arenas.empty() ? 64 : store.batch_arenas[0]->cap);
+      store.batch_arenas.clear();
+      for (size_t k = 0; k < std::max<size_t>(items.size(), micro_batch); ++k) store.batch_arenas.push_back(m.alloc_kv(c));
+    }
+    AsmScratch& sc = scratch_of(store);
+    sc.ensure(0, 0, static_cast<int64_t>(V) * items.size());
+    CK(cudaEventRecord(sc.ev[0], m.stream()));
+    int n_segs = 0;
+    std::vector<model::Model::BatchItem> bi;
+    for (size_t k = 0; k < items.size(); ++k) {
+      model::KVBlock& a = *store.batch_arenas[k];
+      a.rows = 0;
+      a.positions.clear();
+      append_segments(m, items[k].sel, a, sc, n_segs);
+      bi.push_back({items[k].up.tokens.data(), items[k].up.positions.data(),
+                    static_cast<int64_t>(items[k].up.tokens.size()), &a});
+    }
+    launch_segments(m, sc, n_segs);
+    CK(cudaEventRecord(sc.ev[1], m.stream()));
+    m.run_batch(bi, true);
+    const int B = static_cast<int>(items.size());
+    m.argmax_last(B);
+    CK(cudaEventRecord(sc.ev[2], m.stream()));
+    CK(cudaMemcpyAsync(sc.h_logits, m.device_logits(), static_cast<size_t>(B) * V * 4, cudaMemcpyDeviceToHost,
+                       m.stream()));
+    CK(cudaMemcpyAsync(sc.h_tok, m.device_argmax(), B * 4, cudaMemcpyDeviceToHost, m.stream()));
+    CK(cudaStreamSynchronize(m.stream()));
+    float ms_asm = 0, ms_pre = 0;
+    CK(cudaEventElapsedTime(&ms_asm, sc.ev[0], sc.ev[1]));
+    CK(cudaEventElapsedTime(&ms_pre, sc.ev[1], sc.ev[2]));
+    const double ttft = us_since(t0);
+    for (int k = 0; k < B; ++k) {
+      ServeResponse& resp = out[items[k].idx];
+      resp.first_token_logits.assign(sc.h_logits + static_cast<size_t>(k) * V, sc.h_logits + static_cast<size_t>(k + 1) * V);
+      resp.output_tokens.push_back(sc.h_tok[k]);
+      resp.output_text = pml::tok::detokenize(resp.output_tokens);
+      resp.timings.assemble_us = ms_asm * 1000.0;
+      resp.timings.prefill_device_us = ms_pre * 1000.0;
+      resp.timings.uncached_prefill_us = ms_pre * 1000.0;
+      resp.timings.ttft_us = ttft;
+    }
+  }
+  return out;
 }
 
 ServeResponse oracle_serve(const ServeRequest& req, const Schema& schema, model::Model& m) {

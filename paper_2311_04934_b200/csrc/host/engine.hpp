@@ -54,6 +54,12 @@ struct Schema {
 model::KVPtr concat_kv(model::Model& m, const std::vector<cache::EntryPtr>& entries, int64_t extra_cap = 0);
 
 ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::ModuleStore& store);
+// Micro-batched cached serving: requests of one micro-batch are
+// assembled with one kernel launch into their own caches and their uncached suffixes
+// prefilled together (one weight stream per micro-batch, attention per request).
+// First token only (max_new_tokens == 1); other requests take serve().
+std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, const Schema& schema,
+                                       cache::ModuleStore& store, int micro_batch);
 // Block-causal exact reference (engine.cpp:260-334) run on the device.
 ServeResponse oracle_serve(const ServeRequest& req, const Schema& schema, model::Model& m);
 

@@ -100,7 +100,7 @@ uint64_t ModelConfig::hash() const {
 
 // ---------------------------------------------------------------------------
 KVBlock::~KVBlock() {
-  if (data) {
+  if (data && !view) {
     if (host) cudaFreeHost(data);
     else cudaFree(data);
   }
@@ -130,7 +130,8 @@ struct Weights {
 struct Workspace {
   int64_t cap_n = 0, cap_rows = 0, cap_logit = 0, cap_mask = 0;
   int d = 0, V = 0, dt = BF16;
-  int32_t *tok = nullptr, *pos = nullptr, *kvpos = nullptr, *block = nullptr, *argmax = nullptr;
+  int32_t *tok = nullptr, *pos = nullptr, *kvpos = nullptr, *block = nullptr, *argmax = nullptr, *lrows = nullptr;
+  int64_t* kvoff = nullptr;
   uint8_t* mask = nullptr;
   float* h = nullptr;
   void *x = nullptr, *q = nullptr, *attn = nullptr, *mid = nullptr;
@@ -149,7 +150,8 @@ struct Workspace {
   unsigned long long* chain_gbar() const { return reinterpret_cast<unsigned long long*>(counters + 32768); }
 
   ~Workspace() {
-    for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)mask, (void*)h, x, q,
+    for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)lrows, (void*)kvoff,
+                    (void*)mask, (void*)h, x, q,
                     attn, mid, (void*)logits, (void*)gemm_ws, (void*)counters, (void*)attn_scratch})
       if (p) cudaFree(p);
     for (auto& e : staged)
@@ -172,6 +174,8 @@ struct Workspace {
       regrow(tok, c * 4);
       regrow(pos, c * 4);
       regrow(block, c * 4);
+      regrow(kvoff, c * 8);
+      regrow(lrows, c * 4);
       regrow(h, c * d * 4);
       regrow(x, c * d * es);
       regrow(q, c * d * es);
@@ -200,7 +204,7 @@ struct Workspace {
       regrow(counters, 65536 * 4);
       CK(cudaMemset(counters, 0, 65536 * 4));
     }
-    int64_t need_ints = 3 * n + rows + 16;
+    int64_t need_ints = 6 * n + rows + 16;
     if (need_ints > host_ints_cap) {
       for (int sl = 0; sl < 2; ++sl)
         if (staged[sl]) CK(cudaEventSynchronize(staged[sl]));
@@ -514,22 +518,66 @@ void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const vo
 
 void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBlock& kv, const uint8_t* mask,
                 const int32_t* block_ids, int64_t logit_rows) {
+  BatchItem it{tokens, positions, n, &kv};
+  run_impl(&it, 1, mask, block_ids, logit_rows, false);
+}
+
+void Model::run_batch(const std::vector<BatchItem>& items, bool last_row_logits) {
+  if (items.empty()) return;
+  for (size_t i = 1; i < items.size(); ++i)
+    if (items[i].kv->cap != items[0].kv->cap)
+      throw Error(ErrorCode::ShapeMismatch, "run_batch: every request cache must have the same capacity");
+  run_impl(items.data(), static_cast<int>(items.size()), nullptr, nullptr, last_row_logits ? 1 : 0, true);
+}
+
+// One forward over B token segments (requests) concatenated along the token axis:
+// GEMMs, LayerNorm and the fused epilogues see all M = sum(n_i) rows at once (one
+// weight stream for the micro-batch); attention runs per segment over that
+// segment's own cache; QKV writes each token's K/V row into its own request cache.
+// Logits: the last `logit_rows` rows (B == 1), or the last row of every segment
+// (gathered, per_segment_logits).
+void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const int32_t* block_ids,
+                     int64_t logit_rows, bool per_segment_logits) {
   CK(cudaSetDevice(device_));
-  validate(tokens, positions, n, kv);
+  int64_t n = 0, max_total = 0;
+  for (int b = 0; b < B; ++b) {
+    validate(items[b].tokens, items[b].positions, items[b].n, *items[b].kv);
+    n += items[b].n;
+    max_total = std::max(max_total, items[b].kv->rows + items[b].n);
+  }
+  KVBlock& kv = *items[0].kv;
+  if (B > 1 && (mask || block_ids || cfg_.pos_encoding == PosEncoding::Alibi))
+    throw Error(ErrorCode::ShapeMismatch, "batched forward: masks, block ids and ALiBi take one request");
   if (mask && kv.rows) throw Error(ErrorCode::ShapeMismatch, "masked forward takes no past KV");
   if (mask)
     for (int64_t i = 0; i < n; ++i)
       if (!mask[i * n + i]) throw Error(ErrorCode::ShapeMismatch, "mask diagonal must be true");
   if (n <= 0) return;
-  logit_rows = std::min(logit_rows, n);
+  for (int b = 0; b < B; ++b)
+    if (items[b].n <= 0) throw Error(ErrorCode::ShapeMismatch, "batched forward: empty request");
+  logit_rows = per_segment_logits ? (logit_rows > 0 ? B : 0) : std::min(logit_rows, n);
   forward_tokens.fetch_add(n, std::memory_order_relaxed);
   const auto& c = cfg_;
   const int d = c.hidden, H = c.n_heads, hd = c.head_dim;
   const int64_t P = kv.rows, total = P + n;
   const double es = dtype_ == F32 ? 4.0 : 2.0;
   Workspace& W = *ws_;
-  W.ensure(n, total, logit_rows, mask != nullptr);
+  W.ensure(n, std::max(total, max_total), logit_rows, mask != nullptr);
   cudaStream_t s = stream_;
+  const int32_t* tokens = items[0].tokens;
+  const int64_t* positions = items[0].positions;
+  std::vector<int32_t> cat_tok;
+  std::vector<int64_t> cat_pos;
+  if (B > 1) {
+    cat_tok.reserve(n);
+    cat_pos.reserve(n);
+    for (int b = 0; b < B; ++b) {
+      cat_tok.insert(cat_tok.end(), items[b].tokens, items[b].tokens + items[b].n);
+      cat_pos.insert(cat_pos.end(), items[b].positions, items[b].positions + items[b].n);
+    }
+    tokens = cat_tok.data();
+    positions = cat_pos.data();
+  }
 
   // stage token ids / int32 positions (positions < max_position < 2^31, checked)
   int32_t* hi = W.acquire_staging();
@@ -551,6 +599,23 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     int32_t* bp = hi + 2 * n + (alibi ? total : 0);
     std::memcpy(bp, block_ids, n * 4);
     CK(cudaMemcpyAsync(W.block, bp, n * 4, cudaMemcpyHostToDevice, s));
+  }
+  std::vector<int64_t> seg_start(B);
+  if (B > 1) {
+    // per token: K/V element offset of its cache row relative to request 0's layer planes
+    // (equal capacities make the offset layer-independent); gathered logit rows
+    int64_t* ko = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(hi + 2 * n) + 7) & ~uintptr_t(7));
+    int32_t* lr = reinterpret_cast<int32_t*>(ko + n);
+    int64_t m = 0;
+    for (int b = 0; b < B; ++b) {
+      seg_start[b] = m;
+      const int64_t base = (static_cast<char*>(items[b].kv->data) - static_cast<char*>(kv.data)) /
+                           static_cast<int64_t>(items[b].kv->elem());
+      for (int64_t j = 0; j < items[b].n; ++j, ++m) ko[m] = base + (items[b].kv->rows + j) * d;
+      lr[b] = static_cast<int32_t>(m - 1);
+    }
+    CK(cudaMemcpyAsync(W.kvoff, ko, n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(W.lrows, lr, B * 4, cudaMemcpyHostToDevice, s));
   }
   W.release_staging(s);
 
@@ -590,6 +655,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
     e.k_out = kv.k(l);
     e.v_out = kv.v(l);
     e.kv_row0 = P;
+    e.kv_off = B > 1 ? W.kvoff : nullptr;
     e.pos = W.pos;
     e.rope = c.pos_encoding == PosEncoding::Rope;
     e.head_dim = hd;
@@ -611,6 +677,38 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
   ef.ldo = c.vocab_size;
 
   auto attention = [&](int l) {
+    if (B > 1) {
+      double bytes = 0, flops = 0;
+      prof_begin();
+      for (int b = 0; b < B; ++b) {
+        const KVBlock& kb = *items[b].kv;
+        const int64_t nb = items[b].n, Pb = kb.rows;
+        kern::AttnArgs ab = aa;
+        ab.n = nb;
+        ab.P = Pb;
+        ab.q = static_cast<const char*>(aa.q) + seg_start[b] * d * static_cast<int64_t>(es);
+        ab.out = static_cast<char*>(aa.out) + seg_start[b] * d * static_cast<int64_t>(es);
+        ab.k = kb.k(l);
+        ab.v = kb.v(l);
+        if (tc_attn && kern::attention_tc_supported(ab)) {
+          kern::attention_tc(ab, W.attn_scratch, W.attn_scratch_bytes, s);
+        } else {
+          const size_t per_q = static_cast<size_t>(H) * (Pb + nb) * sizeof(double);
+          const int64_t nqb = std::max<int64_t>(1, std::min<int64_t>(nb, static_cast<int64_t>((512ull << 20) / per_q)));
+          W.ensure_attn_scratch(per_q * nqb);
+          for (int64_t i0 = 0; i0 < nb; i0 += nqb) {
+            ab.i0 = i0;
+            ab.nq = std::min(nqb, nb - i0);
+            kern::attention_simt(dtype_, ab, W.attn_scratch, s);
+          }
+        }
+        if (b) ++launches;
+        bytes += 2.0 * (Pb + nb) * d * es + 2.0 * nb * d * es;
+        flops += 4.0 * (double)nb * d * (Pb + (nb + 1) / 2.0);
+      }
+      prof_end(PROF_ATTN, bytes, flops);
+      return;
+    }
     aa.k = kv.k(l);
     aa.v = kv.v(l);
     // algorithmic work: every visible key/value row read once, q in, out written
@@ -677,7 +775,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
       if (l + 1 < c.n_layers) {
         steps[k++] = ln(W.h, n);
         steps[k++] = mm(W.x, w_->wqkv[l + 1], n, 3 * d, d, qkv_epi(l + 1));
-      } else if (logit_rows > 0) {
+      } else if (logit_rows > 0 && !per_segment_logits) {
         steps[k++] = ln(W.h + (n - logit_rows) * d, logit_rows);
         steps[k++] = mm(W.x, w_->unembed, logit_rows, c.vocab_size, d, ef);
       }
@@ -703,7 +801,7 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
       gemm(W.x, w_->w1[l], n, 4 * d, d, &eg);
       gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo);
     }
-    if (logit_rows > 0) {
+    if (logit_rows > 0 && !per_segment_logits) {
       const int64_t r0 = n - logit_rows;
       prof_begin();
       kern::layernorm(dtype_, W.h + r0 * d, logit_rows, d, W.x, s);
@@ -711,8 +809,18 @@ void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBl
       gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
     }
   }
-  kv.rows = total;
-  kv.positions.insert(kv.positions.end(), positions, positions + n);
+  if (logit_rows > 0 && per_segment_logits) {
+    // last row of every request: gathered LayerNorm, then one unembed GEMM of B rows
+    prof_begin();
+    kern::layernorm_rows(dtype_, W.h, B > 1 ? W.lrows : nullptr, logit_rows, d, W.x, s, n - 1);
+    prof_end(PROF_OTHER, (4.0 + es) * logit_rows * d, 0);
+    gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
+  }
+  for (int b = 0; b < B; ++b) {
+    KVBlock& kb = *items[b].kv;
+    kb.rows += items[b].n;
+    kb.positions.insert(kb.positions.end(), items[b].positions, items[b].positions + items[b].n);
+  }
 }
 
 const float* Model::device_logits() const { return ws_->logits; }

@@ -47,6 +47,7 @@ struct KVBlock {
   int64_t rows = 0, cap = 0;
   void* data = nullptr;
   bool host = false;
+  bool view = false;  // non-owning window into another allocation
   std::vector<int64_t> positions;
 
   KVBlock() = default;
@@ -98,6 +99,16 @@ class Model {
   // rows) select exact masked attention (reference forward_masked / oracle).
   void run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBlock& kv, const uint8_t* mask,
            const int32_t* block_ids, int64_t logit_rows);
+  // Batched forward (B requests, micro-batched suffix prefill): each item's n tokens
+  // run over its own cache (all caches of one call share a capacity); logits of the
+  // last row of every item land in device_logits() rows [0, B).
+  struct BatchItem {
+    const int32_t* tokens;
+    const int64_t* positions;
+    int64_t n;
+    KVBlock* kv;
+  };
+  void run_batch(const std::vector<BatchItem>& items, bool last_row_logits);
   const float* device_logits() const;  // [logit_rows][vocab] after run()
   int32_t* device_argmax() const;      // scratch int32 slots
   void argmax_last(int64_t logit_rows);  // device argmax of each logits row -> device_argmax()
@@ -131,6 +142,8 @@ class Model {
  private:
   void validate(const int32_t* tokens, const int64_t* positions, int64_t n, const KVBlock& kv) const;
   void gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi);
+  void run_impl(const BatchItem* items, int B, const uint8_t* mask, const int32_t* block_ids, int64_t logit_rows,
+                bool per_segment_logits);
   void chain(const void* steps, int n_steps, const void* next);  // kern::ChainStep[n_steps], next chain's first
 
   ModelConfig cfg_;

@@ -75,6 +75,14 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int6
       const float pv = __shfl_xor_sync(0xffffffffu, v[j], 1);  // partner column n^1 lives in lane^1
       if (rot) v[j] = odd ? fmaf(pv, pre.b[j], v[j] * pre.a[j]) : fmaf(v[j], pre.a[j], -pv * pre.b[j]);
     }
+    if (seg > 0 && ep.kv_off) {  // batched requests: each token's row lives in its own cache
+      __nv_bfloat16* base = static_cast<__nv_bfloat16*>(seg == 1 ? ep.k_out : ep.v_out) + c;
+      const int64_t* off = ep.kv_off + m0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < jn) base[off[j]] = __float2bfloat16_rn(v[j]);
+      return;
+    }
     __nv_bfloat16* dst = (seg == 0 ? static_cast<__nv_bfloat16*>(ep.q_out)
                                    : static_cast<__nv_bfloat16*>(seg == 1 ? ep.k_out : ep.v_out) + ep.kv_row0 * d) +
                          m0 * d + c;

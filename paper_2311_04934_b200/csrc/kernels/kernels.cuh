@@ -34,6 +34,7 @@ struct Epilogue {
   void* k_out = nullptr;  // layer K base of the cache, row stride d
   void* v_out = nullptr;
   int64_t kv_row0 = 0;
+  const int64_t* kv_off = nullptr;  // batched: per token K/V element offset from k_out/v_out (row-major d)
   const int32_t* pos = nullptr;  // per token (EPI_QKV rope)
   int rope = 0;                  // apply RoPE
   int head_dim = 0;
@@ -56,6 +57,9 @@ void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table
            int d, float* h, cudaStream_t s);
 // out = LN(h) (gamma=1, beta=0, eps 1e-5), rows [row0, row0+n)
 void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s);
+// out[i] = LN(h[rows[i]]) for i < n (rows null: h row row_last for the single row)
+void layernorm_rows(int dtype, const float* h, const int32_t* rows, int64_t n, int d, void* out, cudaStream_t s,
+                    int64_t row_last);
 void argmax_rows(const float* logits, int64_t rows, int V, int32_t* out, cudaStream_t s);
 
 // ---- packed bf16 weights (the tcgen05 GEMM's HBM layout) ----

@@ -154,6 +154,28 @@ __global__ void __launch_bounds__(kLnThreads) k_layernorm(const float* h, int d,
   }
 }
 
+// gathered rows: out row i = LN(h row rows[i]) (rows null: the single row row_last)
+template <typename T>
+__global__ void __launch_bounds__(kLnThreads) k_layernorm_rows(const float* h, const int32_t* rows, int64_t row_last,
+                                                                 int d, T* out) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double red[kLnThreads / 32];
+  const int64_t r = rows ? rows[blockIdx.x] : row_last;
+  const float* row = h + r * d;
+  double s = 0;
+  for (int j = threadIdx.x; j < d; j += kLnThreads) s += row[j];
+  const double mean = ln_block_sum(s, red) / d;
+  double v = 0;
+  for (int j = threadIdx.x; j < d; j += kLnThreads) {
+    const double c = row[j] - mean;
+    v += c * c;
+  }
+  const double inv = 1.0 / sqrt(ln_block_sum(v, red) / d + 1e-5);
+  for (int j = threadIdx.x; j < d; j += kLnThreads)
+    st_f(out, static_cast<int64_t>(blockIdx.x) * d + j, static_cast<float>((row[j] - mean) * inv));
+}
+
 // general-d fallback (d % 4 != 0 or d > 8192): three strided passes
 template <typename T>
 __global__ void __launch_bounds__(kLnThreads) k_layernorm_any(const float* h, int d, T* out) {
@@ -183,6 +205,18 @@ void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStrea
   else
     launch_k(fast ? k_layernorm<__nv_bfloat16> : k_layernorm_any<__nv_bfloat16>, g, b, 0, s, 1, h, d,
              static_cast<__nv_bfloat16*>(out));
+  PCB_CUDA(cudaGetLastError());
+}
+
+void layernorm_rows(int dtype, const float* h, const int32_t* rows, int64_t n, int d, void* out, cudaStream_t s,
+                    int64_t row_last) {
+  if (n <= 0) return;
+  PdlClass pc(PDL_LN);
+  const dim3 g(static_cast<unsigned>(n)), b(kLnThreads);
+  if (dtype == F32)
+    launch_k(k_layernorm_rows<float>, g, b, 0, s, 1, h, rows, row_last, d, static_cast<float*>(out));
+  else
+    launch_k(k_layernorm_rows<__nv_bfloat16>, g, b, 0, s, 1, h, rows, row_last, d, static_cast<__nv_bfloat16*>(out));
   PCB_CUDA(cudaGetLastError());
 }
 
@@ -258,7 +292,7 @@ __device__ __forceinline__ void epi_pair(const Epilogue& e, int64_t m, int n, in
         }
       }
       T* dst = seg == 0 ? static_cast<T*>(e.q_out) + m * e.d
-                        : static_cast<T*>(seg == 1 ? e.k_out : e.v_out) + (e.kv_row0 + m) * e.d;
+                        : static_cast<T*>(seg == 1 ? e.k_out : e.v_out) + (e.kv_off ? e.kv_off[m] : (e.kv_row0 + m) * e.d);
       st_f(dst, c, v0);
       st_f(dst, c + 1, v1);
       return;

@@ -138,3 +138,16 @@ def test_config_canonical_and_hash(host_golden):
     with pytest.raises(pcb.PromptCacheError) as ei:
         pcb.config_hash({"n_layers": 0})
     assert ei.value.code == "InvalidConfig"
+
+
+def test_c4_workload_and_partition():
+    """Config-4 request generator: distinct modules in schema order, deterministic; the
+    data-parallel partition covers every request exactly once."""
+    import bench
+    schema, prompts, picks = bench.workload_c4(64, 8, 256, 8, 4)
+    assert len(prompts) == 256 and all(len(p) == 8 and p == sorted(set(p)) for p in picks)
+    assert bench.workload_c4(64, 8, 256, 8, 4)[2] == picks
+    assert len({tuple(p) for p in picks}) > 200  # differing module combinations
+    for world in (1, 2, 3, 8):
+        parts = [bench.partition(256, r, world) for r in range(world)]
+        assert sorted(i for p in parts for i in p) == list(range(256))
