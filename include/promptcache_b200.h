@@ -41,6 +41,7 @@ typedef struct pcb_model pcb_model;       /* pc::model::Model on one device */
 typedef struct pcb_kv pcb_kv;             /* pc::model::KVState, device resident */
 typedef struct pcb_store pcb_store;       /* pc::cache::ModuleStore */
 typedef struct pcb_response pcb_response; /* pc::engine::ServeResponse */
+typedef struct pcb_group pcb_group;       /* tensor-parallel ranks as threads of one process (tests) */
 
 const char* pcb_last_error(void);
 int pcb_last_error_code(void);
@@ -69,6 +70,17 @@ int64_t pcb_per_token_bytes(const char* config_json);                    /* cach
 
 /* ---- model (model.hpp:59-91) ---- */
 int pcb_model_create(const char* config_json, int dtype, int device, pcb_model** out);
+/* Head-sharded (tensor-parallel) model, SURVEY §8e config 5 -- no reference counterpart
+ * (the reference is single-process): rank tp_rank of tp_size holds n_heads/tp_size heads of
+ * every layer and of the module store, 4*hidden/tp_size MLP columns and vocab_size/tp_size
+ * unembedding rows; collectives run over NCCL (nccl_id from pcb_nccl_unique_id on one rank,
+ * shared out of band) or, for single-GPU tests, a pcb_group of threads.  Every rank then
+ * calls the same pcb_store_* / pcb_serve sequence in lockstep. */
+int pcb_nccl_unique_id(uint8_t* out_128_bytes);
+int pcb_group_create(int size, pcb_group** out);
+void pcb_group_destroy(pcb_group* g);
+int pcb_model_create_tp(const char* config_json, int dtype, int device, int tp_rank, int tp_size,
+                        const uint8_t* nccl_id, pcb_group* group, pcb_model** out);
 void pcb_model_destroy(pcb_model* m);
 int pcb_model_set_option(pcb_model* m, const char* key, int64_t value);  /* "force_simt" (testing), "profile" */
 int pcb_model_weight_checksum(pcb_model* m, const char* tensor, uint64_t* out);

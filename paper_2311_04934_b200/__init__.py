@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = [
     "PromptCacheError", "Schema", "Prompt", "Model", "KV", "ModuleStore", "ServeResponse",
-    "serve", "serve_batch", "oracle_serve", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
+    "serve", "serve_batch", "oracle_serve", "TPGroup", "nccl_unique_id", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
     "F32", "BF16", "FAST", "SLOW", "lib", "LIB_PATH",
 ]
 
@@ -90,6 +90,10 @@ def lib():
         "pcb_serve": (i32, [vp, vp, vp, i32, i32, i32, pvp]),
         "pcb_oracle_serve": (i32, [vp, vp, vp, i32, pvp]),
         "pcb_serve_batch": (i32, [vp, vp, pvp, i32, i32, pvp]),
+        "pcb_nccl_unique_id": (i32, [vp]),
+        "pcb_group_create": (i32, [i32, pvp]),
+        "pcb_group_destroy": (None, [vp]),
+        "pcb_model_create_tp": (i32, [C.c_char_p, i32, i32, i32, i32, vp, vp, pvp]),
         "pcb_response_json": (vp, [vp]), "pcb_response_tokens": (i32, [vp, vp, i32]),
         "pcb_response_first_logits": (i32, [vp, vp, i32]), "pcb_response_destroy": (None, [vp]),
     }
@@ -244,13 +248,40 @@ class KV(_Handle):
         return np.stack([self.layer(l, 1) for l in range(self.n_layers)])
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes), created on one rank and shared out of band."""
+    buf = C.create_string_buffer(128)
+    _check(lib().pcb_nccl_unique_id(buf))
+    return buf.raw
+
+
+class TPGroup(_Handle):
+    """Tensor-parallel ranks as threads of one process on one device (single-GPU tests of the
+    head-sharded path; NCCL is the multi-GPU transport)."""
+    _destroy = "pcb_group_destroy"
+
+    def __init__(self, size: int):
+        h = C.c_void_p()
+        _check(lib().pcb_group_create(size, C.byref(h)))
+        super().__init__(h.value)
+        self.size = size
+
+
 class Model(_Handle):
     _destroy = "pcb_model_destroy"
 
-    def __init__(self, config: dict, dtype: int = BF16, device: int = 0):
+    def __init__(self, config: dict, dtype: int = BF16, device: int = 0, tp_rank: int = 0, tp_size: int = 1,
+                 nccl_id: bytes | None = None, group: "TPGroup | None" = None):
+        """tp_size > 1: head-sharded rank over NCCL (nccl_id) or a TPGroup."""
         h = C.c_void_p()
-        _check(lib().pcb_model_create(_enc(json.dumps(config)), dtype, device, C.byref(h)))
+        if tp_size == 1:
+            _check(lib().pcb_model_create(_enc(json.dumps(config)), dtype, device, C.byref(h)))
+        else:
+            nid = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+            _check(lib().pcb_model_create_tp(_enc(json.dumps(config)), dtype, device, tp_rank, tp_size, nid,
+                                             group.handle if group else None, C.byref(h)))
         super().__init__(h.value)
+        self.tp_rank, self.tp_size = tp_rank, tp_size
         self.config = dict(config)
         self.dtype = dtype
         self.n_layers = config.get("n_layers", 4)

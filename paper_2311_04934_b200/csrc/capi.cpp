@@ -10,6 +10,7 @@
 #include "../../include/promptcache_b200.h"
 #include "host/cache.hpp"
 #include "host/engine.hpp"
+#include "host/collective.hpp"
 #include "host/layout.hpp"
 #include "host/model.hpp"
 #include "host/pml.hpp"
@@ -147,6 +148,32 @@ int64_t pcb_per_token_bytes(const char* j) {
 int pcb_model_create(const char* cfg, int dtype, int device, pcb_model** out) {
   return guard([&] {
     *out = new pcb_model{std::make_unique<model::Model>(model::ModelConfig::from_json(cfg), dtype, device)};
+  });
+}
+struct pcb_group {
+  std::shared_ptr<coll::LocalGroup> g;
+};
+int pcb_nccl_unique_id(uint8_t* out) {
+  return guard([&] { coll::nccl_unique_id(out); });
+}
+int pcb_group_create(int size, pcb_group** out) {
+  return guard([&] {
+    if (size < 1) throw Error(ErrorCode::InvalidConfig, "group size must be positive");
+    *out = new pcb_group{std::make_shared<coll::LocalGroup>(size)};
+  });
+}
+void pcb_group_destroy(pcb_group* g) { delete g; }
+int pcb_model_create_tp(const char* cfg, int dtype, int device, int tp_rank, int tp_size, const uint8_t* nccl_id,
+                        pcb_group* group, pcb_model** out) {
+  return guard([&] {
+    std::shared_ptr<coll::Collective> comm;
+    if (tp_size > 1) {
+      if (group) comm = coll::make_local(group->g, tp_rank);
+      else if (nccl_id) comm = coll::make_nccl(nccl_id, tp_rank, tp_size, device);
+      else throw Error(ErrorCode::InvalidConfig, "tensor parallel needs an NCCL id or a local group");
+    }
+    *out = new pcb_model{
+        std::make_unique<model::Model>(model::ModelConfig::from_json(cfg), dtype, device, tp_rank, tp_size, comm)};
   });
 }
 void pcb_model_destroy(pcb_model* m) { delete m; }
@@ -334,7 +361,7 @@ int pcb_kv_upload(pcb_model* m, const float* k, const float* v, const int64_t* p
   return guard([&] {
     model::Model& mm = *m->m;
     model::KVPtr kv = mm.alloc_kv(rows);
-    const int L = mm.config().n_layers, d = mm.config().hidden;
+    const int L = mm.config().n_layers, d = mm.kv_width();
     const uint64_t cnt = static_cast<uint64_t>(rows) * d;
     float* f = nullptr;
     if (cnt) cudaMalloc(&f, cnt * 4);

@@ -220,7 +220,7 @@ void ModuleStore::save(const std::string& path) const {
   w.put<uint32_t>(kVersion);
   w.put<uint64_t>(m.config().hash());
   w.put<uint32_t>(static_cast<uint32_t>(entries_.size()));
-  const int L = m.config().n_layers, d = m.config().hidden;
+  const int L = m.config().n_layers, d = m.kv_width();
   for (const auto& [key, ep] : entries_) {
     const CacheEntry& e = *ep;
     w.str(e.schema);
@@ -281,7 +281,7 @@ void ModuleStore::load(const std::string& path) {
                 "store version " + std::to_string(version) + ", expected " + std::to_string(kVersion));
   if (r.get<uint64_t>() != m.config().hash())
     throw Error(ErrorCode::ConfigHashMismatch, "store was built with a different model config");
-  const int d = m.config().hidden;
+  const int d = m.kv_width();
   uint32_t count = r.get<uint32_t>();
   std::vector<CacheEntry> loaded;
   for (uint32_t i = 0; i < count; ++i) {

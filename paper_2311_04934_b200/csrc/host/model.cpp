@@ -4,6 +4,7 @@
 //   into the request cache) -> attention -> O GEMM (+residual) -> LN2 -> W1 GEMM
 //   (+GELU) -> W2 GEMM (+residual)] x L -> final LN -> unembed (last rows only).
 #include "model.hpp"
+#include "collective.hpp"
 
 #include <cmath>
 #include <cstdio>
@@ -114,7 +115,8 @@ struct Weights {
   float *cos32 = nullptr, *sin32 = nullptr;
   float* alibi = nullptr;
   float* abs_table = nullptr;
-  bool packed = false;  // bf16 GEMM weights in the tcgen05 tile layout
+  bool packed = false;  // every bf16 GEMM weight in the tcgen05 tile layout
+  bool pk_qkv = false, pk_o = false, pk_1 = false, pk_2 = false, pk_un = false;  // per weight kind
   std::vector<void*> owned;
   ~Weights() {
     for (void* p : owned) cudaFree(p);
@@ -136,6 +138,8 @@ struct Workspace {
   float* h = nullptr;
   void *x = nullptr, *q = nullptr, *attn = nullptr, *mid = nullptr;
   float* logits = nullptr;
+  float *part = nullptr, *logits_loc = nullptr, *logits_gath = nullptr;  // tensor parallel
+  int tp = 1, Vl = 0;
   float* gemm_ws = nullptr;
   size_t gemm_ws_bytes = 0;
   int* counters = nullptr;
@@ -152,7 +156,8 @@ struct Workspace {
   ~Workspace() {
     for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)lrows, (void*)kvoff,
                     (void*)mask, (void*)h, x, q,
-                    attn, mid, (void*)logits, (void*)gemm_ws, (void*)counters, (void*)attn_scratch})
+                    attn, mid, (void*)logits, (void*)part, (void*)logits_loc, (void*)logits_gath, (void*)gemm_ws,
+                    (void*)counters, (void*)attn_scratch})
       if (p) cudaFree(p);
     for (auto& e : staged)
       if (e) {
@@ -181,6 +186,7 @@ struct Workspace {
       regrow(q, c * d * es);
       regrow(attn, c * d * es);
       regrow(mid, c * 4 * d * es);
+      if (tp > 1) regrow(part, c * d * 4);
       cap_n = c;
     }
     if (rows > cap_rows) {
@@ -191,6 +197,10 @@ struct Workspace {
     if (logit_rows > cap_logit) {
       int64_t c = std::max<int64_t>(logit_rows, 1);
       regrow(logits, c * V * 4);
+      if (tp > 1) {
+        regrow(logits_loc, c * Vl * 4);
+        regrow(logits_gath, c * V * 4);
+      }
       cap_logit = c;
     }
     if (want_mask && n * n > cap_mask) {
@@ -239,7 +249,19 @@ static uint64_t stream_seed(const std::string& name, uint64_t seed) {
   return splitmix64(fnv1a64(name.data(), name.size()) ^ splitmix64(seed));
 }
 
-Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtype), device_(device) {
+Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_size,
+             std::shared_ptr<coll::Collective> comm)
+    : cfg_(c), dtype_(dtype), device_(device), tp_rank_(tp_rank), tp_size_(tp_size), comm_(std::move(comm)) {
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) throw Error(ErrorCode::InvalidConfig, "bad tensor-parallel rank");
+  if (tp_size > 1 && (!comm_ || comm_->size != tp_size || comm_->rank != tp_rank))
+    throw Error(ErrorCode::InvalidConfig, "tensor parallel needs a collective of the same size and rank");
+  if (c.n_heads % tp_size || c.vocab_size % tp_size)
+    throw Error(ErrorCode::InvalidConfig, "n_heads and vocab_size must divide by the tensor-parallel size");
+  if (tp_size > 1 && c.pos_encoding == PosEncoding::Alibi)
+    throw Error(ErrorCode::InvalidConfig, "tensor parallel: ALiBi is not sharded");
+  dl_ = c.hidden / tp_size;
+  fl_ = 4 * c.hidden / tp_size;
+  vl_ = c.vocab_size / tp_size;
   if (const char* v = std::getenv("PCB_CHAIN")) use_chain = v[0] != '0';
   if (c.hidden != c.n_heads * c.head_dim) throw Error(ErrorCode::InvalidConfig, "hidden must equal n_heads * head_dim");
   if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 2 || c.head_dim % 2 != 0)
@@ -258,6 +280,8 @@ Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtyp
   ws_ = std::make_unique<Workspace>();
   ws_->d = c.hidden;
   ws_->V = c.vocab_size;
+  ws_->Vl = vl_;
+  ws_->tp = tp_size;
   ws_->dt = dtype;
 
   const int d = c.hidden;
@@ -270,29 +294,49 @@ Model::Model(const ModelConfig& c, int dtype, int device) : cfg_(c), dtype_(dtyp
   kern::init_uniform(F32, w_->embed, Vd, stream_seed("embed", c.seed), 0.1f, stream_);
   // bf16 GEMM weights are stored pre-packed for the tcgen05 kernel (kernels.cuh
   // packed_index); fp32 weights stay row-major for the exact SIMT path.
-  w_->packed = dtype == BF16 && kern::weight_packable(3 * d, d) && kern::weight_packable(4 * d, d) &&
-               kern::weight_packable(d, 4 * d) && kern::weight_packable(c.vocab_size, d);
+  w_->pk_qkv = dtype == BF16 && kern::weight_packable(3 * dl_, d);
+  w_->pk_o = dtype == BF16 && kern::weight_packable(d, dl_);
+  w_->pk_1 = dtype == BF16 && kern::weight_packable(fl_, d);
+  w_->pk_2 = dtype == BF16 && kern::weight_packable(d, fl_);
+  w_->pk_un = dtype == BF16 && kern::weight_packable(vl_, d);
+  w_->packed = w_->pk_qkv && w_->pk_o && w_->pk_1 && w_->pk_2 && w_->pk_un;
   void* staging = nullptr;
-  if (w_->packed) CK(cudaMalloc(&staging, std::max<size_t>(4 * static_cast<size_t>(d) * d, Vd) * es));
-  // generate the fp32 stream of each named part into rows [row0, row0 + rows) of an [N][K] matrix
-  auto make = [&](int N, int K, std::initializer_list<std::pair<std::string, float>> parts) {
+  if (dtype == BF16) CK(cudaMalloc(&staging, std::max<size_t>(4 * static_cast<size_t>(d) * d, Vd) * es));
+  // One [N][K] weight from named stream blocks: each part is rows [row0, row0+rows) x
+  // columns [col0, col0+K) of a full [*][full_cols] reference tensor (tensor-parallel
+  // shards are row ranges of column-parallel and column ranges of row-parallel weights).
+  struct Part {
+    std::string name;
+    float scale;
+    int64_t rows, row0, col0, full_cols;
+  };
+  auto make = [&](int N, int K, std::vector<Part> parts, bool pack) {
     void* dst = w_->alloc(static_cast<size_t>(N) * K * es);
-    char* gen = static_cast<char*>(w_->packed ? staging : dst);
-    const size_t part = static_cast<size_t>(N) * K / parts.size();
+    char* gen = static_cast<char*>(pack ? staging : dst);
     size_t off = 0;
-    for (auto& [name, scale] : parts) {
-      kern::init_uniform(dtype, gen + off * es, part, stream_seed(name, c.seed), scale, stream_);
-      off += part;
+    for (auto& p : parts) {
+      if (p.row0 == 0 && p.col0 == 0 && p.full_cols == K)
+        kern::init_uniform(dtype, gen + off * es, static_cast<size_t>(p.rows) * K, stream_seed(p.name, c.seed), p.scale,
+                           stream_);
+      else
+        kern::init_uniform_block(dtype, gen + off * es, p.rows, K, stream_seed(p.name, c.seed), p.scale, p.row0, p.col0,
+                                 p.full_cols, stream_);
+      off += static_cast<size_t>(p.rows) * K;
     }
-    if (w_->packed) kern::pack_weight_bf16(staging, dst, N, K, stream_);
+    if (pack) kern::pack_weight_bf16(staging, dst, N, K, stream_);
     return dst;
   };
-  w_->unembed = make(c.vocab_size, d, {{"unembed", ws}});
+  const int r = tp_rank_;
+  w_->unembed = make(vl_, d, {{"unembed", ws, vl_, static_cast<int64_t>(r) * vl_, 0, d}}, w_->pk_un);
   for (int l = 0; l < c.n_layers; ++l) {
-    w_->wqkv.push_back(make(3 * d, d, {{tname(l, "wq"), ws}, {tname(l, "wk"), ws}, {tname(l, "wv"), ws}}));
-    w_->wo.push_back(make(d, d, {{tname(l, "wo"), ws}}));
-    w_->w1.push_back(make(4 * d, d, {{tname(l, "w1"), ws}}));
-    w_->w2.push_back(make(d, 4 * d, {{tname(l, "w2"), ws2}}));
+    const int64_t h0 = static_cast<int64_t>(r) * dl_;
+    w_->wqkv.push_back(make(3 * dl_, d,
+                            {{tname(l, "wq"), ws, dl_, h0, 0, d}, {tname(l, "wk"), ws, dl_, h0, 0, d},
+                             {tname(l, "wv"), ws, dl_, h0, 0, d}},
+                            w_->pk_qkv));
+    w_->wo.push_back(make(d, dl_, {{tname(l, "wo"), ws, d, 0, h0, d}}, w_->pk_o));
+    w_->w1.push_back(make(fl_, d, {{tname(l, "w1"), ws, fl_, static_cast<int64_t>(r) * fl_, 0, d}}, w_->pk_1));
+    w_->w2.push_back(make(d, fl_, {{tname(l, "w2"), ws2, d, 0, static_cast<int64_t>(r) * fl_, 4 * d}}, w_->pk_2));
   }
   if (staging) {
     CK(cudaStreamSynchronize(stream_));
@@ -437,7 +481,7 @@ KVPtr Model::alloc_kv(int64_t cap, bool host) const {
   auto kv = std::make_shared<KVBlock>();
   kv->dtype = dtype_;
   kv->n_layers = cfg_.n_layers;
-  kv->hidden = cfg_.hidden;
+  kv->hidden = dl_;
   kv->cap = cap;
   kv->host = host;
   if (cap > 0) {
@@ -475,7 +519,7 @@ void Model::validate(const int32_t* tokens, const int64_t* positions, int64_t n,
     if (tokens[i] < 0 || tokens[i] >= cfg_.vocab_size)
       throw Error(ErrorCode::ShapeMismatch, "token id out of vocab range");
   }
-  if (kv.n_layers != cfg_.n_layers || kv.hidden != cfg_.hidden || kv.dtype != dtype_)
+  if (kv.n_layers != cfg_.n_layers || kv.hidden != dl_ || kv.dtype != dtype_)
     throw Error(ErrorCode::ShapeMismatch, "past KV shape mismatch");
   if (kv.host) throw Error(ErrorCode::ShapeMismatch, "forward needs a device-resident KV block");
   if (kv.rows + n > kv.cap) throw Error(ErrorCode::ShapeMismatch, "KV block capacity exceeded");
@@ -505,13 +549,13 @@ void Model::chain(const void* steps_v, int n_steps, const void* next) {
   prof_end(PROF_GEMM, bytes, flops);
 }
 
-void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi) {
+void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi, bool packed) {
   const auto& e = *static_cast<const kern::Epilogue*>(epi);
   prof_begin();
-  if (w_->packed && !force_simt && !force_simt_gemm && kern::gemm_tc_supported(M, N, K))
+  if (packed && !force_simt && !force_simt_gemm && kern::gemm_tc_supported(M, N, K))
     kern::gemm_tc(A, W, M, N, K, e, ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->counters, stream_);
   else
-    kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_, w_->packed);
+    kern::gemm_simt(dtype_, A, W, M, N, K, e, stream_, packed);
   // algorithmic bytes: weights + activations in + outputs (residual: read + write fp32)
   prof_end(PROF_GEMM, gemm_alg_bytes(dtype_, M, N, K, e.kind), 2.0 * M * N * K);
 }
@@ -611,7 +655,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       seg_start[b] = m;
       const int64_t base = (static_cast<char*>(items[b].kv->data) - static_cast<char*>(kv.data)) /
                            static_cast<int64_t>(items[b].kv->elem());
-      for (int64_t j = 0; j < items[b].n; ++j, ++m) ko[m] = base + (items[b].kv->rows + j) * d;
+      for (int64_t j = 0; j < items[b].n; ++j, ++m) ko[m] = base + (items[b].kv->rows + j) * dl_;
       lr[b] = static_cast<int32_t>(m - 1);
     }
     CK(cudaMemcpyAsync(W.kvoff, ko, n * 8, cudaMemcpyHostToDevice, s));
@@ -626,9 +670,9 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   kern::AttnArgs aa;
   aa.n = n;
   aa.P = P;
-  aa.H = H;
+  aa.H = H / tp_size_;
   aa.hd = hd;
-  aa.d = d;
+  aa.d = dl_;
   aa.q = W.q;
   aa.out = W.attn;
   aa.mask = mask ? W.mask : nullptr;
@@ -650,7 +694,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   auto qkv_epi = [&](int l) {
     kern::Epilogue e;
     e.kind = kern::EPI_QKV;
-    e.d = d;
+    e.d = dl_;
     e.q_out = W.q;
     e.k_out = kv.k(l);
     e.v_out = kv.v(l);
@@ -673,8 +717,27 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   eg.out = W.mid;
   kern::Epilogue ef;
   ef.kind = kern::EPI_F32;
-  ef.outf = W.logits;
-  ef.ldo = c.vocab_size;
+  ef.outf = tp_size_ > 1 ? W.logits_loc : W.logits;
+  ef.ldo = vl_;
+  // tensor parallel: row-parallel GEMM partials -> all-reduce -> residual add
+  kern::Epilogue epart;
+  epart.kind = kern::EPI_F32;
+  epart.outf = W.part;
+  epart.ldo = d;
+  auto tp_reduce_into_h = [&]() {
+    comm_->all_reduce_sum(W.part, static_cast<size_t>(n) * d, s);
+    prof_begin();
+    kern::add_inplace(W.h, W.part, n * d, s);
+    prof_end(PROF_OTHER, 12.0 * n * d, 0);
+  };
+  // logits of `rows` LN'd rows in W.x: this rank's vocab rows, gathered over ranks
+  auto unembed = [&](int64_t rows) {
+    gemm(W.x, w_->unembed, rows, vl_, d, &ef, w_->pk_un);
+    if (tp_size_ > 1) {
+      comm_->all_gather(W.logits_loc, W.logits_gath, static_cast<size_t>(rows) * vl_, s);
+      kern::interleave_shards(W.logits_gath, tp_size_, rows, vl_, W.logits, s);
+    }
+  };
 
   auto attention = [&](int l) {
     if (B > 1) {
@@ -686,8 +749,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
         kern::AttnArgs ab = aa;
         ab.n = nb;
         ab.P = Pb;
-        ab.q = static_cast<const char*>(aa.q) + seg_start[b] * d * static_cast<int64_t>(es);
-        ab.out = static_cast<char*>(aa.out) + seg_start[b] * d * static_cast<int64_t>(es);
+        ab.q = static_cast<const char*>(aa.q) + seg_start[b] * dl_ * static_cast<int64_t>(es);
+        ab.out = static_cast<char*>(aa.out) + seg_start[b] * dl_ * static_cast<int64_t>(es);
         ab.k = kb.k(l);
         ab.v = kb.v(l);
         if (tc_attn && kern::attention_tc_supported(ab)) {
@@ -703,8 +766,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
           }
         }
         if (b) ++launches;
-        bytes += 2.0 * (Pb + nb) * d * es + 2.0 * nb * d * es;
-        flops += 4.0 * (double)nb * d * (Pb + (nb + 1) / 2.0);
+        bytes += 2.0 * (Pb + nb) * dl_ * es + 2.0 * nb * dl_ * es;
+        flops += 4.0 * (double)nb * dl_ * (Pb + (nb + 1) / 2.0);
       }
       prof_end(PROF_ATTN, bytes, flops);
       return;
@@ -712,8 +775,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     aa.k = kv.k(l);
     aa.v = kv.v(l);
     // algorithmic work: every visible key/value row read once, q in, out written
-    const double attn_bytes = 2.0 * total * d * es + 2.0 * n * d * es;
-    const double attn_flops = 4.0 * (double)n * d * (mask || block_ids || P == 0 ? (total + 1) / 2.0 : (P + (n + 1) / 2.0));
+    const double attn_bytes = 2.0 * total * dl_ * es + 2.0 * n * dl_ * es;
+    const double attn_flops = 4.0 * (double)n * dl_ * (mask || block_ids || P == 0 ? (total + 1) / 2.0 : (P + (n + 1) / 2.0));
     if (tc_attn) {
       prof_begin();
       kern::attention_tc(aa, W.attn_scratch, W.attn_scratch_bytes, s);
@@ -735,7 +798,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   // Few-token regime (suffix prefill, decode): the GEMM/LayerNorm segments between two
   // attention launches run as one persistent chain kernel each (chain_tc.cu), so the
   // weight stream does not stop at GEMM boundaries.
-  const bool chain_now = use_chain && dtype_ == BF16 && w_->packed && !force_simt && !force_simt_gemm &&
+  const bool chain_now = use_chain && tp_size_ == 1 && dtype_ == BF16 && w_->packed && !force_simt && !force_simt_gemm &&
                          kern::chain_ln_supported(d) && kern::chain_tc_supported(n, 3 * d, d) &&
                          kern::chain_tc_supported(n, 4 * d, d) && kern::chain_tc_supported(n, d, 4 * d) &&
                          (logit_rows == 0 || kern::chain_tc_supported(logit_rows, c.vocab_size, d));
@@ -792,21 +855,31 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       kern::layernorm(dtype_, W.h, n, d, W.x, s);
       prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
       kern::Epilogue e = qkv_epi(l);
-      gemm(W.x, w_->wqkv[l], n, 3 * d, d, &e);
+      gemm(W.x, w_->wqkv[l], n, 3 * dl_, d, &e, w_->pk_qkv);
       attention(l);
-      gemm(W.attn, w_->wo[l], n, d, d, &eo);
+      if (tp_size_ > 1) {
+        gemm(W.attn, w_->wo[l], n, d, dl_, &epart, w_->pk_o);  // partial over this rank's heads
+        tp_reduce_into_h();
+      } else {
+        gemm(W.attn, w_->wo[l], n, d, d, &eo, w_->pk_o);
+      }
       prof_begin();
       kern::layernorm(dtype_, W.h, n, d, W.x, s);
       prof_end(PROF_OTHER, (4.0 + es) * n * d, 0);
-      gemm(W.x, w_->w1[l], n, 4 * d, d, &eg);
-      gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo);
+      gemm(W.x, w_->w1[l], n, fl_, d, &eg, w_->pk_1);
+      if (tp_size_ > 1) {
+        gemm(W.mid, w_->w2[l], n, d, fl_, &epart, w_->pk_2);
+        tp_reduce_into_h();
+      } else {
+        gemm(W.mid, w_->w2[l], n, d, 4 * d, &eo, w_->pk_2);
+      }
     }
     if (logit_rows > 0 && !per_segment_logits) {
       const int64_t r0 = n - logit_rows;
       prof_begin();
       kern::layernorm(dtype_, W.h + r0 * d, logit_rows, d, W.x, s);
       prof_end(PROF_OTHER, (4.0 + es) * logit_rows * d, 0);
-      gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
+      unembed(logit_rows);
     }
   }
   if (logit_rows > 0 && per_segment_logits) {
@@ -814,7 +887,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     prof_begin();
     kern::layernorm_rows(dtype_, W.h, B > 1 ? W.lrows : nullptr, logit_rows, d, W.x, s, n - 1);
     prof_end(PROF_OTHER, (4.0 + es) * logit_rows * d, 0);
-    gemm(W.x, w_->unembed, logit_rows, c.vocab_size, d, &ef);
+    unembed(logit_rows);
   }
   for (int b = 0; b < B; ++b) {
     KVBlock& kb = *items[b].kv;
@@ -839,7 +912,7 @@ ForwardOutput Model::forward(const std::vector<int>& tokens, const std::vector<i
                              const KVBlock* past) {
   if (tokens.size() != positions.size())
     throw Error(ErrorCode::ShapeMismatch, "tokens/position_ids length mismatch");
-  if (past && (past->n_layers != cfg_.n_layers || past->hidden != cfg_.hidden || past->dtype != dtype_))
+  if (past && (past->n_layers != cfg_.n_layers || past->hidden != dl_ || past->dtype != dtype_))
     throw Error(ErrorCode::ShapeMismatch, "past KV shape mismatch");
   if (past)
     for (int64_t p : past->positions)

@@ -14,6 +14,10 @@
 
 #include "errors.hpp"
 
+namespace pcb::coll {
+class Collective;
+}
+
 namespace pcb::model {
 
 enum class PosEncoding { Rope, Alibi, AbsTable };
@@ -78,7 +82,13 @@ struct Workspace;
 
 class Model {
  public:
-  Model(const ModelConfig& config, int dtype, int device);
+  // Tensor parallel (head-sharded) when tp_size > 1: this rank holds
+  // heads [r H/T, (r+1) H/T) of Wq/Wk/Wv and its KV, the matching input columns of Wo,
+  // MLP columns [r 4d/T, ...) of W1 and input columns of W2, and vocab rows
+  // [r V/T, ...) of the unembedding; `comm` all-reduces after Wo and W2 and gathers
+  // the vocab shards of the logits.
+  Model(const ModelConfig& config, int dtype, int device, int tp_rank = 0, int tp_size = 1,
+        std::shared_ptr<coll::Collective> comm = nullptr);
   ~Model();
   Model(const Model&) = delete;
   Model& operator=(const Model&) = delete;
@@ -87,6 +97,9 @@ class Model {
   int dtype() const { return dtype_; }
   int device() const { return device_; }
   cudaStream_t stream() const { return stream_; }
+  int tp_rank() const { return tp_rank_; }
+  int tp_size() const { return tp_size_; }
+  int kv_width() const { return dl_; }  // hidden columns of K/V this rank stores
 
   KVPtr alloc_kv(int64_t cap, bool host = false) const;
 
@@ -141,13 +154,16 @@ class Model {
 
  private:
   void validate(const int32_t* tokens, const int64_t* positions, int64_t n, const KVBlock& kv) const;
-  void gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi);
+  void gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi, bool packed);
   void run_impl(const BatchItem* items, int B, const uint8_t* mask, const int32_t* block_ids, int64_t logit_rows,
                 bool per_segment_logits);
   void chain(const void* steps, int n_steps, const void* next);  // kern::ChainStep[n_steps], next chain's first
 
   ModelConfig cfg_;
   int dtype_, device_;
+  int tp_rank_ = 0, tp_size_ = 1;
+  int dl_ = 0, fl_ = 0, vl_ = 0;  // local attention width, MLP width, vocab rows
+  std::shared_ptr<coll::Collective> comm_;
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Weights> w_;
   std::unique_ptr<Workspace> ws_;

@@ -51,6 +51,11 @@ struct Epilogue {
 // ---- weights (PCG32 jump-ahead; bit-identical to the reference's fill_uniform) ----
 void init_uniform(int dtype, void* dst, uint64_t count, uint64_t stream_seed, float scale, cudaStream_t s);
 void fill_const(float* dst, uint64_t count, float v, cudaStream_t s);
+void init_uniform_block(int dtype, void* dst, int64_t rows, int64_t cols, uint64_t seed, float scale, int64_t row0,
+                        int64_t col0, int64_t full_cols, cudaStream_t s);
+// tensor parallel helpers
+void add_inplace(float* h, const float* part, int64_t n, cudaStream_t s);
+void interleave_shards(const float* in, int T, int64_t rows, int64_t Vl, float* out, cudaStream_t s);
 
 // ---- small ops ----
 void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table, const float* abs_table,

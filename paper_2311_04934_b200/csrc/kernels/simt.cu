@@ -67,6 +67,70 @@ void init_uniform(int dtype, void* dst, uint64_t count, uint64_t seed, float sca
   PCB_CUDA(cudaGetLastError());
 }
 
+// Block of a larger stream-backed [*][full_cols] tensor: dst[i][j] = element
+// (row0 + i) * full_cols + col0 + j of the stream (tensor-parallel shards: row ranges of
+// column-parallel weights, column ranges of row-parallel ones), one jump per row chunk.
+template <typename T>
+__global__ void k_init_uniform_block(T* dst, int64_t rows, int64_t cols, uint64_t seed, float scale, int64_t row0,
+                                     int64_t col0, int64_t full_cols, int64_t chunk) {
+  const int64_t chunks_per_row = (cols + chunk - 1) / chunk;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * chunks_per_row) return;
+  const int64_t i = t / chunks_per_row, j0 = (t % chunks_per_row) * chunk;
+  const int64_t j1 = min(j0 + chunk, cols);
+  uint64_t state = lcg_advance(seed + kInc, static_cast<uint64_t>((row0 + i) * full_cols + col0 + j0) + 1);
+  for (int64_t j = j0; j < j1; ++j) {
+    uint32_t x = pcg_out(state);
+    state = state * kMul + kInc;
+    float u = __fmul_rn(static_cast<float>(x >> 8), 1.0f / 16777216.0f);
+    float w = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), scale);
+    st_f(dst, i * cols + j, w);
+  }
+}
+void init_uniform_block(int dtype, void* dst, int64_t rows, int64_t cols, uint64_t seed, float scale, int64_t row0,
+                        int64_t col0, int64_t full_cols, cudaStream_t s) {
+  const int64_t chunk = 256;
+  const int64_t threads = rows * ((cols + chunk - 1) / chunk);
+  const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
+  if (dtype == F32)
+    k_init_uniform_block<float><<<blocks, 256, 0, s>>>(static_cast<float*>(dst), rows, cols, seed, scale, row0, col0,
+                                                        full_cols, chunk);
+  else
+    k_init_uniform_block<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), rows, cols, seed,
+                                                                scale, row0, col0, full_cols, chunk);
+  PCB_CUDA(cudaGetLastError());
+}
+
+// h += part (tensor-parallel: the all-reduced partial sums of a row-parallel GEMM)
+__global__ void k_add_inplace(float* __restrict__ h, const float* __restrict__ part, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    h[i] = __fadd_rn(h[i], part[i]);
+}
+void add_inplace(float* h, const float* part, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1184));
+  launch_k(k_add_inplace, dim3(blocks), dim3(256), 0, s, 1, h, part, n);
+  PCB_CUDA(cudaGetLastError());
+}
+
+// vocab shards gathered rank-major [T][rows][Vl] -> logits rows [rows][T*Vl]
+__global__ void k_interleave_shards(const float* __restrict__ in, int T, int64_t rows, int64_t Vl, float* __restrict__ out) {
+  const int64_t n = T * rows * Vl;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (T * Vl), rem = i % (T * Vl), t = rem / Vl, v = rem % Vl;
+    out[i] = in[(t * rows + r) * Vl + v];
+  }
+}
+void interleave_shards(const float* in, int T, int64_t rows, int64_t Vl, float* out, cudaStream_t s) {
+  const int64_t n = T * rows * Vl;
+  if (n <= 0) return;
+  k_interleave_shards<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1184)), 256, 0, s>>>(in, T, rows, Vl,
+                                                                                                      out);
+  PCB_CUDA(cudaGetLastError());
+}
+
 __global__ void k_fill(float* d, uint64_t n, float v) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     d[i] = v;
