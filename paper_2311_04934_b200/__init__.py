@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = [
     "PromptCacheError", "Schema", "Prompt", "Model", "KV", "ModuleStore", "ServeResponse",
-    "serve", "serve_batch", "oracle_serve", "TPGroup", "nccl_unique_id", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
+    "serve", "serve_batch", "oracle_serve", "TPGroup", "nccl_unique_id", "tp_shard_plan", "share_nccl_id", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
     "F32", "BF16", "FAST", "SLOW", "lib", "LIB_PATH",
 ]
 
@@ -253,6 +253,28 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().pcb_nccl_unique_id(buf))
     return buf.raw
+
+
+def tp_shard_plan(config: dict, tp_size: int) -> list:
+    """Per rank, the slices of the reference tensors a head-sharded model holds (mirrors
+    Model::Model, model.cpp): rows of wq/wk/wv and w1 and unembed (column-parallel GEMMs),
+    columns of wo and w2 (row-parallel GEMMs, all-reduced), heads and KV columns."""
+    d = config.get("hidden", config["n_heads"] * config["head_dim"])
+    H, V = config["n_heads"], config["vocab_size"]
+    if H % tp_size or V % tp_size:
+        raise PromptCacheError(3, "InvalidConfig: n_heads and vocab_size must divide by the tensor-parallel size")
+    dl, fl, vl = d // tp_size, 4 * d // tp_size, V // tp_size
+    return [{"heads": (r * H // tp_size, (r + 1) * H // tp_size), "qkv_rows": (r * dl, (r + 1) * dl),
+             "wo_cols": (r * dl, (r + 1) * dl), "kv_cols": (r * dl, (r + 1) * dl),
+             "w1_rows": (r * fl, (r + 1) * fl), "w2_cols": (r * fl, (r + 1) * fl),
+             "unembed_rows": (r * vl, (r + 1) * vl)} for r in range(tp_size)]
+
+
+def share_nccl_id(dist, make=None) -> bytes:
+    """Rank 0 creates the NCCL unique id, every rank of the torch.distributed group receives it."""
+    obj = [(make or nccl_unique_id)() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
 class TPGroup(_Handle):
