@@ -125,10 +125,30 @@ def partition(n: int, rank: int, world: int) -> list:
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    def __init__(self, device: int):
-        self.device, self.rows, self.proc = device, [], None
+    """SM clock + clock-event reasons sampled DURING the timed region: NVML polled every 5 ms from a
+    thread (a 10-step region lasts tens of ms, too short for nvidia-smi's 100 ms loop); nvidia-smi
+    as the fallback when pynvml is missing."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device: int, period_s: float = 0.005):
+        self.device, self.period, self.rows, self.proc, self.nvml = device, period_s, [], None, None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx))
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.nvml[1], pynvml.NVML_CLOCK_SM)
+            self._sample()  # at least one sample even for a very short region
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
         try:
@@ -141,13 +161,43 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _sample(self):
+        pynvml, h = self.nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:  # noqa: BLE001
+            bits = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((sm, self.max_mhz, bits))
+
+    def _poll(self):
+        while not self.stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                return
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
-                self.rows.append(parts)
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                bits = 0
+                for i, nm in enumerate(names):
+                    if parts[2 + i].lower() == "active":
+                        bits |= next(k for k, v in self.REASONS.items() if v == nm)
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), bits))
+                except ValueError:
+                    pass
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -157,13 +207,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({v for r in self.rows for k, v in self.REASONS.items() if r[2] & k})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -549,7 +597,8 @@ def run_ours(a) -> None:
             "precompute_ms": precompute_ms,
             "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "gemm_tc (tcgen05 swap-AB weight streaming, all GEMMs of a step)",
+            "roofline": {"bound": "hbm", "kernel": "k_chain (persistent tcgen05 GEMM/LayerNorm chains: every GEMM "
+                                                   "of a step, swap-AB weight streaming)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                          "traffic": traffic, "traffic_unit": "bytes per step (all GEMM launches)",
                          "traffic_source": traffic_src, "peak_source": peak_src,

@@ -72,9 +72,11 @@ def main(tag):
         a[0] += 1
         a[1] += k[i]["gpu__time_duration.sum"]
         a[2] += k[i].get("dram__bytes_read.sum", 0) + k[i].get("dram__bytes_write.sum", 0)
-    gemm_traffic = agg.get("k_gemm_sk", [0, 0, 0])[2]
+    gemm_kernels = ("k_chain", "k_gemm_sk")  # the GEMM class: persistent chains (+ any per-GEMM launches)
+    gemm_traffic = sum(agg[g][2] for g in gemm_kernels if g in agg)
     with open(os.path.join(dst, f"{tag}_traffic.json"), "w") as f:
-        json.dump({"gemm_dram_bytes_per_step": gemm_traffic, "gemm_launches_per_step": agg["k_gemm_sk"][0],
+        json.dump({"gemm_dram_bytes_per_step": gemm_traffic,
+                   "gemm_launches_per_step": sum(agg[g][0] for g in gemm_kernels if g in agg),
                    "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over one cached request "
                              f"(profiles/{tag}_launches.csv)"}, f, indent=1)
 
@@ -93,7 +95,7 @@ def main(tag):
             "lts__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
             "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active"]
-    for kern in ("k_gemm_sk", "k_attn_tc", "k_assemble"):
+    for kern in ("k_chain", "k_gemm_sk", "k_attn_tc", "k_assemble"):
         rep = os.path.join(src, f"full_{kern}.ncu-rep")
         if not os.path.exists(rep):
             continue
