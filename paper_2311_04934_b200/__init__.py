@@ -23,7 +23,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpcb200.so")
+LIB_PATH = os.environ.get("PCB_LIB_PATH") or os.path.join(HERE, "lib", "libpcb200.so")  # override: A/B builds
 F32, BF16 = 0, 1
 FAST, SLOW = 0, 1
 

@@ -2,7 +2,7 @@
 // against a range of key rows of the assembled cache (reference model.cpp:401-427:
 // causal by sequence order, query i sees keys j <= P + i).
 //
-//   warp 0     TMA: Q tile once, then K/V blocks of 64 keys (KV_STAGES-deep ring)
+//   warp 0     TMA: Q tile once, then K/V blocks of 64 keys (ring as deep as smem allows)
 //   warp 1     TMEM alloc + MMA issue: S_j = Q K_j^T (M=128, N=64, K=hd) into one of
 //              two TMEM score buffers, O += P_j V_j (M=128, N=hd, K=64; V is an
 //              MN-major operand) accumulated in TMEM across all blocks
@@ -26,7 +26,11 @@ CUtensorMap tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, uint32_t
 
 namespace {
 
-constexpr int BQ = 128, BKV = 64, kAttnThreads = 192, KV_STAGES = 3;
+constexpr int BQ = 128, BKV = 64, kAttnThreads = 192;
+constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
+#ifndef PCB_ATTN_STAGES
+#define PCB_ATTN_STAGES 6
+#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: stale max tolerated up to 2^8
 
 template <int HD>
@@ -36,7 +40,11 @@ struct AttnSmem {
   static constexpr int kKV = BKV * HD * 2;
   static constexpr int kStage = 2 * kKV;  // K + V
   static constexpr int kP = BQ * BKV * 2;  // one P buffer (two are used)
-  static constexpr int kBytes = kQ + KV_STAGES * kStage + 2 * kP + 1024 + 1024;
+  // as many K/V stages as fit next to Q and the two P buffers (a stage is held from its
+  // TMA load through the PV MMA, so depth is what keeps HBM busy on long caches)
+  static constexpr int kStagesFit = (kSmemMax - kQ - 2 * kP - 2048) / kStage;
+  static constexpr int kStages = kStagesFit > PCB_ATTN_STAGES ? PCB_ATTN_STAGES : kStagesFit;
+  static constexpr int kBytes = kQ + kStages * kStage + 2 * kP + 1024 + 1024;
   static constexpr uint32_t kTmemCols = 2 * BKV + HD <= 256 ? 256 : 512;
 };
 
@@ -84,6 +92,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   using S = AttnSmem<HD>;
+  constexpr int KV_STAGES = S::kStages;
   constexpr int kRedRow = HD + 4;  // padded fp32 row of a parked partial O
   static_assert(BQ * (kRedRow + 2) * 4 <= KV_STAGES * S::kStage, "split merge buffer must fit the K/V stages");
   extern __shared__ uint8_t smem_raw[];
@@ -206,10 +215,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int64_t limit = p.P + qi;  // last visible key (sequence order)
     const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
     float m = -INFINITY, l = 0.f;
+    // a warp whose 32 query rows are all past n (the suffix fills half a 128-row tile)
+    // only keeps the barrier protocol: its P rows feed O rows nobody reads
+    const bool live = q0 + qd * 32 < p.n;
     for (int it = 0; it < nb; ++it) {
       const int64_t j0 = (b0 + it) * BKV;
+      if (!live) {
+        if (it > 0) mbar_wait(p_full, (it - 1) & 1);  // never arrive into an earlier phase
+        mbar_arrive(p_full);
+        continue;
+      }
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
-      if (threadIdx.x == 64) probe(p, 0, it);
+      if (threadIdx.x == 128) probe(p, 0, it);
       tc_fence_after();
       float sv[BKV];
       {
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
         for (int c = 0; c < BKV; ++c) sv[c] = __uint_as_float(raw[c]);
       }
-      if (threadIdx.x == 64) probe(p, 6, it);
+      if (threadIdx.x == 128) probe(p, 6, it);
       // scores stay raw (unscaled); the 1/sqrt(hd) * log2(e) factor is folded into
       // one FFMA per element in front of ex2.approx
       if (j0 + BKV - 1 > limit) {  // diagonal block only
@@ -228,9 +245,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int c = 0; c < BKV; ++c)
           if (j0 + c > limit) sv[c] = -INFINITY;
       }
-      float bm = sv[0];
+      // 8 independent max chains + a 3-level tree (a single chain is 63 dependent FMNMX)
+      float mx[8];
 #pragma unroll
-      for (int c = 1; c < BKV; ++c) bm = fmaxf(bm, sv[c]);
+      for (int c = 0; c < 8; ++c) mx[c] = sv[c];
+#pragma unroll
+      for (int c = 8; c < BKV; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
+#pragma unroll
+      for (int w = 4; w; w >>= 1)
+#pragma unroll
+        for (int c = 0; c < w; ++c) mx[c] = fmaxf(mx[c], mx[c + w]);
+      const float bm = mx[0];
       // lazy max update: move the reference max only when it grows by > 2^8
       const bool grow = bm > m + kRescaleThreshold / p.scale_log2 || (m == -INFINITY && bm > -INFINITY);
       if (__any_sync(0xffffffffu, grow) && it > 0) {
@@ -253,21 +278,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         m = bm;
       }
       const float mb = (m == -INFINITY) ? 0.f : m * p.scale_log2;  // all scores -inf when m is
-      float bsum = 0.f;
+      float bs[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
       uint32_t packed[BKV / 2];
 #pragma unroll
       for (int c = 0; c < BKV; c += 2) {
         const float p0 = fast_exp2(fmaf(sv[c], p.scale_log2, -mb));
         const float p1 = fast_exp2(fmaf(sv[c + 1], p.scale_log2, -mb));
-        bsum += p0 + p1;
+        bs[(c >> 1) & 3] += p0 + p1;
         __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
         packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
       }
-      l += bsum;
-      if (threadIdx.x == 64) probe(p, 7, it);
+      l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
+      if (threadIdx.x == 128) probe(p, 7, it);
       // P buffer it&1 is free once PV(it-2) completed
       if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
-      if (threadIdx.x == 64) probe(p, 8, it);
+      if (threadIdx.x == 128) probe(p, 8, it);
       uint8_t* prow = sP + (it & 1) * S::kP + r * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -276,8 +301,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
+      // a fast warp must not arrive for block it while block it-1's phase is still
+      // collecting arrivals (its arrival would complete that phase early)
+      if (it > 0) mbar_wait(p_full, (it - 1) & 1);
       mbar_arrive(p_full);
-      if (threadIdx.x == 64) probe(p, 1, it);
+      if (threadIdx.x == 128) probe(p, 1, it);
     }
     if (nb > 0) {
       mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
