@@ -415,6 +415,10 @@ void gemm_tc(const void* A, const void* Wp, int64_t M, int N, int K, const Epilo
   // PDL-launched GEMM overlaps this one's drain -- measured slower, 8.1 vs 6.6 ms per 7B
   // request: shallower pipelines and uneven CTA placement.  The few-token path is the
   // persistent chain kernel, chain_tc.cu.)
+  if (gemm_2sm_supported(M, N, K)) {
+    gemm_2sm(A, Wp, M, N, K, e, s);
+    return;
+  }
   if (M <= 16) launch_sk<16, 10>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
   else if (M <= 32) launch_sk<32, 10>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);
   else if (M <= 64) launch_sk<64, 8>(A, Wp, M, N, K, e, ws, ws_bytes, flags, s, sms);

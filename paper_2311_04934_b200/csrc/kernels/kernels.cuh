@@ -86,6 +86,10 @@ void gemm_simt(int dtype, const void* A, const void* W, int64_t M, int N, int K,
 // tcgen05 persistent stream-K GEMM (bf16 in, fp32 accumulate) over PACKED weights.
 // Requires K%64==0, N%128==0.  workspace >= 148*128*256*4 bytes; flags >= #SMs ints (zeroed once).
 bool gemm_tc_supported(int64_t M, int N, int K);
+// CTA-pair (cta_group::2) 256x256-tile GEMM for M >= 256 over the same packed weights
+// (gemm_2sm.cu); gemm_tc dispatches to it.
+bool gemm_2sm_supported(int64_t M, int N, int K);
+void gemm_2sm(const void* A, const void* W_packed, int64_t M, int N, int K, const Epilogue& e, cudaStream_t s);
 // debug: GEMM timeline probe (PCB_GEMM_PROBE=1); shapes [n][4] = {M,N,K,ctas}, times [n][160][4]
 int gemm_probe_dump(int64_t* shapes, unsigned long long* times, int max_launches);
 void gemm_tc(const void* A, const void* W_packed, int64_t M, int N, int K, const Epilogue& e, float* workspace,
