@@ -46,6 +46,8 @@ constexpr int kWTileC = 128 * 64 * 2;
 struct PhaseDev {
   int kind;  // CHAIN_GEMM / CHAIN_LN
   int N, K, kbs;
+  int S;      // k-splits per 128-row weight tile (1: whole tiles; 2 or 4 when tiles are few)
+  int items;  // tiles * S work items, item i -> CTA i mod C
   int64_t M, units;
   const uint8_t* w;
   const float* ln_src;
@@ -228,39 +230,38 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Work items of a GEMM phase: item i = (tile i / S, k-split i % S) with k-blocks
+  // [j kbs / S, (j+1) kbs / S); CTA c takes items c, c + C, ...  S = 1 (tiles >= C/2):
+  // every tile finishes inside one CTA, straight from TMEM.  S = 2 or 4 (few tiles: Wo,
+  // W2): the S CTAs of a tile each park a partial and then finish 1/S of its token
+  // columns from all S partials (one batch of loads, summed in split order).
+  auto item_kb = [](const PhaseDev& P, int i, int& tile, int& kb0, int& kb1) {
+    tile = i / P.S;
+    const int j = i - tile * P.S;
+    kb0 = j * P.kbs / P.S;
+    kb1 = (j + 1) * P.kbs / P.S;
+  };
   if (warp == 0) {
     // ---- W producer: never waits for a phase boundary ----
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();
-      // L2 prefetch runs pf_units ahead of the bulk copies (and past the end of this
-      // chain into the next one), so HBM keeps streaming through phase boundaries and
-      // the attention launch between chains; the ring then refills at L2 speed.
-      WCursor pf{-1, 0, 0};
-      pf.settle(p, c, C);
-      int64_t issued = 0, prefetched = 0;
       int it = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
         const PhaseDev& P = p.ph[ph];
         if (P.kind != CHAIN_GEMM) continue;
-        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
-        for (int64_t g = g0; g < g1; ++g, ++it, ++issued) {
-          for (; pf.valid(p) && prefetched < issued + p.pf_units; ++prefetched) {
-            if (prefetched >= issued + STAGES) prefetch_l2(pf.addr(p), kWTileC);  // the ring covers the first STAGES
-            ++pf.g;
-            pf.settle(p, c, C);
+        for (int i = c; i < P.items; i += C) {
+          int tile, kb0, kb1;
+          item_kb(P, i, tile, kb0, kb1);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            mbar_expect_tx(&full[s], S::kStage);
+            // packed tiles of one 128-row block are contiguous along K
+            bulk_load(smem + s * S::kStage, P.w + (static_cast<int64_t>(tile) * P.kbs + kb) * kWTileC, kWTileC,
+                      &full[s], pol_w);
           }
-          const int s = it % STAGES;
-          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          mbar_expect_tx(&full[s], S::kStage);
-          // unit g = (n_tile, k-block): packed tiles of one 128-row block are contiguous along K
-          bulk_load(smem + s * S::kStage, P.w + g * kWTileC, kWTileC, &full[s], pol_w);
         }
         ctl(p, ph, 3);
-      }
-      for (; pf.valid(p) && prefetched < issued + p.pf_units; ++prefetched) {  // into the next chain
-        if (prefetched >= issued) prefetch_l2(pf.addr(p), kWTileC);
-        ++pf.g;
-        pf.settle(p, c, C);
       }
     }
   } else if (warp == 2) {
@@ -270,40 +271,40 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
       int it = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
         const PhaseDev& P = p.ph[ph];
-        if (P.kind != CHAIN_GEMM) continue;
-        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
-        if (g0 == g1) continue;
+        if (P.kind != CHAIN_GEMM || c >= P.items) continue;
         ctl(p, ph, 6);
         if (ph == 0) pdl_wait();
         else grid_wait(p, ph);
         ctl(p, ph, 7);
         fence_proxy_async_global();  // generic-proxy stores of other CTAs -> our TMA reads
         ctl(p, ph, 0);
-        for (int64_t g = g0; g < g1; ++g, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          const int kx = static_cast<int>(g % P.kbs) * 64;
-          tma_load_2d_hint(smem + s * S::kStage + kWTileC, &p.tm[ph], &full[s], kx, 0, pol_x);
+        for (int i = c; i < P.items; i += C) {
+          int tile, kb0, kb1;
+          item_kb(P, i, tile, kb0, kb1);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            tma_load_2d_hint(smem + s * S::kStage + kWTileC, &p.tm[ph], &full[s], kb * 64, 0, pol_x);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer ----
+    // ---- MMA issuer: one accumulator per item ----
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
       int it = 0, seg = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
         const PhaseDev& P = p.ph[ph];
         if (P.kind != CHAIN_GEMM) continue;
-        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
-        const int kbs = P.kbs;
-        for (int64_t g = g0; g < g1; ++seg) {
-          const int64_t ge = min(g1, (g / kbs + 1) * kbs);
+        for (int i = c; i < P.items; i += C, ++seg) {
+          int tile, kb0, kb1;
+          item_kb(P, i, tile, kb0, kb1);
           const int buf = seg & 1;
           mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t acc = tmem + buf * BN;
-          for (int64_t u = g; u < ge; ++u, ++it) {
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&full[s], (it / STAGES) & 1);
             tc_fence_after();
@@ -311,11 +312,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               umma_bf16(acc, sw128_kmajor_desc(wa + k * 32), sw128_kmajor_desc(xb + k * 32), idesc,
-                        (u > g || k > 0) ? 1u : 0u);
+                        (kb > kb0 || k > 0) ? 1u : 0u);
             umma_commit(&empty[s]);
           }
           umma_commit(&acc_full[buf]);
-          g = ge;
         }
         ctl(p, ph, 1);
       }
@@ -341,57 +341,99 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         for (int64_t r = c; r < P.M; r += C) ln_row(P, r, red, et);
       } else {
         const Epilogue& e = P.e;
-        const int kbs = P.kbs;
         const int64_t M = P.M;
+        const int Mc = static_cast<int>(M < BN ? M : BN);
         const int epoch = p.epoch0 + ph;
-        float* ws = p.ws + (ph & 1) * p.ws_half;
-        const int64_t g0 = unit_begin(c, P.units, C), g1 = unit_begin(c + 1, P.units, C);
-        for (int64_t g = g0; g < g1; ++seg) {
-          const int64_t t = g / kbs;
-          const int64_t tb = t * kbs, te = tb + kbs;
-          const int64_t ge = min(g1, te);
-          const int n = static_cast<int>(t) * 128 + row;
+        float* ws = p.ws + (ph & 1) * p.ws_half;  // [items][128][BN] partials
+        for (int i = c; i < P.items; i += C, ++seg) {
+          const int tile = i / P.S, j = i - tile * P.S;
+          const int n = tile * 128 + row;
           const int buf = seg & 1;
           const uint32_t acc = tmem + buf * BN + lane_off;
-          EpiPre cur;
-          if (g == tb) epi_prefetch(e, n, P.N, 0, M, cur);
+          EpiPre cur, nxt;
+          if (P.S == 1) epi_prefetch(e, n, P.N, 0, M, cur);  // before the accumulator is ready
           mbar_wait(&acc_full[buf], (seg >> 1) & 1);
           tc_fence_after();
           if (et == 0) ctl(p, ph, 4);
-          if (g > tb) {
-            // tile started in an earlier CTA: park the partial for its owner
-            float* dst = ws + (static_cast<int64_t>(c) * 128 + row) * BN;
+          if (P.S == 1) {
 #pragma unroll 1
-            for (int cc = 0; cc < BN; cc += 16) {
+            for (int cc = 0; cc < Mc; cc += 16) {
+              if (cc + 16 < Mc) epi_prefetch(e, n, P.N, cc + 16, M, nxt);
+              tmem_ld16(acc + cc, v);
+              epi_chunk(e, n, P.N, cc, M, v, cur);
+              cur = nxt;
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+            if (et == 0) ctl(p, ph, 5);
+            continue;
+          }
+          // split tile: park this k-split's partial, then finish a 1/S slice of the
+          // token columns from all S partials of the tile
+          {
+            float* dst = ws + (static_cast<int64_t>(i) * 128 + row) * BN;
+#pragma unroll 1
+            for (int cc = 0; cc < Mc; cc += 16) {
               tmem_ld16(acc + cc, v);
 #pragma unroll
-              for (int j = 0; j < 16; j += 4)
-                *reinterpret_cast<float4*>(dst + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              for (int x = 0; x < 16; x += 4)
+                *reinterpret_cast<float4*>(dst + cc + x) = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
             }
-            tc_fence_before();
-            mbar_arrive(&acc_empty[buf]);
-            // one gpu-scope release by et 0 (st_release) publishes the CTA's partial: bar.sync
-            // orders the other threads' stores before it (cumulativity)
-            named_bar(1, 128);
-            if (et == 0) st_release(p.flags + c, epoch);
-          } else {
-            const int c_last = ge < te ? cta_of(te - 1, P.units, C) : c;
-            if (c_last > c) {
-              for (int pp = c + 1 + et; pp <= c_last; pp += 128)
-                for (uint32_t spins = 0; has_units(pp, P.units, C) && ld_relaxed(p.flags + pp) < epoch;) {
-                  __nanosleep(64);
-                  if (++spins == (1u << 25)) wait_timeout("chain stream-K flag", p.flags + pp, epoch);
-                }
-              fence_acquire_gpu();
-              named_bar(1, 128);
-            }
-            if (et == 0) ctl(p, ph, 5);
-            owner_finish<BN>(e, acc, n, P.N, M, ws, c, c_last, P.units, C, row, cur,
-                             (p.tl && et == 0) ? p.tl + (static_cast<size_t>(ph) * 160 + blockIdx.x) * 12 + 8 : nullptr);
-            tc_fence_before();
-            mbar_arrive(&acc_empty[buf]);
           }
-          g = ge;
+          tc_fence_before();
+          mbar_arrive(&acc_empty[buf]);
+          // one gpu-scope release by et 0 publishes the partial: bar.sync orders the other
+          // threads' stores before it (cumulativity)
+          named_bar(1, 128);
+          if (et == 0) st_release(p.flags + i, epoch);
+          const int Mr = (Mc + 3) & ~3;
+          const int sw = ((Mr + P.S - 1) / P.S + 3) & ~3;
+          const int s0 = j * sw, s1 = min(Mr, s0 + sw);
+          const int64_t lim = min(static_cast<int64_t>(s1), M);
+          if (s0 < lim) epi_prefetch(e, n, P.N, s0, lim, cur);
+          const int base = tile * P.S;
+          if (et < P.S)
+            for (uint32_t spins = 0; ld_relaxed(p.flags + base + et) < epoch;) {
+              __nanosleep(32);
+              if (++spins == (1u << 25)) wait_timeout("chain split flag", p.flags + base + et, epoch);
+            }
+          fence_acquire_gpu();
+          named_bar(1, 128);
+          if (et == 0) ctl(p, ph, 5);
+#pragma unroll 1
+          for (int m0 = s0; m0 < lim; m0 += 16) {
+            // all S partials of these 16 columns in one batch of independent loads
+            float4 f[4][4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+              if (jj < P.S) {
+                const float4* src = reinterpret_cast<const float4*>(ws + (static_cast<int64_t>(base + jj) * 128 + row) *
+                                                                              BN + m0);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) f[jj][x] = __ldcg(src + x);
+              }
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              v[4 * x] = f[0][x].x;
+              v[4 * x + 1] = f[0][x].y;
+              v[4 * x + 2] = f[0][x].z;
+              v[4 * x + 3] = f[0][x].w;
+            }
+#pragma unroll
+            for (int jj = 1; jj < 4; ++jj)
+              if (jj < P.S) {
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                  v[4 * x] += f[jj][x].x;
+                  v[4 * x + 1] += f[jj][x].y;
+                  v[4 * x + 2] += f[jj][x].z;
+                  v[4 * x + 3] += f[jj][x].w;
+                }
+              }
+            if (m0 + 16 < lim) epi_prefetch(e, n, P.N, m0 + 16, lim, nxt);
+            epi_chunk(e, n, P.N, m0, lim, v, cur);
+            cur = nxt;
+          }
         }
       }
       if (et == 0) ctl(p, ph, 2);
@@ -457,7 +499,10 @@ void launch_chain(const ChainStep* steps, int n, const ChainStep* next, float* w
       d.K = st.K;
       d.kbs = st.K / 64;
       d.units = static_cast<int64_t>(st.N / 128) * d.kbs;
-      if (!units_fit_u32(d.units, C)) throw std::runtime_error("chain: too many work units for the 32-bit split");
+      const int tiles = st.N / 128;
+      d.S = 2 * tiles > C ? 1 : std::min({4, C / tiles, d.kbs});
+      if (d.S == 3) d.S = 2;  // slices of 1/S of the columns: S in {1, 2, 4}
+      d.items = tiles * d.S;
       d.w = static_cast<const uint8_t*>(st.w);
       d.e = st.e;
       p.tm[i] = tmap_bf16_2d(st.x, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.K), BN);
