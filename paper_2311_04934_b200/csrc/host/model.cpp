@@ -531,7 +531,7 @@ static double gemm_alg_bytes(int dtype, int64_t M, int N, int K, int epi_kind) {
   return (double)N * K * es + (double)M * K * es + (double)M * N * out_b;
 }
 
-void Model::chain(const void* steps_v, int n_steps, const void* next) {
+void Model::chain(const void* steps_v, int n_steps) {
   const auto* steps = static_cast<const kern::ChainStep*>(steps_v);
   double bytes = 0, flops = 0;
   for (int i = 0; i < n_steps; ++i) {
@@ -544,7 +544,7 @@ void Model::chain(const void* steps_v, int n_steps, const void* next) {
     }
   }
   prof_begin();
-  kern::chain_tc(steps, n_steps, static_cast<const kern::ChainStep*>(next), ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->chain_flags(), ws_->chain_gbar(),
+  kern::chain_tc(steps, n_steps, ws_->gemm_ws, ws_->gemm_ws_bytes, ws_->chain_flags(), ws_->chain_gbar(),
                  ws_->chain_bar, stream_);
   prof_end(PROF_GEMM, bytes, flops);
 }
@@ -826,8 +826,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     kern::ChainStep steps[8];
     steps[0] = ln(W.h, n);
     steps[1] = mm(W.x, w_->wqkv[0], n, 3 * d, d, qkv_epi(0));
-    kern::ChainStep next_o = mm(W.attn, w_->wo[0], n, d, d, eo);
-    chain(steps, 2, &next_o);
+    chain(steps, 2);
     for (int l = 0; l < c.n_layers; ++l) {
       attention(l);
       int k = 0;
@@ -842,12 +841,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
         steps[k++] = ln(W.h + (n - logit_rows) * d, logit_rows);
         steps[k++] = mm(W.x, w_->unembed, logit_rows, c.vocab_size, d, ef);
       }
-      if (l + 1 < c.n_layers) {
-        next_o = mm(W.attn, w_->wo[l + 1], n, d, d, eo);
-        chain(steps, k, &next_o);
-      } else {
-        chain(steps, k, nullptr);
-      }
+      chain(steps, k);
     }
   } else {
     for (int l = 0; l < c.n_layers; ++l) {

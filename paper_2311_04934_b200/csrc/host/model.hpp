@@ -157,7 +157,7 @@ class Model {
   void gemm(const void* A, const void* W, int64_t M, int N, int K, const void* epi, bool packed);
   void run_impl(const BatchItem* items, int B, const uint8_t* mask, const int32_t* block_ids, int64_t logit_rows,
                 bool per_segment_logits);
-  void chain(const void* steps, int n_steps, const void* next);  // kern::ChainStep[n_steps], next chain's first
+  void chain(const void* steps, int n_steps);  // kern::ChainStep[n_steps]
 
   ModelConfig cfg_;
   int dtype_, device_;

@@ -22,9 +22,13 @@
 // global memory, release/acquire at gpu scope, proxy fences on both sides because the
 // consumers read through TMA).  All CTAs are co-resident: the grid is one CTA per SM
 // and dependents are released (PDL trigger) only after the first barrier proves it.
-// Within a GEMM phase the work split is the stream-K split of gemm_tc.cu (equal
-// weight bytes per SM, deterministic fix-up in CTA order), with per-phase epochs and
-// a partial-tile workspace double-buffered by phase parity.
+// Within a GEMM phase the work is tile-granular: a 128-row weight tile is one item
+// (finished straight from TMEM) when there are at least C/2 tiles, else it is split
+// along K into S = 2 or 4 items whose CTAs each park a partial and then finish 1/S of
+// the token columns from all S partials (one batch of loads, split order: deterministic).
+// A stream-K split (equal bytes per SM) was measured first: its owner-side fix-up at
+// every phase end cost 8-17 us per phase against ~2-6 us here.  Partials are double-
+// buffered by phase parity; flags carry per-phase epochs.
 #include <cuda.h>
 
 #include <algorithm>
@@ -66,9 +70,6 @@ struct ChainParams {
   int* flags;              // [C] partial-ready epochs
   unsigned long long* gbar;  // grid barrier arrival counter (monotonic)
   unsigned long long gbar_base;
-  int pf_units;              // L2 prefetch distance of the weight stream (units of 16 KB)
-  const uint8_t* next_w;     // first GEMM of the next chain (prefetched into L2 at the end)
-  int64_t next_units;
   unsigned long long* tl;    // timeline probe [phase][cta][4] (null: off)
 };
 
@@ -82,37 +83,6 @@ __device__ __forceinline__ void ctl(const ChainParams& p, int ph, int ev) {
     p.tl[(static_cast<size_t>(ph) * 160 + blockIdx.x) * 12 + ev] = t;
   }
 }
-
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
-               : "memory");
-}
-
-// This CTA's weight units of every GEMM phase in stream order, then its units of the
-// next chain's first GEMM: the L2 prefetch cursor of the W producer.
-struct WCursor {
-  int ph;  // phase index; n_phases = the next chain's first GEMM; > n_phases = done
-  int64_t g, g1;
-  __device__ void settle(const ChainParams& p, int c, int C) {
-    while (ph <= p.n_phases && g >= g1) {
-      ++ph;
-      if (ph < p.n_phases) {
-        if (p.ph[ph].kind != CHAIN_GEMM) continue;
-        g = unit_begin(c, p.ph[ph].units, C);
-        g1 = unit_begin(c + 1, p.ph[ph].units, C);
-      } else if (ph == p.n_phases && p.next_w) {
-        g = unit_begin(c, p.next_units, C);
-        g1 = unit_begin(c + 1, p.next_units, C);
-      } else {
-        ph = p.n_phases + 1;
-      }
-    }
-  }
-  __device__ bool valid(const ChainParams& p) const { return ph <= p.n_phases; }
-  __device__ const uint8_t* addr(const ChainParams& p) const {
-    return (ph < p.n_phases ? p.ph[ph].w : p.next_w) + g * (128 * 64 * 2);
-  }
-};
 
 template <int BN, int STAGES>
 struct ChainSmem {
@@ -455,10 +425,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 }
 
 std::atomic<int> g_chain_epoch{0};
-int g_chain_pf = [] {
-  const char* v = std::getenv("PCB_CHAIN_PF");
-  return v ? std::max(0, std::atoi(v)) : 0;
-}();
+
 
 constexpr int kProbeMax = 256;
 unsigned long long* g_ctl = nullptr;
@@ -477,7 +444,7 @@ unsigned long long* chain_probe_slot(int n_phases) {
 }
 
 template <int BN, int STAGES>
-void launch_chain(const ChainStep* steps, int n, const ChainStep* next, float* ws, size_t ws_bytes, int* flags, unsigned long long* gbar,
+void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int* flags, unsigned long long* gbar,
                   unsigned long long& gbar_count, cudaStream_t s, int sms) {
   using Sm = ChainSmem<BN, STAGES>;
   static bool attr = [] {
@@ -519,12 +486,7 @@ void launch_chain(const ChainStep* steps, int n, const ChainStep* next, float* w
   p.epoch0 = g_chain_epoch.fetch_add(n) + 1;
   p.gbar = gbar;
   p.gbar_base = gbar_count;
-  p.pf_units = g_chain_pf;
   p.tl = chain_probe_slot(n);
-  if (next && next->kind == CHAIN_GEMM) {
-    p.next_w = static_cast<const uint8_t*>(next->w);
-    p.next_units = static_cast<int64_t>(next->N / 128) * (next->K / 64);
-  }
   gbar_count += static_cast<unsigned long long>(n - 1) * C;  // one arrival per CTA per phase boundary
   PdlClass pc(PDL_GEMM);
   launch_k(k_chain<BN, STAGES>, dim3(C), dim3(kChainThreads), Sm::kBytes, s, 1, p);
@@ -534,7 +496,6 @@ void launch_chain(const ChainStep* steps, int n, const ChainStep* next, float* w
 
 bool chain_tc_supported(int64_t M, int N, int K) { return M >= 1 && M <= 128 && weight_packable(N, K); }
 bool chain_ln_supported(int d) { return d % 4 == 0 && d <= 8192; }
-void chain_set_prefetch(int units) { g_chain_pf = std::max(0, units); }
 
 int chain_probe_dump(unsigned long long* times, int max_launches, int* phases) {
   PCB_CUDA(cudaDeviceSynchronize());
@@ -547,7 +508,7 @@ int chain_probe_dump(unsigned long long* times, int max_launches, int* phases) {
   return n;
 }
 
-void chain_tc(const ChainStep* steps, int n_steps, const ChainStep* next, float* ws, size_t ws_bytes, int* flags,
+void chain_tc(const ChainStep* steps, int n_steps, float* ws, size_t ws_bytes, int* flags,
               unsigned long long* gbar, unsigned long long& gbar_count, cudaStream_t s) {
   if (n_steps <= 0) return;
   if (n_steps > kMaxPhases) throw std::runtime_error("chain: too many phases");
@@ -565,10 +526,10 @@ void chain_tc(const ChainStep* steps, int n_steps, const ChainStep* next, float*
     if (st.kind == CHAIN_LN && !chain_ln_supported(st.ln_d)) throw std::runtime_error("chain: unsupported LN width");
     M = std::max<int64_t>(M, st.M);
   }
-  if (M <= 16) launch_chain<16, 10>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
-  else if (M <= 32) launch_chain<32, 10>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
-  else if (M <= 64) launch_chain<64, 8>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
-  else launch_chain<128, 6>(steps, n_steps, next, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  if (M <= 16) launch_chain<16, 10>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else if (M <= 32) launch_chain<32, 10>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else if (M <= 64) launch_chain<64, 8>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else launch_chain<128, 6>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
 }
 
 }  // namespace pcb::kern

@@ -112,14 +112,11 @@ struct ChainStep {
 };
 bool chain_tc_supported(int64_t M, int N, int K);
 bool chain_ln_supported(int d);
-void chain_set_prefetch(int units);  // L2 prefetch distance (16 KB units; 0 = off)
 // debug: chain timeline probe (PCB_CHAIN_PROBE=1): times [n][8 phases][160 CTAs][4]
 int chain_probe_dump(unsigned long long* times, int max_launches, int* phases);
 // flags: >= #SMs ints (zeroed once, private to the chain); gbar: one zeroed u64 whose
 // arrival count the caller tracks in gbar_count (advanced by this call).
-// next: the first step of the chain that follows (its weights are prefetched into L2
-// at the end of this one), or null.
-void chain_tc(const ChainStep* steps, int n_steps, const ChainStep* next, float* ws, size_t ws_bytes, int* flags,
+void chain_tc(const ChainStep* steps, int n_steps, float* ws, size_t ws_bytes, int* flags,
               unsigned long long* gbar, unsigned long long& gbar_count, cudaStream_t s);
 
 // ---- attention over a KV cache ----

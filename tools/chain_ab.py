@@ -2,7 +2,7 @@
 timeline of the persistent chain kernel for one 7B-shape cached request.
 
   python tools/chain_ab.py [rounds]
-Variants are model options (set_option): chain on/off, chain L2 prefetch distance.
+Variants are model options (set_option): chain on/off.
 """
 import ctypes as C
 import os
@@ -32,7 +32,7 @@ def dump():
 
 VARIANTS = [
     ("per-GEMM kernels", {"chain": 0}),
-    ("chain", {"chain": 1, "chain_pf": 0}),
+    ("chain", {"chain": 1}),
 
 ]
 if os.environ.get("AB_VARIANTS"):
@@ -63,7 +63,6 @@ for name, v in res.items():
 
 # ---- chain timeline of one request ----
 m.set_option("chain", 1)
-m.set_option("chain_pf", int(os.environ.get("TL_PF", "0")))
 pcb.serve(st, s, parsed[0], max_new_tokens=1)
 m.sync()
 dump()
