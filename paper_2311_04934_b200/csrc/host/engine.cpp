@@ -466,9 +466,26 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
     int64_t cap = 0;
     for (auto& it : items) cap = std::max<int64_t>(cap, it.n_cached + static_cast<int64_t>(it.up.tokens.size()));
     if (store.batch_arenas.size() < items.size() || (!store.batch_arenas.empty() && store.batch_arenas[0]->cap < cap)) {
+      // one allocation, request caches at a uniform stride (one batched attention launch)
       const int64_t c = std::max<int64_t>(cap, store.batch_arenas.empty() ? 64 : store.batch_arenas[0]->cap);
+      const size_t nreq = std::max<size_t>(items.size(), micro_batch);
       store.batch_arenas.clear();
-      for (size_t k = 0; k < std::max<size_t>(items.size(), micro_batch); ++k) store.batch_arenas.push_back(m.alloc_kv(c));
+      store.batch_raw.reset();
+      model::KVPtr probe = m.alloc_kv(0);
+      const size_t req_bytes = static_cast<size_t>(c) * probe->row_bytes() * 2 * probe->n_layers;
+      void* raw = nullptr;
+      CK(cudaMalloc(&raw, req_bytes * nreq));
+      store.batch_raw = std::shared_ptr<void>(raw, [](void* p) { cudaFree(p); });
+      for (size_t k = 0; k < nreq; ++k) {
+        auto v = std::make_shared<model::KVBlock>();
+        v->dtype = probe->dtype;
+        v->n_layers = probe->n_layers;
+        v->hidden = probe->hidden;
+        v->cap = c;
+        v->view = true;
+        v->data = static_cast<char*>(raw) + k * req_bytes;
+        store.batch_arenas.push_back(v);
+      }
     }
     AsmScratch& sc = scratch_of(store);
     sc.ensure(0, 0, static_cast<int64_t>(V) * items.size());

@@ -134,6 +134,7 @@ struct Workspace {
   int d = 0, V = 0, dt = BF16;
   int32_t *tok = nullptr, *pos = nullptr, *kvpos = nullptr, *block = nullptr, *argmax = nullptr, *lrows = nullptr;
   int64_t* kvoff = nullptr;
+  int4* req = nullptr;  // batched attention: {first q row, n, P, 0} per request
   uint8_t* mask = nullptr;
   float* h = nullptr;
   void *x = nullptr, *q = nullptr, *attn = nullptr, *mid = nullptr;
@@ -155,6 +156,7 @@ struct Workspace {
 
   ~Workspace() {
     for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)lrows, (void*)kvoff,
+                    (void*)req,
                     (void*)mask, (void*)h, x, q,
                     attn, mid, (void*)logits, (void*)part, (void*)logits_loc, (void*)logits_gath, (void*)gemm_ws,
                     (void*)counters, (void*)attn_scratch})
@@ -181,6 +183,7 @@ struct Workspace {
       regrow(block, c * 4);
       regrow(kvoff, c * 8);
       regrow(lrows, c * 4);
+      regrow(req, c * 16);
       regrow(h, c * d * 4);
       regrow(x, c * d * es);
       regrow(q, c * d * es);
@@ -214,7 +217,7 @@ struct Workspace {
       regrow(counters, 65536 * 4);
       CK(cudaMemset(counters, 0, 65536 * 4));
     }
-    int64_t need_ints = 6 * n + rows + 16;
+    int64_t need_ints = 10 * n + rows + 32;
     if (need_ints > host_ints_cap) {
       for (int sl = 0; sl < 2; ++sl)
         if (staged[sl]) CK(cudaEventSynchronize(staged[sl]));
@@ -658,8 +661,13 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       for (int64_t j = 0; j < items[b].n; ++j, ++m) ko[m] = base + (items[b].kv->rows + j) * dl_;
       lr[b] = static_cast<int32_t>(m - 1);
     }
+    int4* rq = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(lr + B) + 15) & ~uintptr_t(15));
+    for (int b = 0; b < B; ++b)
+      rq[b] = make_int4(static_cast<int>(seg_start[b]), static_cast<int>(items[b].n),
+                        static_cast<int>(items[b].kv->rows), 0);
     CK(cudaMemcpyAsync(W.kvoff, ko, n * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(W.lrows, lr, B * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(W.req, rq, B * 16, cudaMemcpyHostToDevice, s));
   }
   W.release_staging(s);
 
@@ -739,7 +747,42 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     }
   };
 
+  // batched attention in one launch when the request caches sit at a uniform stride
+  int64_t req_stride = 0, max_P = 0, max_nb = 0;
+  bool batched_attn = B > 1 && tc_attn;
+  if (batched_attn) {
+    req_stride = static_cast<char*>(items[1].kv->data) - static_cast<char*>(items[0].kv->data);
+    for (int b = 0; b < B; ++b) {
+      batched_attn = batched_attn && req_stride > 0 && items[b].n <= 128 &&
+                     static_cast<char*>(items[b].kv->data) - static_cast<char*>(items[0].kv->data) == b * req_stride;
+      max_P = std::max(max_P, items[b].kv->rows);
+      max_nb = std::max(max_nb, items[b].n);
+    }
+  }
   auto attention = [&](int l) {
+    if (batched_attn) {
+      kern::AttnArgs ab = aa;
+      ab.n = n;
+      ab.P = 0;
+      ab.k = kv.k(l);
+      ab.v = kv.v(l);
+      ab.req = W.req;
+      ab.n_req = B;
+      ab.req_stride = req_stride;
+      ab.kv_cap = kv.cap;
+      ab.max_P = max_P;
+      ab.max_n = max_nb;
+      double bytes = 0, flops = 0;
+      for (int b = 0; b < B; ++b) {
+        const int64_t nb = items[b].n, Pb = items[b].kv->rows;
+        bytes += 2.0 * (Pb + nb) * dl_ * es + 2.0 * nb * dl_ * es;
+        flops += 4.0 * (double)nb * dl_ * (Pb + (nb + 1) / 2.0);
+      }
+      prof_begin();
+      kern::attention_tc(ab, W.attn_scratch, W.attn_scratch_bytes, s);
+      prof_end(PROF_ATTN, bytes, flops);
+      return;
+    }
     if (B > 1) {
       double bytes = 0, flops = 0;
       prof_begin();

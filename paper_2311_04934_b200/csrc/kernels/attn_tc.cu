@@ -59,6 +59,9 @@ struct AttnParams {
   int kv_head_major;
   int64_t kv_rows;  // rows per head plane (head-major layout)
   int* counters;    // [H] split arrival counters (zero between launches)
+  // batched requests (one launch for a micro-batch): blockIdx.x = request, per request
+  // {first q row, n, P}; K/V come from a 3-D tensor map {d, rows, request}
+  const int4* req = nullptr;
   unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
 };
 
@@ -110,9 +113,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q_tile = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, split = blockIdx.z;  // heaviest tiles first
+  const int h = blockIdx.y, split = blockIdx.z;
+  int64_t n_ = p.n, P_ = p.P, qrow0 = 0;
+  int breq = 0, q_tile = gridDim.x - 1 - blockIdx.x;  // heaviest tiles first
+  if (p.req) {
+    breq = blockIdx.x;
+    const int4 rq = p.req[breq];
+    qrow0 = rq.x;
+    n_ = rq.y;
+    P_ = rq.z;
+    q_tile = 0;
+  }
+  const int64_t total_ = P_ + n_;
   const int64_t q0 = static_cast<int64_t>(q_tile) * BQ;
-  const int64_t key_end = min(p.total, p.P + q0 + BQ);  // causal key range of this tile
+  const int64_t key_end = min(total_, P_ + q0 + BQ);  // causal key range of this tile
   const int64_t nblk = (key_end + BKV - 1) / BKV;
   const int64_t b0 = nblk * split / p.splits, b1 = nblk * (split + 1) / p.splits;
   const int nb = static_cast<int>(b1 - b0);
@@ -149,7 +163,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (elect_one() && nb > 0) {
       mbar_expect_tx(q_full, S::kQ);
       for (int a = 0; a < S::kAtoms; ++a)
-        tma_load_2d(sQ + a * (BQ * 128), &tmQ, q_full, h * HD + a * 64, static_cast<int>(q0));
+        tma_load_2d(sQ + a * (BQ * 128), &tmQ, q_full, h * HD + a * 64, static_cast<int>(qrow0 + q0));
       for (int it = 0; it < nb; ++it) {
         const int s = it % KV_STAGES;
         mbar_wait(&kv_empty[s], ((it / KV_STAGES) & 1) ^ 1);
@@ -162,8 +176,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int kx = p.kv_head_major ? 0 : h * HD;
         const int ky = p.kv_head_major ? static_cast<int>(h * p.kv_rows + j0) : j0;
         for (int a = 0; a < S::kAtoms; ++a) {
-          tma_load_2d(st + a * (BKV * 128), &tmK, &kv_full[s], kx + a * 64, ky);
-          tma_load_2d(st + S::kKV + a * (BKV * 128), &tmV, &kv_full[s], kx + a * 64, ky);
+          if (p.req) {
+            tma_load_3d(st + a * (BKV * 128), &tmK, &kv_full[s], kx + a * 64, ky, breq);
+            tma_load_3d(st + S::kKV + a * (BKV * 128), &tmV, &kv_full[s], kx + a * 64, ky, breq);
+          } else {
+            tma_load_2d(st + a * (BKV * 128), &tmK, &kv_full[s], kx + a * 64, ky);
+            tma_load_2d(st + S::kKV + a * (BKV * 128), &tmV, &kv_full[s], kx + a * 64, ky);
+          }
         }
       }
     }
@@ -212,12 +231,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
     const int64_t qi = q0 + r;       // query index within the n new rows
-    const int64_t limit = p.P + qi;  // last visible key (sequence order)
+    const int64_t limit = P_ + qi;  // last visible key (sequence order)
     const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
     float m = -INFINITY, l = 0.f;
     // a warp whose 32 query rows are all past n (the suffix fills half a 128-row tile)
     // only keeps the barrier protocol: its P rows feed O rows nobody reads
-    const bool live = q0 + qd * 32 < p.n;
+    const bool live = q0 + qd * 32 < n_;
     for (int it = 0; it < nb; ++it) {
       const int64_t j0 = (b0 + it) * BKV;
       if (!live) {
@@ -312,12 +331,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_after();
       if (p.splits == 1) {
         const float inv = 1.f / l;
-        __nv_bfloat16* dst = p.out + qi * p.d + h * HD;
+        __nv_bfloat16* dst = p.out + (qrow0 + qi) * p.d + h * HD;
 #pragma unroll 1
         for (int c = 0; c < HD; c += 16) {
           float ov[16];
           tmem_ld16(tO + lane_off + c, ov);
-          if (qi < p.n) {
+          if (qi < n_) {
             uint4 w[2];
             __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w);
 #pragma unroll
@@ -354,7 +373,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       constexpr int kTpr = 8;                     // threads per row
       constexpr int kXs = HD / kTpr;              // hd values per thread
       const uint32_t red0 = smem_u32(sKV);
-      for (int64_t row = split + static_cast<int64_t>(t / kTpr) * p.splits; row < p.n;
+      for (int64_t row = split + static_cast<int64_t>(t / kTpr) * p.splits; row < n_;
            row += static_cast<int64_t>(128 / kTpr) * p.splits) {
         float ms[8], ls[8];
         float M = -INFINITY;
@@ -384,7 +403,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
         }
         const float inv = 1.f / den;
-        __nv_bfloat16* dst = p.out + row * p.d + h * HD + x0;
+        __nv_bfloat16* dst = p.out + (qrow0 + row) * p.d + h * HD + x0;
 #pragma unroll
         for (int x = 0; x < kXs; x += 8) {
           uint4 v;
@@ -400,6 +419,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, S::kTmemCols);
+}
+
+// 3-D bf16 map {cols, rows, planes} (plane stride in bytes), box {64, box_rows, 1}, SW128
+CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t planes, uint64_t plane_stride,
+                         uint32_t box_rows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    PCB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &qr));
+    return reinterpret_cast<EncodeFn>(q);
+  }();
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cols, rows, planes};
+  cuuint64_t strides[2] = {cols * 2, plane_stride};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+  return m;
 }
 
 template <int HD>
@@ -424,13 +467,15 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   p.d = a.d;
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   p.out = static_cast<__nv_bfloat16*>(a.out);
-  const int q_tiles = static_cast<int>((a.n + BQ - 1) / BQ);
-  const int64_t nblk0 = (std::min<int64_t>(p.total, a.P + BQ) + BKV - 1) / BKV;  // tile 0 key blocks
+  const bool batched = a.n_req > 0;  // one launch over the requests of a micro-batch
+  const int q_tiles = batched ? a.n_req : static_cast<int>((a.n + BQ - 1) / BQ);
+  const int64_t nblk0 = batched ? (a.max_P + a.max_n + BKV - 1) / BKV
+                                : (std::min<int64_t>(p.total, a.P + BQ) + BKV - 1) / BKV;  // tile 0 key blocks
   // one CTA per SM; for single-tile (suffix) launches pick the split count that
   // minimises waves x blocks per CTA (+ a per-split fixed cost)
   const int base = q_tiles * a.H;
   int splits = 1;
-  if (q_tiles == 1 && base < 2 * sms) {
+  if ((q_tiles == 1 || batched) && base < 2 * sms) {
     int64_t best = -1;
     for (int s2 = 1; s2 <= std::max<int64_t>(1, std::min<int64_t>(nblk0 / 2, 8)); ++s2) {  // cluster <= 8
       const size_t need = static_cast<size_t>(a.H) * s2 * BQ * (HD + 2) * sizeof(float);
@@ -460,12 +505,18 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
     std::memset(dbg, 0, 12 * 64 * sizeof(unsigned long long));
     p.dbg = dbg;
   }
-  CUtensorMap tk = p.kv_head_major
-                       ? tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
-                       : tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
-  CUtensorMap tv = p.kv_head_major
-                       ? tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
-                       : tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+  CUtensorMap tk, tv;
+  if (batched) {
+    // request r's cache rows: {d, rows, request} with the request stride between planes
+    p.req = a.req;
+    tk = tmap_bf16_3d(a.k, a.d, a.kv_cap, a.n_req, a.req_stride, BKV);
+    tv = tmap_bf16_3d(a.v, a.d, a.kv_cap, a.n_req, a.req_stride, BKV);
+  } else {
+    tk = p.kv_head_major ? tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
+                         : tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+    tv = p.kv_head_major ? tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
+                         : tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+  }
   dim3 grid(q_tiles, a.H, splits);
   PdlClass pc(PDL_ATTN);
   launch_k(k_attn_tc<HD>, grid, dim3(kAttnThreads), Sm::kBytes, s, splits, tq, tk, tv, p);  // cluster = splits

@@ -136,6 +136,12 @@ struct AttnArgs {
   const int32_t* kv_pos = nullptr;     // [P+n] positions (alibi)
   int64_t i0 = 0, nq = -1;             // query sub-range [i0, i0+nq) (nq < 0: all n)
   int* counters = nullptr;             // tc split-KV: [H] zeroed arrival counters
+  // batched (tc only): n_req requests in one launch; req[r] = {first q row, n, P, 0} on the
+  // device; k/v = request 0's layer planes, request r's at + r * req_stride bytes (caches
+  // of one capacity kv_cap); q/out hold all requests' rows; n = total q rows
+  const int4* req = nullptr;
+  int n_req = 0;
+  int64_t req_stride = 0, kv_cap = 0, max_P = 0, max_n = 0;
 };
 void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s);
 size_t attention_simt_scratch(const AttnArgs& a);
