@@ -117,6 +117,9 @@ struct Weights {
   float* abs_table = nullptr;
   bool packed = false;  // every bf16 GEMM weight in the tcgen05 tile layout
   bool pk_qkv = false, pk_o = false, pk_1 = false, pk_2 = false, pk_un = false;  // per weight kind
+  // LN fold (bf16 chain): sum_k W[n][k] of the GEMMs that consume a LayerNorm output
+  std::vector<float*> wsum_qkv, wsum_1;
+  float* wsum_un = nullptr;
   std::vector<void*> owned;
   ~Weights() {
     for (void* p : owned) cudaFree(p);
@@ -140,6 +143,7 @@ struct Workspace {
   void *x = nullptr, *q = nullptr, *attn = nullptr, *mid = nullptr;
   float* logits = nullptr;
   float *part = nullptr, *logits_loc = nullptr, *logits_gath = nullptr;  // tensor parallel
+  float* lnstats = nullptr;  // LN fold: [hidden/128 tiles][cap_n][2]
   int tp = 1, Vl = 0;
   float* gemm_ws = nullptr;
   size_t gemm_ws_bytes = 0;
@@ -158,7 +162,8 @@ struct Workspace {
     for (void* p : {(void*)tok, (void*)pos, (void*)kvpos, (void*)block, (void*)argmax, (void*)lrows, (void*)kvoff,
                     (void*)req,
                     (void*)mask, (void*)h, x, q,
-                    attn, mid, (void*)logits, (void*)part, (void*)logits_loc, (void*)logits_gath, (void*)gemm_ws,
+                    attn, mid, (void*)logits, (void*)part, (void*)logits_loc, (void*)logits_gath, (void*)lnstats,
+                    (void*)gemm_ws,
                     (void*)counters, (void*)attn_scratch})
       if (p) cudaFree(p);
     for (auto& e : staged)
@@ -190,6 +195,7 @@ struct Workspace {
       regrow(attn, c * d * es);
       regrow(mid, c * 4 * d * es);
       if (tp > 1) regrow(part, c * d * 4);
+      regrow(lnstats, ((d + 127) / 128) * c * 8);
       cap_n = c;
     }
     if (rows > cap_rows) {
@@ -266,6 +272,7 @@ Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_si
   fl_ = 4 * c.hidden / tp_size;
   vl_ = c.vocab_size / tp_size;
   if (const char* v = std::getenv("PCB_CHAIN")) use_chain = v[0] != '0';
+  if (const char* v = std::getenv("PCB_LN_FOLD")) ln_fold = v[0] != '0';
   if (c.hidden != c.n_heads * c.head_dim) throw Error(ErrorCode::InvalidConfig, "hidden must equal n_heads * head_dim");
   if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 2 || c.head_dim % 2 != 0)
     throw Error(ErrorCode::InvalidConfig, "bad layer/head geometry");
@@ -313,7 +320,7 @@ Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_si
     float scale;
     int64_t rows, row0, col0, full_cols;
   };
-  auto make = [&](int N, int K, std::vector<Part> parts, bool pack) {
+  auto make = [&](int N, int K, std::vector<Part> parts, bool pack, float** row_sums = nullptr) {
     void* dst = w_->alloc(static_cast<size_t>(N) * K * es);
     char* gen = static_cast<char*>(pack ? staging : dst);
     size_t off = 0;
@@ -326,19 +333,26 @@ Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_si
                                  p.full_cols, stream_);
       off += static_cast<size_t>(p.rows) * K;
     }
+    if (row_sums && dtype == BF16) {
+      *row_sums = static_cast<float*>(w_->alloc(static_cast<size_t>(N) * 4));
+      kern::row_sums_bf16(gen, N, K, *row_sums, stream_);
+    }
     if (pack) kern::pack_weight_bf16(staging, dst, N, K, stream_);
     return dst;
   };
   const int r = tp_rank_;
-  w_->unembed = make(vl_, d, {{"unembed", ws, vl_, static_cast<int64_t>(r) * vl_, 0, d}}, w_->pk_un);
+  w_->unembed = make(vl_, d, {{"unembed", ws, vl_, static_cast<int64_t>(r) * vl_, 0, d}}, w_->pk_un, &w_->wsum_un);
   for (int l = 0; l < c.n_layers; ++l) {
     const int64_t h0 = static_cast<int64_t>(r) * dl_;
+    float *sq = nullptr, *s1 = nullptr;
     w_->wqkv.push_back(make(3 * dl_, d,
                             {{tname(l, "wq"), ws, dl_, h0, 0, d}, {tname(l, "wk"), ws, dl_, h0, 0, d},
                              {tname(l, "wv"), ws, dl_, h0, 0, d}},
-                            w_->pk_qkv));
+                            w_->pk_qkv, &sq));
+    w_->wsum_qkv.push_back(sq);
     w_->wo.push_back(make(d, dl_, {{tname(l, "wo"), ws, d, 0, h0, d}}, w_->pk_o));
-    w_->w1.push_back(make(fl_, d, {{tname(l, "w1"), ws, fl_, static_cast<int64_t>(r) * fl_, 0, d}}, w_->pk_1));
+    w_->w1.push_back(make(fl_, d, {{tname(l, "w1"), ws, fl_, static_cast<int64_t>(r) * fl_, 0, d}}, w_->pk_1, &s1));
+    w_->wsum_1.push_back(s1);
     w_->w2.push_back(make(d, fl_, {{tname(l, "w2"), ws2, d, 0, static_cast<int64_t>(r) * fl_, 4 * d}}, w_->pk_2));
   }
   if (staging) {
@@ -873,16 +887,49 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     for (int l = 0; l < c.n_layers; ++l) {
       attention(l);
       int k = 0;
-      steps[k++] = mm(W.attn, w_->wo[l], n, d, d, eo);
-      steps[k++] = ln(W.h, n);
-      steps[k++] = mm(W.x, w_->w1[l], n, 4 * d, d, eg);
-      steps[k++] = mm(W.mid, w_->w2[l], n, d, 4 * d, eo);
-      if (l + 1 < c.n_layers) {
+      if (ln_fold && d % 128 == 0) {
+        // LayerNorm folded into the GEMMs around it (no LN phases, two fewer grid
+        // barriers per layer): the residual phases (Wo, W2) also write bf16(h) and
+        // per-tile row sums; the next GEMM runs on bf16(h) and corrects its accumulator,
+        // LN(h) W^T = rstd (h W^T - mean * sum_k W)
+        auto res = [&](const void* x, const void* w, int K) {
+          kern::Epilogue e = eo;
+          e.x_out = W.x;
+          kern::ChainStep st = mm(x, w, n, d, K, e);
+          st.stats_out = W.lnstats;
+          st.stats_ld = static_cast<int>(n);
+          return st;
+        };
+        auto cons = [&](const void* w, int64_t rows, int N, kern::Epilogue e, const float* wsum, int64_t row0) {
+          e.ln_wsum = wsum;
+          kern::ChainStep st = mm(W.x, w, rows, N, d, e);
+          st.x = static_cast<const char*>(W.x) + row0 * d * static_cast<int64_t>(es);
+          st.stats_in = W.lnstats;
+          st.stats_tiles = d / 128;
+          st.stats_ld = static_cast<int>(n);
+          st.stats_row0 = static_cast<int>(row0);
+          st.ln_dim = d;
+          return st;
+        };
+        steps[k++] = res(W.attn, w_->wo[l], d);
+        steps[k++] = cons(w_->w1[l], n, 4 * d, eg, w_->wsum_1[l], 0);
+        steps[k++] = res(W.mid, w_->w2[l], 4 * d);
+        if (l + 1 < c.n_layers)
+          steps[k++] = cons(w_->wqkv[l + 1], n, 3 * d, qkv_epi(l + 1), w_->wsum_qkv[l + 1], 0);
+        else if (logit_rows > 0 && !per_segment_logits)
+          steps[k++] = cons(w_->unembed, logit_rows, c.vocab_size, ef, w_->wsum_un, n - logit_rows);
+      } else {
+        steps[k++] = mm(W.attn, w_->wo[l], n, d, d, eo);
         steps[k++] = ln(W.h, n);
-        steps[k++] = mm(W.x, w_->wqkv[l + 1], n, 3 * d, d, qkv_epi(l + 1));
-      } else if (logit_rows > 0 && !per_segment_logits) {
-        steps[k++] = ln(W.h + (n - logit_rows) * d, logit_rows);
-        steps[k++] = mm(W.x, w_->unembed, logit_rows, c.vocab_size, d, ef);
+        steps[k++] = mm(W.x, w_->w1[l], n, 4 * d, d, eg);
+        steps[k++] = mm(W.mid, w_->w2[l], n, d, 4 * d, eo);
+        if (l + 1 < c.n_layers) {
+          steps[k++] = ln(W.h, n);
+          steps[k++] = mm(W.x, w_->wqkv[l + 1], n, 3 * d, d, qkv_epi(l + 1));
+        } else if (logit_rows > 0 && !per_segment_logits) {
+          steps[k++] = ln(W.h + (n - logit_rows) * d, logit_rows);
+          steps[k++] = mm(W.x, w_->unembed, logit_rows, c.vocab_size, d, ef);
+        }
       }
       chain(steps, k);
     }

@@ -150,6 +150,7 @@ class Model {
   bool force_simt_gemm = false;  // testing: SIMT GEMM only
   bool force_simt_attn = false;  // testing: SIMT attention only
   bool use_chain = true;         // few-token GEMM/LN segments as one persistent chain kernel (PCB_CHAIN=0: off)
+  bool ln_fold = true;           // chain: LayerNorm folded into the neighbouring GEMMs (PCB_LN_FOLD=0: off)
   int64_t launches = 0;          // kernels launched by run() (bench evidence)
 
  private:

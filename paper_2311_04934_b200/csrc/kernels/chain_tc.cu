@@ -52,6 +52,11 @@ struct PhaseDev {
   int N, K, kbs;
   int S;      // k-splits per 128-row weight tile (1: whole tiles; 2 or 4 when tiles are few)
   int items;  // tiles * S work items, item i -> CTA i mod C
+  // folded LayerNorm: a residual phase writes per-(tile, token) {sum h, sum h^2} of the new
+  // residual; the next GEMM phase turns them into {mean, rstd} per token
+  float* stats_out;
+  const float* stats_in;
+  int stats_tiles, stats_ld, stats_row0, ln_dim;
   int64_t M, units;
   const uint8_t* w;
   const float* ln_src;
@@ -87,7 +92,7 @@ __device__ __forceinline__ void ctl(const ChainParams& p, int ph, int ev) {
 template <int BN, int STAGES>
 struct ChainSmem {
   static constexpr int kStage = kWTileC + BN * 128;
-  static constexpr int kBytes = STAGES * kStage + 1024 + 1024;
+  static constexpr int kBytes = STAGES * kStage + 1024 + 1024 + 1024 + 2 * 16 * 128 * 4;  // + LN-fold scratch
   static constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;
 };
 
@@ -176,6 +181,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   double* red = reinterpret_cast<double*>(acc_empty + 4);  // [4] LayerNorm partial sums
+  float2* lnst = reinterpret_cast<float2*>(smem + STAGES * S::kStage + 1024);  // [128] {mean, rstd}
+  float* colsum = reinterpret_cast<float*>(lnst + 128);  // [2][16 tokens][128 columns] h, h^2 of a chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x, c = blockIdx.x;
@@ -313,6 +320,57 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         const Epilogue& e = P.e;
         const int64_t M = P.M;
         const int Mc = static_cast<int>(M < BN ? M : BN);
+        const float2* ln = nullptr;
+        if (P.stats_in) {
+          // {mean, rstd} per token from the residual phase's per-tile partial sums (fp64, tile order)
+          if (et < Mc) {
+            double s1 = 0, s2 = 0;
+            const float2* src = reinterpret_cast<const float2*>(P.stats_in) + P.stats_row0 + et;
+#pragma unroll 1
+            for (int t0 = 0; t0 < P.stats_tiles; t0 += 8) {  // 8 independent loads per round trip
+              float2 st[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                st[u] = t0 + u < P.stats_tiles ? __ldcg(src + static_cast<int64_t>(t0 + u) * P.stats_ld)
+                                               : make_float2(0.f, 0.f);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                s1 += st[u].x;
+                s2 += st[u].y;
+              }
+            }
+            const double mean = s1 / P.ln_dim, var = fmax(s2 / P.ln_dim - mean * mean, 0.0);
+            lnst[et] = make_float2(static_cast<float>(mean), static_cast<float>(1.0 / sqrt(var + 1e-5)));
+          }
+          named_bar(1, 128);
+          ln = lnst;
+        }
+        // column sums of the new residual of one 16-token chunk -> stats_out[tile][m]
+        // (transposed through smem: each thread parks its 16 values, then 8 threads per
+        // token sum 16 columns each and combine with 3 shuffles)
+        auto stats_chunk = [&](int tile, int64_t m0, int64_t lim) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            colsum[j * 128 + row] = v[j];
+            colsum[2048 + j * 128 + row] = v[j] * v[j];
+          }
+          named_bar(1, 128);
+          const int j = et >> 3, g = (et & 7) * 16;
+          float a = 0.f, b = 0.f;
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            a += colsum[j * 128 + g + x];
+            b += colsum[2048 + j * 128 + g + x];
+          }
+#pragma unroll
+          for (int o = 4; o; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+          }
+          if ((et & 7) == 0 && m0 + j < lim)
+            reinterpret_cast<float2*>(P.stats_out)[static_cast<int64_t>(tile) * P.stats_ld + m0 + j] = make_float2(a, b);
+          named_bar(1, 128);
+        };
         const int epoch = p.epoch0 + ph;
         float* ws = p.ws + (ph & 1) * p.ws_half;  // [items][128][BN] partials
         for (int i = c; i < P.items; i += C, ++seg) {
@@ -330,7 +388,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             for (int cc = 0; cc < Mc; cc += 16) {
               if (cc + 16 < Mc) epi_prefetch(e, n, P.N, cc + 16, M, nxt);
               tmem_ld16(acc + cc, v);
-              epi_chunk(e, n, P.N, cc, M, v, cur);
+              epi_chunk(e, n, P.N, cc, M, v, cur, ln);
+              if (P.stats_out) stats_chunk(tile, cc, M);
               cur = nxt;
             }
             tc_fence_before();
@@ -401,7 +460,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 }
               }
             if (m0 + 16 < lim) epi_prefetch(e, n, P.N, m0 + 16, lim, nxt);
-            epi_chunk(e, n, P.N, m0, lim, v, cur);
+            epi_chunk(e, n, P.N, m0, lim, v, cur, ln);
+            if (P.stats_out) stats_chunk(tile, m0, lim);
             cur = nxt;
           }
         }
@@ -472,6 +532,12 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.items = tiles * d.S;
       d.w = static_cast<const uint8_t*>(st.w);
       d.e = st.e;
+      d.stats_out = st.stats_out;
+      d.stats_in = st.stats_in;
+      d.stats_tiles = st.stats_tiles;
+      d.stats_ld = st.stats_ld;
+      d.stats_row0 = st.stats_row0;
+      d.ln_dim = st.ln_dim;
       p.tm[i] = tmap_bf16_2d(st.x, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.K), BN);
     } else {
       d.ln_src = st.ln_src;

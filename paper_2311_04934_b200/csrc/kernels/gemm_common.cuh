@@ -62,9 +62,17 @@ __device__ __forceinline__ float gelu_bf16path(float x) {
 // throughput: fields are read once into registers, full chunks take an unguarded,
 // fully unrolled path, and only a ragged last chunk is guarded.
 __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int64_t m0, int64_t M, float* v,
-                                          const EpiPre& pre) {
+                                          const EpiPre& pre, const float2* lnst = nullptr) {
   const int kind = ep.kind;
   const int jn = M - m0 >= 16 ? 16 : static_cast<int>(M - m0);
+  if (lnst) {  // folded LayerNorm: {mean, rstd} of token m0 + j
+    const float ws = ep.ln_wsum[n];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float2 st = lnst[j < jn ? m0 + j : m0];
+      v[j] = st.y * fmaf(-st.x, ws, v[j]);
+    }
+  }
   if (kind == EPI_QKV) {
     const int d = ep.d;
     const int seg = n / d, c = n - seg * d;
@@ -98,6 +106,20 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int6
   }
   if (kind == EPI_RESID) {
     float* dst = ep.resid + m0 * N + n;
+    if (ep.x_out) {  // LN fold: the new residual also as the next GEMM's bf16 input; v <- new residual
+      __nv_bfloat16* xo = static_cast<__nv_bfloat16*>(ep.x_out) + m0 * N + n;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[j] = pre.a[j] + v[j];
+        if (j < jn) {
+          dst[j * N] = v[j];
+          xo[j * N] = __float2bfloat16_rn(v[j]);
+        } else {
+          v[j] = 0.f;
+        }
+      }
+      return;
+    }
     if (jn == 16) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) dst[j * N] = pre.a[j] + v[j];

@@ -46,6 +46,12 @@ struct Epilogue {
   void* out = nullptr;
   float* outf = nullptr;
   int64_t ldo = 0;
+  // LayerNorm folded into the neighbouring GEMMs (chain kernel, bf16):
+  //   EPI_RESID with x_out: also x_out[m][n] = bf16(new residual) (the next GEMM's raw input)
+  //   ln_wsum (consumer):   acc -> rstd[m] * (acc - mean[m] * ln_wsum[n]),  ln_wsum[n] = sum_k W[n][k]
+  //                         = LN(h) . W^T  (gamma 1, beta 0), row statistics passed per chunk
+  void* x_out = nullptr;
+  const float* ln_wsum = nullptr;
 };
 
 // ---- weights (PCG32 jump-ahead; bit-identical to the reference's fill_uniform) ----
@@ -62,6 +68,8 @@ void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table
            int d, float* h, cudaStream_t s);
 // out = LN(h) (gamma=1, beta=0, eps 1e-5), rows [row0, row0+n)
 void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s);
+// out[n] = sum_k W[n][k] of a row-major bf16 [N][K] matrix (fp32, LN-fold weight sums)
+void row_sums_bf16(const void* W, int N, int K, float* out, cudaStream_t s);
 // out[i] = LN(h[rows[i]]) for i < n (rows null: h row row_last for the single row)
 void layernorm_rows(int dtype, const float* h, const int32_t* rows, int64_t n, int d, void* out, cudaStream_t s,
                     int64_t row_last);
@@ -109,6 +117,12 @@ struct ChainStep {
   const float* ln_src = nullptr;  // LN: fp32 rows [M][ln_d]
   void* ln_dst = nullptr;         // LN: bf16 rows [M][ln_d]
   int ln_d = 0;
+  // folded LayerNorm (GEMM steps): a residual step (e.x_out set) writes {sum h, sum h^2} per
+  // (128-column tile, token) to stats_out [tiles][stats_ld][2]; a consumer step (e.ln_wsum
+  // set) reads stats_in rows [stats_row0, stats_row0 + M) of stats_tiles tiles, ln_dim wide
+  float* stats_out = nullptr;
+  const float* stats_in = nullptr;
+  int stats_tiles = 0, stats_ld = 0, stats_row0 = 0, ln_dim = 0;
 };
 bool chain_tc_supported(int64_t M, int N, int K);
 bool chain_ln_supported(int d);

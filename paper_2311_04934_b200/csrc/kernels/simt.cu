@@ -101,6 +101,20 @@ void init_uniform_block(int dtype, void* dst, int64_t rows, int64_t cols, uint64
   PCB_CUDA(cudaGetLastError());
 }
 
+// out[n] = sum_k W[n][k] (bf16 row-major; one warp per row, fp64 accumulation)
+__global__ void k_row_sums_bf16(const __nv_bfloat16* W, int N, int K, float* out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (row >= N) return;
+  double acc = 0;
+  for (int k = lane; k < K; k += 32) acc += static_cast<double>(__bfloat162float(W[static_cast<int64_t>(row) * K + k]));
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[row] = static_cast<float>(acc);
+}
+void row_sums_bf16(const void* W, int N, int K, float* out, cudaStream_t s) {
+  k_row_sums_bf16<<<(N + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(W), N, K, out);
+  PCB_CUDA(cudaGetLastError());
+}
+
 // h += part (tensor-parallel: the all-reduced partial sums of a row-parallel GEMM)
 __global__ void k_add_inplace(float* __restrict__ h, const float* __restrict__ part, int64_t n) {
   pdl_trigger();

@@ -32,7 +32,8 @@ def dump():
 
 VARIANTS = [
     ("per-GEMM kernels", {"chain": 0}),
-    ("chain", {"chain": 1}),
+    ("chain", {"chain": 1, "ln_fold": 1}),
+    ("chain, LN phases", {"chain": 1, "ln_fold": 0}),
 
 ]
 if os.environ.get("AB_VARIANTS"):
@@ -63,19 +64,20 @@ for name, v in res.items():
 
 # ---- chain timeline of one request ----
 m.set_option("chain", 1)
+m.set_option("ln_fold", int(os.environ.get("TL_FOLD", "1")))
 pcb.serve(st, s, parsed[0], max_new_tokens=1)
 m.sync()
 dump()
 pcb.serve(st, s, parsed[1], max_new_tokens=1)
 n = dump()
-names6 = ["O", "LN2", "W1", "W2", "LN1", "QKV"]
+names6 = ["O", "LN2", "W1", "W2", "LN1", "QKV"] if os.environ.get("TL_FOLD", "1") == "0" else ["O", "W1", "W2", "QKV"]
 print(f"chain launches {n}")
 agg = {}
 prev_end = None
 for i in range(n):
     npn = int(phases[i])
     t = times[i, :npn, :148].astype(np.int64)  # [ph][cta][ev]
-    names = ["LN1", "QKV"] if npn == 2 else names6[:npn]
+    names = ["LN1", "QKV"] if npn == 2 else (names6 + ["?"] * 8)[:npn]
     for ph in range(npn):
         ev = t[ph]
         done = ev[:, 2]
