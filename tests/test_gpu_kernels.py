@@ -90,3 +90,27 @@ def test_assembly_bytes_at_scale(m7):
     assert np.array_equal(cat.positions(), np.arange(start))
     want_k = np.concatenate([x[0].k() for x in kvs], axis=1)
     assert np.array_equal(cat.k(), want_k)
+
+
+def test_chain_and_ln_fold_full_depth():
+    """32-layer Llama-2-7B shape cached request: the persistent chain with LayerNorm folded
+    into its GEMMs vs the same chain with explicit LN phases vs one kernel per GEMM (the
+    fold rewrites LN(h)W^T as rstd (hW^T - mean sum_k W); depth must not amplify it)."""
+    cfg = dict(L7B, n_layers=32)
+    m = pcb.Model(cfg, dtype=pcb.BF16)
+    doc = "".join(chr(97 + (i * 11) % 26) for i in range(4096))
+    schema = pcb.Schema.parse(f'<schema name="deep"><module name="doc">{doc}</module></schema>')
+    store = pcb.ModuleStore(m)
+    store.encode_schema(schema)
+    prompt = '<prompt schema="deep"><doc/>' + ("Summarise the document above briefly " * 2)[:64] + '</prompt>'
+    out = {}
+    for name, opts in (("fold", {"chain": 1, "ln_fold": 1}), ("ln", {"chain": 1, "ln_fold": 0}),
+                       ("kernels", {"chain": 0})):
+        for k, v in opts.items():
+            m.set_option(k, v)
+        out[name] = pcb.serve(store, schema, prompt, 1).first_token_logits
+    m.set_option("chain", 1)
+    m.set_option("ln_fold", 1)
+    for other in ("ln", "kernels"):
+        assert rel(out["fold"], out[other]) <= BF16_REL
+        assert same_greedy_token(out["fold"], out[other])
