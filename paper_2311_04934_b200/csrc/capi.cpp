@@ -257,6 +257,10 @@ int pcb_debug_chain_probe(unsigned long long* times, int max_launches, int* n_ou
   return guard([&] { *n_out = kern::chain_probe_dump(times, max_launches, phases_out); });
 }
 
+int pcb_debug_attn_tl(unsigned long long* out, int max_ctas, int* n_out) {
+  return guard([&] { *n_out = kern::attn_tl_dump(out, max_ctas); });
+}
+
 int pcb_debug_kernel_bench(const char* which, int64_t a0, int64_t a1, int64_t a2, int iters, double* us_out) {
   return guard([&] {
     cudaStream_t s;

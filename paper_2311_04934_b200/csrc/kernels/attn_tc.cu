@@ -63,8 +63,17 @@ struct AttnParams {
   // {first q row, n, P}; K/V come from a 3-D tensor map {d, rows, request}
   const int4* req = nullptr;
   unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
+  unsigned long long* tl = nullptr;   // per-CTA phase timeline [cta][8] (PCB_ATTN_TL)
 };
 
+__device__ __forceinline__ void tlm(const AttnParams& p, int ev) {
+  if (p.tl) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    p.tl[cta * 8 + ev] = t;
+  }
+}
 __device__ __forceinline__ void probe(const AttnParams& p, int ev, int it) {
   if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && it < 64) {
     unsigned long long t;
@@ -113,6 +122,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) tlm(p, 0);  // entry
   const int h = blockIdx.y, split = blockIdx.z;
   int64_t n_ = p.n, P_ = p.P, qrow0 = 0;
   int breq = 0, q_tile = gridDim.x - 1 - blockIdx.x;  // heaviest tiles first
@@ -158,6 +168,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   // griddepcontrol.wait while the attention grid never completed -- tools/pdl_bisect2.sh,
   // test_cached_serve_equals_oracle_7b_shape), so dependents start at completion.
   pdl_wait();  // Q/K/V come from the QKV GEMM (and the assembly) just before
+  if (threadIdx.x == 0) tlm(p, 1);  // prologue done
 
   if (warp == 0) {
     if (elect_one() && nb > 0) {
@@ -195,6 +206,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       auto issue_qk = [&](int it) {
         const int s = it % KV_STAGES;
         mbar_wait(&kv_full[s], (it / KV_STAGES) & 1);
+        if (it == 0) tlm(p, 2);  // first K/V block landed
         probe(p, 5, it);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sKV + s * S::kStage);
@@ -225,6 +237,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         umma_commit(&kv_empty[it % KV_STAGES]);
         probe(p, 3, it);
       }
+      tlm(p, 3);  // last PV issued
     }
   } else {
     // ---- softmax warps: query row = TMEM lane ----
@@ -362,6 +375,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 64) tlm(p, 4);  // softmax / output done
   if (p.splits > 1) {
     // The split CTAs of one head form a thread-block cluster.  After every partial
     // is parked, CTA rank s merges query rows {s, s+S, s+2S, ...} of all S partials
@@ -375,31 +389,46 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t red0 = smem_u32(sKV);
       for (int64_t row = split + static_cast<int64_t>(t / kTpr) * p.splits; row < n_;
            row += static_cast<int64_t>(128 / kTpr) * p.splits) {
+        // every DSMEM load of a phase is issued before any is consumed (the merge was a
+        // chain of ~10 dependent cluster round trips: 6.7 us of a 26 us launch)
         float ms[8], ls[8];
-        float M = -INFINITY;
-        for (int s2 = 0; s2 < p.splits; ++s2) {
-          const uint32_t ml = mapa_shared(red0 + (BQ * kRedRow + 2 * static_cast<uint32_t>(row)) * 4, s2);
-          ms[s2] = ld_dsmem_f32(ml);
-          ls[s2] = ld_dsmem_f32(ml + 4);
-          if (ls[s2] > 0.f) M = fmaxf(M, ms[s2]);
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) {
+          ms[s2] = -INFINITY;
+          ls[s2] = 0.f;
+          if (s2 < p.splits) {
+            const uint32_t ml = mapa_shared(red0 + (BQ * kRedRow + 2 * static_cast<uint32_t>(row)) * 4, s2);
+            ms[s2] = ld_dsmem_f32(ml);
+            ls[s2] = ld_dsmem_f32(ml + 4);
+          }
         }
+        float M = -INFINITY;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2)
+          if (s2 < p.splits && ls[s2] > 0.f) M = fmaxf(M, ms[s2]);
         float den = 0.f, acc[kXs];
 #pragma unroll
         for (int x = 0; x < kXs; ++x) acc[x] = 0.f;
         const int x0 = (t % kTpr) * kXs;
-        for (int s2 = 0; s2 < p.splits; ++s2) {
-          if (!(ls[s2] > 0.f)) continue;
-          const float w = fast_exp2((ms[s2] - M) * p.scale_log2);
-          den += w * ls[s2];
-          const uint32_t src = mapa_shared(red0 + (static_cast<uint32_t>(row) * kRedRow + x0) * 4, s2);
 #pragma unroll
-          for (int x = 0; x < kXs; x += 4) {
-            float f[4];
-            ld_dsmem_v4(src + x * 4, f);
-            acc[x] += w * f[0];
-            acc[x + 1] += w * f[1];
-            acc[x + 2] += w * f[2];
-            acc[x + 3] += w * f[3];
+        for (int g = 0; g < 8; g += 4) {  // splits in groups of 4: 16 outstanding 16-byte loads
+          if (g >= p.splits) break;
+          float f[4][kXs];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (g + u < p.splits) {
+              const uint32_t src = mapa_shared(red0 + (static_cast<uint32_t>(row) * kRedRow + x0) * 4, g + u);
+#pragma unroll
+              for (int x = 0; x < kXs; x += 4) ld_dsmem_v4(src + x * 4, f[u] + x);
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int s2 = g + u;
+            if (s2 >= p.splits || !(ls[s2] > 0.f)) continue;
+            const float w = fast_exp2((ms[s2] - M) * p.scale_log2);
+            den += w * ls[s2];
+#pragma unroll
+            for (int x = 0; x < kXs; ++x) acc[x] += w * f[u][x];
           }
         }
         const float inv = 1.f / den;
@@ -416,6 +445,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     cluster_sync_all();  // peers are done reading this CTA's smem
   }
+  if (threadIdx.x == 0) tlm(p, 5);  // merge done
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, S::kTmemCols);
@@ -444,6 +474,9 @@ CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
   return m;
 }
+
+unsigned long long* g_tlbuf = nullptr;
+int g_tl_ctas = 0;
 
 template <int HD>
 void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s) {
@@ -498,6 +531,11 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), BQ);
   p.kv_head_major = std::getenv("PCB_ATTN_HM_PROBE") ? 1 : 0;  // timing probe (values meaningless)
   p.kv_rows = p.total;
+  if (std::getenv("PCB_ATTN_TL")) {  // per-CTA phase timeline of the LAST launch (attn_tl_dump)
+    if (!g_tlbuf) PCB_CUDA(cudaMalloc(&g_tlbuf, 8192 * 8 * sizeof(unsigned long long)));
+    p.tl = g_tlbuf;
+    g_tl_ctas = q_tiles * a.H * std::min(splits, 8);
+  }
   static unsigned long long* dbg = nullptr;
   const bool probe_on = std::getenv("PCB_ATTN_DBG") != nullptr;  // timeline probe of CTA 0 (debug)
   if (probe_on) {
@@ -538,6 +576,14 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
 }
 
 }  // namespace
+
+int attn_tl_dump(unsigned long long* out, int max_ctas) {
+  if (!g_tlbuf) return 0;
+  PCB_CUDA(cudaDeviceSynchronize());
+  const int n = std::min(g_tl_ctas, max_ctas);
+  PCB_CUDA(cudaMemcpy(out, g_tlbuf, static_cast<size_t>(n) * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return n;
+}
 
 bool attention_tc_supported(const AttnArgs& a) {
   return (a.hd == 128 || a.hd == 64) && !a.mask && !a.block_id && !a.alibi && a.n >= 1 && a.d % 64 == 0 &&

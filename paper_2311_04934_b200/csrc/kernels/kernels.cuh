@@ -161,6 +161,7 @@ void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s
 size_t attention_simt_scratch(const AttnArgs& a);
 bool attention_tc_supported(const AttnArgs& a);
 void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s);
+int attn_tl_dump(unsigned long long* out, int max_ctas);  // debug: last launch's per-CTA phases (PCB_ATTN_TL)
 
 // ---- KV assembly: batched contiguous copies (one descriptor per segment) ----
 struct CopySeg {
