@@ -86,7 +86,21 @@ struct AsmScratch {
   float* h_logits = nullptr;
   int64_t logit_cap = 0;
   cudaEvent_t ev[4] = {};
+  // slow tier: pinned-host module blocks stream in on a side stream, one event per layer,
+  // so the suffix prefill of layer l only waits for layer l's rows (engine.cpp:229-234)
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_start = nullptr;
+  std::vector<cudaEvent_t> layer_ev;
+  struct SlowCopy {
+    const model::KVBlock* src;
+    model::KVBlock* dst;
+    int64_t row;
+  };
+  std::vector<SlowCopy> slow;
   ~AsmScratch() {
+    for (auto& e : layer_ev) cudaEventDestroy(e);
+    if (side_start) cudaEventDestroy(side_start);
+    if (side) cudaStreamDestroy(side);
     if (h_segs) cudaFreeHost(h_segs);
     if (h_first) cudaFreeHost(h_first);
     if (d_segs) cudaFree(d_segs);
@@ -168,8 +182,7 @@ int append_segments(model::Model& m, const std::vector<cache::EntryPtr>& entries
     if (b.rows) {
       if (b.host) {
         ++slow;
-        CK(cudaMemcpy2DAsync(dst.plane(0, 0) + row * rb, dst.plane_bytes(), b.plane(0, 0), b.plane_bytes(),
-                             b.rows * rb, 2 * L, cudaMemcpyHostToDevice, m.stream()));
+        sc.slow.push_back({&b, &dst, row});  // issued layer by layer on the side stream
       } else if (rb % 16 == 0) {
         for (int l = 0; l < L; ++l)
           for (int w = 0; w < 2; ++w)
@@ -184,6 +197,35 @@ int append_segments(model::Model& m, const std::vector<cache::EntryPtr>& entries
   }
   dst.rows = row;
   return slow;
+}
+
+// Slow-tier rows: per layer, the K and V planes of every pinned-host block H2D on the
+// side stream, then that layer's event; the model waits for layer l right before its
+// attention (Model::set_layer_events), so the suffix GEMMs run under the upload.
+void launch_slow(model::Model& m, AsmScratch& sc) {
+  if (sc.slow.empty()) return;
+  const int L = m.config().n_layers;
+  if (!sc.side) {
+    CK(cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&sc.side_start, cudaEventDisableTiming));
+  }
+  while (static_cast<int>(sc.layer_ev.size()) < L) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sc.layer_ev.push_back(e);
+  }
+  CK(cudaEventRecord(sc.side_start, m.stream()));  // the destination cache is free
+  CK(cudaStreamWaitEvent(sc.side, sc.side_start, 0));
+  for (int l = 0; l < L; ++l) {
+    for (const auto& c : sc.slow) {
+      const size_t rb = c.dst->row_bytes();
+      CK(cudaMemcpy2DAsync(c.dst->plane(l, 0) + c.row * rb, c.dst->plane_bytes(), c.src->plane(l, 0),
+                           c.src->plane_bytes(), c.src->rows * rb, 2, cudaMemcpyHostToDevice, sc.side));
+    }
+    CK(cudaEventRecord(sc.layer_ev[l], sc.side));
+  }
+  m.set_layer_events(sc.layer_ev.data(), L);
+  sc.slow.clear();
 }
 
 // One assembly-kernel launch for every queued device segment.
@@ -206,6 +248,7 @@ int assemble(model::Model& m, const std::vector<cache::EntryPtr>& entries, model
   int n_segs = 0;
   const int slow = append_segments(m, entries, dst, sc, n_segs);
   launch_segments(m, sc, n_segs);
+  launch_slow(m, sc);
   return slow;
 }
 
@@ -336,6 +379,8 @@ model::KVPtr concat_kv(model::Model& m, const std::vector<cache::EntryPtr>& entr
   AsmScratch sc;
   assemble(m, entries, *out, sc);
   CK(cudaStreamSynchronize(m.stream()));
+  if (sc.side) CK(cudaStreamSynchronize(sc.side));  // slow-tier rows landed; no forward consumes the events
+  m.set_layer_events(nullptr, 0);
   return out;
 }
 
@@ -501,6 +546,7 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
                     static_cast<int64_t>(items[k].up.tokens.size()), &a});
     }
     launch_segments(m, sc, n_segs);
+    launch_slow(m, sc);
     CK(cudaEventRecord(sc.ev[1], m.stream()));
     m.run_batch(bi, true);
     const int B = static_cast<int>(items.size());

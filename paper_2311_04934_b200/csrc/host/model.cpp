@@ -773,7 +773,10 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       max_nb = std::max(max_nb, items[b].n);
     }
   }
+  std::vector<cudaEvent_t> layer_ev;
+  layer_ev.swap(layer_events_);  // consumed by this call
   auto attention = [&](int l) {
+    if (l < static_cast<int>(layer_ev.size())) CK(cudaStreamWaitEvent(s, layer_ev[l], 0));
     if (batched_attn) {
       kern::AttnArgs ab = aa;
       ab.n = n;

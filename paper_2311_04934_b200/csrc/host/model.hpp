@@ -122,6 +122,9 @@ class Model {
     KVBlock* kv;
   };
   void run_batch(const std::vector<BatchItem>& items, bool last_row_logits);
+  // The next run()/run_batch() waits for events[l] before layer l's attention (past K/V
+  // rows still streaming in, e.g. the pinned-host tier); consumed by that call.
+  void set_layer_events(const cudaEvent_t* events, int n) { layer_events_.assign(events, events + n); }
   const float* device_logits() const;  // [logit_rows][vocab] after run()
   int32_t* device_argmax() const;      // scratch int32 slots
   void argmax_last(int64_t logit_rows);  // device argmax of each logits row -> device_argmax()
@@ -165,6 +168,7 @@ class Model {
   int tp_rank_ = 0, tp_size_ = 1;
   int dl_ = 0, fl_ = 0, vl_ = 0;  // local attention width, MLP width, vocab rows
   std::shared_ptr<coll::Collective> comm_;
+  std::vector<cudaEvent_t> layer_events_;
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Weights> w_;
   std::unique_ptr<Workspace> ws_;
