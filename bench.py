@@ -562,6 +562,14 @@ def run_ours(a) -> None:
             full.append(r.timings["ttft_us"] / 1e3)
     full_ms = D.max(statistics.median(full))
 
+    # ---- decode after the cached prefill (reference finish_decode / generate): 32 greedy
+    # tokens, device argmax feeding the next step; time per output token
+    tpot = []
+    for i in range(2):
+        r = pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=33)
+        tpot.append(r.timings["decode_us_per_token"] / 1e3)
+    decode_tpot_ms = D.max(min(tpot))
+
     # ---- slow tier (modules in pinned host memory, H2D per request)
     slow = None
     if not a.skip_slow:
@@ -599,7 +607,7 @@ def run_ours(a) -> None:
                        "l2": "inputs larger than L2 (12.9 GB weights + 2.1 GB KV per step)"},
             "ttft_ms": ttft_mean, "full_prefill_ttft_ms": full_ms, "ttft_speedup_vs_full_prefill": full_ms / ttft_mean,
             "device_ms_per_request": dev_ms / a.steps, "ttft_slow_tier_ms": slow,
-            "precompute_ms": precompute_ms,
+            "precompute_ms": precompute_ms, "decode_tpot_ms": decode_tpot_ms,
             "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "k_chain (persistent tcgen05 GEMM/LayerNorm chains: every GEMM "
