@@ -384,16 +384,54 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           tc_fence_after();
           if (et == 0) ctl(p, ph, 4);
           if (P.S == 1) {
+            // bf16 outputs (QKV, GELU) of <= 64 tokens: stage the 128 x Mc tile in shared
+            // memory (the LN-fold scratch, idle in these phases) and store whole 256-byte
+            // token rows -- 8 16-byte stores per thread instead of 64 scattered 2-byte ones
+            const bool tstore = (e.kind == EPI_QKV || e.kind == EPI_GELU) && Mc <= 64 && !P.stats_out;
+            __nv_bfloat16* T = reinterpret_cast<__nv_bfloat16*>(colsum);  // [64 tokens][128 rows]
 #pragma unroll 1
             for (int cc = 0; cc < Mc; cc += 16) {
               if (cc + 16 < Mc) epi_prefetch(e, n, P.N, cc + 16, M, nxt);
               tmem_ld16(acc + cc, v);
-              epi_chunk(e, n, P.N, cc, M, v, cur, ln);
-              if (P.stats_out) stats_chunk(tile, cc, M);
+              if (tstore) {
+                epi_values(e, n, cc, M, v, cur, ln);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) T[(cc + j) * 128 + row] = __float2bfloat16_rn(v[j]);
+              } else {
+                epi_chunk(e, n, P.N, cc, M, v, cur, ln);
+                if (P.stats_out) stats_chunk(tile, cc, M);
+              }
               cur = nxt;
             }
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
+            if (tstore) {
+              named_bar(1, 128);
+              __nv_bfloat16* base;
+              int64_t ld;
+              const int64_t* off = nullptr;
+              if (e.kind == EPI_GELU) {
+                base = static_cast<__nv_bfloat16*>(e.out) + static_cast<int64_t>(tile) * 128;
+                ld = P.N;
+              } else {
+                const int seg = (tile * 128) / e.d, c0 = tile * 128 - seg * e.d;
+                ld = e.d;
+                if (seg == 0) {
+                  base = static_cast<__nv_bfloat16*>(e.q_out) + c0;
+                } else {
+                  base = static_cast<__nv_bfloat16*>(seg == 1 ? e.k_out : e.v_out) + c0;
+                  if (e.kv_off) off = e.kv_off;
+                  else base += e.kv_row0 * e.d;
+                }
+              }
+              for (int i = et; i < Mc * 16; i += 128) {
+                const int m = i >> 4, q16 = i & 15;
+                const uint4 val = *reinterpret_cast<const uint4*>(T + m * 128 + q16 * 8);
+                __nv_bfloat16* dst = off ? base + off[m] + q16 * 8 : base + m * ld + q16 * 8;
+                *reinterpret_cast<uint4*>(dst) = val;
+              }
+              named_bar(1, 128);  // T is reused by this CTA's next item
+            }
             if (et == 0) ctl(p, ph, 5);
             continue;
           }

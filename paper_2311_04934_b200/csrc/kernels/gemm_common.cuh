@@ -147,6 +147,36 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int6
   }
 }
 
+// The value part of epi_chunk for the bf16-output kinds (QKV, GELU): folded-LN
+// correction, RoPE (partner column in lane^1) or GELU applied in place, no stores -- for
+// epilogues that stage the tile in shared memory and store whole rows.
+__device__ __forceinline__ void epi_values(const Epilogue& ep, int n, int64_t m0, int64_t M, float* v,
+                                           const EpiPre& pre, const float2* lnst) {
+  const int jn = M - m0 >= 16 ? 16 : static_cast<int>(M - m0);
+  if (lnst) {
+    const float ws = ep.ln_wsum[n];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float2 st = lnst[j < jn ? m0 + j : m0];
+      v[j] = st.y * fmaf(-st.x, ws, v[j]);
+    }
+  }
+  if (ep.kind == EPI_QKV) {
+    const int d = ep.d;
+    const int seg = n / d, c = n - seg * d;
+    const bool rot = seg < 2 && ep.rope;
+    const bool odd = c & 1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float pv = __shfl_xor_sync(0xffffffffu, v[j], 1);
+      if (rot) v[j] = odd ? fmaf(pv, pre.b[j], v[j] * pre.a[j]) : fmaf(v[j], pre.a[j], -pv * pre.b[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = gelu_bf16path(v[j]);
+  }
+}
+
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
