@@ -11,7 +11,8 @@ cached serve request through to the first token.
                resolve, H2D of tokens/positions, D2H of first-token logits + token, host-clock timed
   ttft_ms      mean cached TTFT (host clock, request receipt -> first token on host)
   full_prefill_ttft_ms  same prompt with use_cache=False (4160-token prefill on the GPU)
-  roofline     dominant kernel class (GEMM weight streaming, HBM-bound at 64 tokens), CUDA events
+  roofline     dominant kernel class (the persistent chains: attention + weight-streaming GEMMs,
+               HBM-bound at 64 tokens), CUDA events
   cpu_baseline reference C++ (oracle/_ref, unmodified) on this host, bounded sample, extrapolated
 
 ``--impl reference`` times the reference's own CPU implementation (oracle/_ref) instead.
@@ -540,7 +541,7 @@ def run_ours(a) -> None:
     gemm_ms_step = g["ms"] / a.steps
     gemm_bytes_step = g["bytes"] / a.steps
     achieved = gemm_bytes_step / (gemm_ms_step / 1e3) / 1e9
-    # DRAM traffic of the same GEMM launches from the committed ncu capture (profiles/)
+    # DRAM traffic of the same chain launches from the committed ncu capture (profiles/)
     traffic, traffic_src = None, None
     import glob
     tr = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), key=os.path.getmtime)
@@ -610,10 +611,11 @@ def run_ours(a) -> None:
             "precompute_ms": precompute_ms, "decode_tpot_ms": decode_tpot_ms,
             "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "k_chain (persistent tcgen05 GEMM/LayerNorm chains: every GEMM "
-                                                   "of a step, swap-AB weight streaming)",
+            "roofline": {"bound": "hbm", "kernel": "k_chain (persistent tcgen05 chains: every GEMM of a step "
+                                                   "(swap-AB weight streaming) and, as each chain's first phase, "
+                                                   "the layer's attention over the assembled cache)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": traffic, "traffic_unit": "bytes per step (all GEMM launches)",
+                         "traffic": traffic, "traffic_unit": "bytes per step (all chain launches)",
                          "traffic_source": traffic_src, "peak_source": peak_src,
                          "alg_bytes_per_step": gemm_bytes_step, "gemm_ms_per_step": gemm_ms_step,
                          "tensor_peak_tflops": tc_peak},

@@ -185,6 +185,7 @@ int pcb_model_set_option(pcb_model* m, const char* key, int64_t v) {
     else if (std::strcmp(key, "profile") == 0) m->m->set_profiling(v != 0);
     else if (std::strcmp(key, "chain") == 0) m->m->use_chain = v != 0;
     else if (std::strcmp(key, "ln_fold") == 0) m->m->ln_fold = v != 0;
+    else if (std::strcmp(key, "chain_attn") == 0) m->m->chain_attn = v != 0;
     else throw Error(ErrorCode::InvalidConfig, std::string("unknown option ") + key);
   });
 }

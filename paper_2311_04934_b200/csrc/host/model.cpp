@@ -273,6 +273,7 @@ Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_si
   vl_ = c.vocab_size / tp_size;
   if (const char* v = std::getenv("PCB_CHAIN")) use_chain = v[0] != '0';
   if (const char* v = std::getenv("PCB_LN_FOLD")) ln_fold = v[0] != '0';
+  if (const char* v = std::getenv("PCB_CHAIN_ATTN")) chain_attn = v[0] != '0';
   if (c.hidden != c.n_heads * c.head_dim) throw Error(ErrorCode::InvalidConfig, "hidden must equal n_heads * head_dim");
   if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 2 || c.head_dim % 2 != 0)
     throw Error(ErrorCode::InvalidConfig, "bad layer/head geometry");
@@ -556,6 +557,9 @@ void Model::chain(const void* steps_v, int n_steps) {
     if (st.kind == kern::CHAIN_GEMM) {
       bytes += gemm_alg_bytes(dtype_, st.M, st.N, st.K, st.e.kind);
       flops += 2.0 * st.M * st.N * st.K;
+    } else if (st.kind == kern::CHAIN_ATTN) {
+      bytes += 2.0 * (st.aP + st.M) * st.a_d * 2 + 2.0 * st.M * st.a_d * 2;
+      flops += 4.0 * st.M * st.a_d * (st.aP + (st.M + 1) / 2.0);
     } else {
       bytes += 6.0 * st.M * st.ln_d;
     }
@@ -883,13 +887,34 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       st.e = e;
       return st;
     };
+    // one request's attention joins the chain as its first phase (no launch, no prologue,
+    // the next weights stream in as soon as each CTA's softmax is done)
+    const bool fuse_attn = chain_attn && B == 1 && tc_attn && hd == 128 && !mask && !block_ids && !alibi &&
+                           kern::chain_attn_supported(n, P, H, hd);
     kern::ChainStep steps[8];
     steps[0] = ln(W.h, n);
     steps[1] = mm(W.x, w_->wqkv[0], n, 3 * d, d, qkv_epi(0));
     chain(steps, 2);
     for (int l = 0; l < c.n_layers; ++l) {
-      attention(l);
       int k = 0;
+      if (fuse_attn) {
+        if (l < static_cast<int>(layer_ev.size())) CK(cudaStreamWaitEvent(s, layer_ev[l], 0));
+        kern::ChainStep st;
+        st.kind = kern::CHAIN_ATTN;
+        st.M = n;
+        st.aq = W.q;
+        st.ak = kv.k(l);
+        st.av = kv.v(l);
+        st.aout = W.attn;
+        st.aP = P;
+        st.aH = H;
+        st.a_d = d;
+        st.a_scratch = W.attn_scratch;
+        st.a_scratch_bytes = W.attn_scratch_bytes;
+        steps[k++] = st;
+      } else {
+        attention(l);
+      }
       if (ln_fold && d % 128 == 0) {
         // LayerNorm folded into the GEMMs around it (no LN phases, two fewer grid
         // barriers per layer): the residual phases (Wo, W2) also write bf16(h) and

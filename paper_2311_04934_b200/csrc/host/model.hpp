@@ -154,6 +154,7 @@ class Model {
   bool force_simt_attn = false;  // testing: SIMT attention only
   bool use_chain = true;         // few-token GEMM/LN segments as one persistent chain kernel (PCB_CHAIN=0: off)
   bool ln_fold = true;           // chain: LayerNorm folded into the neighbouring GEMMs (PCB_LN_FOLD=0: off)
+  bool chain_attn = true;        // chain: a single request's attention as the chain's first phase (PCB_CHAIN_ATTN=0: off)
   int64_t launches = 0;          // kernels launched by run() (bench evidence)
 
  private:

@@ -1,10 +1,15 @@
 // Persistent chain of weight-streaming GEMM and LayerNorm phases for the few-token
 // (suffix prefill / decode) regime, one launch per transformer-layer segment:
 //
-//   [O_l (+resid), LN2_l, W1_l (+GELU), W2_l (+resid), LN1_{l+1}, QKV_{l+1} (+RoPE, K/V -> cache)]
+//   [attention_l, O_l (+resid), LN2_l, W1_l (+GELU), W2_l (+resid), LN1_{l+1}, QKV_{l+1} (+RoPE, K/V -> cache)]
 //
-// (reference Model::run, model.cpp:376-436; attention stays its own kernel between
-// two chains).  At 64 tokens every GEMM is HBM-bound on its weights, and as separate
+// (reference Model::run, model.cpp:376-436).  The attention phase (one request, hd 128)
+// runs the attn_tc.cu pipeline on the ring's shared memory -- TMA Q and K/V blocks, QK^T
+// and PV on tcgen05 with S / O in TMEM, online softmax on the epilogue warps -- over
+// (head, key split) items, and merges the split partials through global memory; each
+// CTA hands the ring back to the weight stream as soon as its own item is done.  (As a
+// separate kernel it cost a launch, a prologue and the next chain's cold start per layer.)
+// At 64 tokens every GEMM is HBM-bound on its weights, and as separate
 // launches each one paid a ramp (launch, prologue, first weight bytes) and a drain
 // (stream-K fix-up, epilogue, the slowest CTA) during which HBM idles: the measured
 // per-layer time was ~2.6x the weight-streaming time (tools/gemm_timeline.py).
@@ -63,10 +68,17 @@ struct PhaseDev {
   __nv_bfloat16* ln_dst;
   int ln_d;
   Epilogue e;
+  // attention phase: item = (head, key split); partials [items][128][128] then (m, l) [items][128]
+  int64_t aP;
+  int aH, aS, a_d;
+  float ascale;  // log2(e) / sqrt(128)
+  float* apart;
+  __nv_bfloat16* aout;
 };
 
 struct ChainParams {
   CUtensorMap tm[kMaxPhases];  // activation maps of the GEMM phases
+  CUtensorMap tma[3];          // attention phase: Q [n][d], K and V planes [P + n][d]
   PhaseDev ph[kMaxPhases];
   int n_phases;
   int epoch0;
@@ -94,7 +106,30 @@ struct ChainSmem {
   static constexpr int kStage = kWTileC + BN * 128;
   static constexpr int kBytes = STAGES * kStage + 1024 + 1024 + 1024 + 2 * 16 * 128 * 4;  // + LN-fold scratch
   static constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;
+  // attention phase layout of the ring: Q (32 KB), two P buffers (32 KB), K/V stages of 32 KB
+  static constexpr int kAttnFit = (STAGES * kStage - 65536) / 32768;
+  static constexpr int kAttnKV = kAttnFit > 4 ? 4 : kAttnFit;  // 2 stages: +4.7 us per layer
+  static_assert(kAttnKV >= 2, "attention phase needs two K/V stages in the ring");
 };
+
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain: stale max tolerated up to 2^8 (as attn_tc.cu)
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -186,6 +221,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x, c = blockIdx.x;
+  // attention phase (first phase only): the ring's shared memory is re-carved as Q, P and
+  // K/V stages; its barriers sit 512 bytes into the barrier block; S and O live in TMEM
+  // columns [256, 512), clear of the GEMM accumulators
+  const bool has_attn = p.ph[0].kind == CHAIN_ATTN;
+  constexpr int AKV = S::kAttnKV;
+  uint8_t* aQ = smem;
+  uint8_t* aPb = smem + 32768;
+  uint8_t* aKV = smem + 65536;
+  uint64_t* a_qfull = full + 64;
+  uint64_t* a_kvfull = a_qfull + 1;    // [AKV]
+  uint64_t* a_kvempty = a_kvfull + 4;  // [AKV]
+  uint64_t* a_sfull = a_kvempty + 4;   // [2]
+  uint64_t* a_pfull = a_sfull + 2;
+  uint64_t* a_pvdone = a_pfull + 1;    // [2]
+  uint64_t* a_done = a_pvdone + 2;     // this CTA's attention is off the ring (128 arrivals)
+  const uint32_t tcols = has_attn ? 512u : S::kCols;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -196,16 +247,39 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 128);
     }
+    if (has_attn) {
+      mbar_init(a_qfull, 1);
+      for (int s = 0; s < AKV; ++s) {
+        mbar_init(&a_kvfull[s], 1);
+        mbar_init(&a_kvempty[s], 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&a_sfull[b], 1);
+        mbar_init(&a_pvdone[b], 1);
+      }
+      mbar_init(a_pfull, 128);
+      mbar_init(a_done, 128);
+    }
     fence_barrier_init();
   }
   if (warp == 2 && lane == 0)
     for (int ph = 0; ph < p.n_phases; ++ph)
       if (p.ph[ph].kind == CHAIN_GEMM) tma_prefetch(&p.tm[ph]);
-  if (warp == 1) tmem_alloc(tmem_slot, S::kCols);
+  if (warp == 1) tmem_alloc(tmem_slot, tcols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t aS0 = tmem + 256, aO = tmem + 384;  // attention: two score buffers, O
+
+  // attention item of this CTA: head h, key split sp -> key blocks [b0, b0 + nb) of 64
+  auto attn_range = [&](const PhaseDev& A, int& h, int& sp, int& b0, int& nb) {
+    h = c / A.aS;
+    sp = c - h * A.aS;
+    const int64_t nblk = (A.aP + A.M + 63) / 64;
+    b0 = static_cast<int>(nblk * sp / A.aS);
+    nb = static_cast<int>(nblk * (sp + 1) / A.aS) - b0;
+  };
 
   // Work items of a GEMM phase: item i = (tile i / S, k-split i % S) with k-blocks
   // [j kbs / S, (j+1) kbs / S); CTA c takes items c, c + C, ...  S = 1 (tiles >= C/2):
@@ -221,6 +295,34 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   if (warp == 0) {
     // ---- W producer: never waits for a phase boundary ----
     if (elect_one()) {
+      if (has_attn) {
+        // attention loads first (Q once, then the K/V blocks of this CTA's split); the
+        // weight stream resumes once this CTA's attention no longer uses the ring
+        const PhaseDev& A = p.ph[0];
+        if (c < A.items) {
+          int h, sp, b0, nb;
+          attn_range(A, h, sp, b0, nb);
+          tma_prefetch(&p.tma[0]);
+          tma_prefetch(&p.tma[1]);
+          tma_prefetch(&p.tma[2]);
+          pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
+          mbar_expect_tx(a_qfull, 32768);
+          for (int a = 0; a < 2; ++a) tma_load_2d(aQ + a * 16384, &p.tma[0], a_qfull, h * 128 + a * 64, 0);
+          for (int it = 0; it < nb; ++it) {
+            const int s = it % AKV;
+            mbar_wait(&a_kvempty[s], ((it / AKV) & 1) ^ 1);
+            uint8_t* st = aKV + s * 32768;
+            const int j0 = (b0 + it) * 64;
+            mbar_expect_tx(&a_kvfull[s], 32768);
+            for (int a = 0; a < 2; ++a) {
+              tma_load_2d(st + a * 8192, &p.tma[1], &a_kvfull[s], h * 128 + a * 64, j0);
+              tma_load_2d(st + 16384 + a * 8192, &p.tma[2], &a_kvfull[s], h * 128 + a * 64, j0);
+            }
+          }
+        }
+        mbar_wait(a_done, 0);
+        ctl(p, 0, 3);
+      }
       const uint64_t pol_w = policy_evict_first();
       int it = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
@@ -269,6 +371,42 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   } else if (warp == 1) {
     // ---- MMA issuer: one accumulator per item ----
     if (elect_one()) {
+      if (has_attn && c < p.ph[0].items) {
+        // S_j = Q K_j^T (M=128, N=64, K=128) into one of two score buffers while the
+        // softmax of block j-1 runs; O += P_j V_j (V MN-major) accumulated in TMEM
+        int h, sp, b0, nb;
+        attn_range(p.ph[0], h, sp, b0, nb);
+        constexpr uint32_t idS = idesc_bf16(128, 64);
+        constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
+        const uint32_t q_addr = smem_u32(aQ), p_addr = smem_u32(aPb);
+        mbar_wait(a_qfull, 0);
+        auto issue_qk = [&](int it) {
+          const int s = it % AKV;
+          mbar_wait(&a_kvfull[s], (it / AKV) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(aKV + s * 32768);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_bf16(aS0 + (it & 1) * 64, sw128_kmajor_desc(q_addr + (k >> 2) * 16384 + (k & 3) * 32),
+                      sw128_kmajor_desc(k_addr + (k >> 2) * 8192 + (k & 3) * 32), idS, k > 0 ? 1u : 0u);
+          umma_commit(&a_sfull[it & 1]);
+        };
+        issue_qk(0);
+        for (int it = 0; it < nb; ++it) {
+          if (it + 1 < nb) issue_qk(it + 1);
+          mbar_wait(a_pfull, it & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(aKV + (it % AKV) * 32768 + 16384);
+          const uint32_t pb = p_addr + (it & 1) * 16384;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(aO, sw128_kmajor_desc(pb + k * 32), sw128_mnmajor_desc(v_addr + k * 2048, 8192, 1024), idO,
+                      (it > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&a_pvdone[it & 1]);
+          umma_commit(&a_kvempty[it % AKV]);
+        }
+        ctl(p, 0, 1);
+      }
       constexpr uint32_t idesc = idesc_bf16(128, BN);
       int it = 0, seg = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
@@ -316,6 +454,204 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
       }
       if (P.kind == CHAIN_LN) {
         for (int64_t r = c; r < P.M; r += C) ln_row(P, r, red, et);
+      } else if (P.kind == CHAIN_ATTN) {
+        // ---- softmax: query row = TMEM lane (reference model.cpp:401-427, causal by
+        // sequence order: query i sees keys j <= P + i) ----
+        const int epoch = p.epoch0 + ph;
+        int h = 0, sp = 0, b0 = 0, nb = 0;
+        if (c < P.items) attn_range(P, h, sp, b0, nb);
+        const int64_t n_ = P.M;
+        const int64_t limit = P.aP + row;
+        float m = -INFINITY, l = 0.f;
+        const bool live = q * 32 < n_;  // a warp whose rows are all past n keeps the protocol only
+        if (et == 0) ctl(p, ph, 0);
+        for (int it = 0; it < nb; ++it) {
+          const int64_t j0 = static_cast<int64_t>(b0 + it) * 64;
+          if (!live) {
+            if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
+            mbar_arrive(a_pfull);
+            continue;
+          }
+          mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
+          tc_fence_after();
+          float sv[64];
+          {
+            uint32_t raw[64];
+#pragma unroll
+            for (int x = 0; x < 64; x += 16) tmem_ld16_nowait(aS0 + (it & 1) * 64 + lane_off + x, raw + x);
+            tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 64; ++x) sv[x] = __uint_as_float(raw[x]);
+          }
+          if (j0 + 63 > limit) {
+#pragma unroll
+            for (int x = 0; x < 64; ++x)
+              if (j0 + x > limit) sv[x] = -INFINITY;
+          }
+          float mx[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) mx[x] = sv[x];
+#pragma unroll
+          for (int x = 8; x < 64; ++x) mx[x & 7] = fmaxf(mx[x & 7], sv[x]);
+#pragma unroll
+          for (int w = 4; w; w >>= 1)
+#pragma unroll
+            for (int x = 0; x < w; ++x) mx[x] = fmaxf(mx[x], mx[x + w]);
+          const float bm = mx[0];
+          const bool grow = bm > m + kRescaleThreshold / P.ascale || (m == -INFINITY && bm > -INFINITY);
+          if (__any_sync(0xffffffffu, grow) && it > 0) {
+            mbar_wait(&a_pvdone[(it - 1) & 1], ((it - 1) >> 1) & 1);
+            tc_fence_after();
+            const float f = grow ? fast_exp2((m - bm) * P.ascale) : 1.f;
+#pragma unroll 1
+            for (int x = 0; x < 128; x += 16) {
+              float ov[16];
+              tmem_ld16(aO + lane_off + x, ov);
+#pragma unroll
+              for (int y = 0; y < 16; ++y) ov[y] *= f;
+              tmem_st16(aO + lane_off + x, ov);
+            }
+            tmem_st_wait();
+          }
+          if (grow) {
+            l *= fast_exp2((m - bm) * P.ascale);
+            m = bm;
+          }
+          const float mb = (m == -INFINITY) ? 0.f : m * P.ascale;
+          float bs[4] = {0.f, 0.f, 0.f, 0.f};
+          uint32_t packed[32];
+#pragma unroll
+          for (int x = 0; x < 64; x += 2) {
+            const float p0 = fast_exp2(fmaf(sv[x], P.ascale, -mb));
+            const float p1 = fast_exp2(fmaf(sv[x + 1], P.ascale, -mb));
+            bs[(x >> 1) & 3] += p0 + p1;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            packed[x >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
+          if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);  // P buffer free
+          uint8_t* prow = aPb + (it & 1) * 16384 + row * 128;
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            uint4 v4 = make_uint4(packed[4 * x], packed[4 * x + 1], packed[4 * x + 2], packed[4 * x + 3]);
+            *reinterpret_cast<uint4*>(prow + ((x ^ (row & 7)) << 4)) = v4;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_fence_before();
+          if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
+          mbar_arrive(a_pfull);
+        }
+        float* part = P.apart + (static_cast<int64_t>(c) * 128 + row) * 128;
+        float2* ml = reinterpret_cast<float2*>(P.apart + static_cast<int64_t>(P.items) * 128 * 128);
+        if (nb > 0) {
+          mbar_wait(&a_pvdone[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+          tc_fence_after();
+          if (P.aS == 1) {
+            const float inv = 1.f / l;
+            __nv_bfloat16* dst = P.aout + row * P.a_d + h * 128;
+#pragma unroll 1
+            for (int x = 0; x < 128; x += 16) {
+              float ov[16];
+              tmem_ld16(aO + lane_off + x, ov);
+              if (row < n_) {
+                uint4 w2[2];
+                __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w2);
+#pragma unroll
+                for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
+                *reinterpret_cast<uint4*>(dst + x) = w2[0];
+                *reinterpret_cast<uint4*>(dst + x + 8) = w2[1];
+              }
+            }
+          } else {
+            // park the unnormalised O row and (m, l) for the split merge
+#pragma unroll 1
+            for (int x = 0; x < 128; x += 16) {
+              float ov[16];
+              tmem_ld16(aO + lane_off + x, ov);
+              if (row < n_)
+#pragma unroll
+                for (int y = 0; y < 16; y += 4)
+                  __stcg(reinterpret_cast<float4*>(part + x + y), make_float4(ov[y], ov[y + 1], ov[y + 2], ov[y + 3]));
+            }
+            if (row < n_) __stcg(ml + static_cast<int64_t>(c) * 128 + row, make_float2(m, l));
+          }
+        }
+        tc_fence_before();
+        if (et == 0) ctl(p, ph, 4);
+        // a_done releases the W producer onto the ring (the next phase's weights).  A split
+        // CTA publishes its partial first: with the weight prefetch already in flight its
+        // flag became visible ~2 us later (tools/chain_ab.py, per-CTA attention events)
+        if (!(c < P.items && P.aS > 1)) mbar_arrive(a_done);
+        if (c < P.items && P.aS > 1) {
+          // the S split CTAs of head h each merge query rows {sp, sp + S, ...} of all S
+          // partials in split order (deterministic):
+          //   O = sum_s w_s O_s / sum_s w_s l_s,  w_s = 2^((m_s - M) scale),  M = max_s m_s
+          named_bar(1, 128);
+          if (et == 0) st_release(p.flags + c, epoch);
+          mbar_arrive(a_done);
+          const int base = h * P.aS;
+          if (et < P.aS)
+            for (uint32_t spins = 0; ld_relaxed(p.flags + base + et) < epoch;) {
+              __nanosleep(32);
+              if (++spins == (1u << 25)) wait_timeout("chain attention split flag", p.flags + base + et, epoch);
+            }
+          fence_acquire_gpu();
+          named_bar(1, 128);
+          if (et == 0) ctl(p, ph, 5);
+          const int x0 = (et & 7) * 16;
+          for (int64_t r2 = sp + static_cast<int64_t>(et >> 3) * P.aS; r2 < n_; r2 += 16 * P.aS) {
+            float ms[8], ls[8];
+#pragma unroll
+            for (int s2 = 0; s2 < 8; ++s2) {
+              float2 v2 = make_float2(-INFINITY, 0.f);
+              if (s2 < P.aS) v2 = __ldcg(ml + static_cast<int64_t>(base + s2) * 128 + r2);
+              ms[s2] = v2.x;
+              ls[s2] = v2.y;
+            }
+            float M = -INFINITY;
+#pragma unroll
+            for (int s2 = 0; s2 < 8; ++s2)
+              if (s2 < P.aS && ls[s2] > 0.f) M = fmaxf(M, ms[s2]);
+            float den = 0.f, acc[16];
+#pragma unroll
+            for (int x = 0; x < 16; ++x) acc[x] = 0.f;
+#pragma unroll
+            for (int g = 0; g < 8; g += 4) {
+              if (g >= P.aS) break;
+              float4 f[4][4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (g + u < P.aS) {
+                  const float4* src =
+                      reinterpret_cast<const float4*>(P.apart + (static_cast<int64_t>(base + g + u) * 128 + r2) * 128 + x0);
+#pragma unroll
+                  for (int x = 0; x < 4; ++x) f[u][x] = __ldcg(src + x);
+                }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int s2 = g + u;
+                if (s2 >= P.aS || !(ls[s2] > 0.f)) continue;
+                const float w = fast_exp2((ms[s2] - M) * P.ascale);
+                den += w * ls[s2];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                  acc[4 * x] += w * f[u][x].x;
+                  acc[4 * x + 1] += w * f[u][x].y;
+                  acc[4 * x + 2] += w * f[u][x].z;
+                  acc[4 * x + 3] += w * f[u][x].w;
+                }
+              }
+            }
+            const float inv = 1.f / den;
+            __nv_bfloat16* dst = P.aout + r2 * P.a_d + h * 128 + x0;
+            uint4 w2[2];
+            __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w2);
+#pragma unroll
+            for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(acc[2 * y] * inv, acc[2 * y + 1] * inv);
+            *reinterpret_cast<uint4*>(dst) = w2[0];
+            *reinterpret_cast<uint4*>(dst + 8) = w2[1];
+          }
+        }
       } else {
         const Epilogue& e = P.e;
         const int64_t M = P.M;
@@ -519,7 +855,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, S::kCols);
+  if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
 std::atomic<int> g_chain_epoch{0};
@@ -577,6 +913,22 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.stats_row0 = st.stats_row0;
       d.ln_dim = st.ln_dim;
       p.tm[i] = tmap_bf16_2d(st.x, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.K), BN);
+    } else if (st.kind == CHAIN_ATTN) {
+      if (i != 0) throw std::runtime_error("chain: attention must be the first phase");
+      d.aP = st.aP;
+      d.aH = st.aH;
+      d.a_d = st.a_d;
+      const int64_t nblk = (st.aP + st.M + 63) / 64;
+      d.aS = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({C / st.aH, nblk, 8})));
+      d.items = st.aH * d.aS;
+      d.ascale = 1.4426950408889634f / sqrtf(128.f);
+      d.apart = st.a_scratch;
+      d.aout = static_cast<__nv_bfloat16*>(st.aout);
+      if (static_cast<size_t>(d.items) * 128 * 130 * sizeof(float) > st.a_scratch_bytes)
+        throw std::runtime_error("chain: attention scratch too small");
+      p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 128);
+      p.tma[1] = tmap_bf16_2d(st.ak, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
+      p.tma[2] = tmap_bf16_2d(st.av, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
     } else {
       d.ln_src = st.ln_src;
       d.ln_dst = static_cast<__nv_bfloat16*>(st.ln_dst);
@@ -600,6 +952,12 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
 
 bool chain_tc_supported(int64_t M, int N, int K) { return M >= 1 && M <= 128 && weight_packable(N, K); }
 bool chain_ln_supported(int d) { return d % 4 == 0 && d <= 8192; }
+bool chain_attn_supported(int64_t n, int64_t P, int H, int hd) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return hd == 128 && n >= 1 && n <= 128 && H >= 1 && H <= sms && P >= 0 && P + n < (1LL << 31);
+}
 
 int chain_probe_dump(unsigned long long* times, int max_launches, int* phases) {
   PCB_CUDA(cudaDeviceSynchronize());
@@ -628,6 +986,8 @@ void chain_tc(const ChainStep* steps, int n_steps, float* ws, size_t ws_bytes, i
     if (st.kind == CHAIN_GEMM && !chain_tc_supported(st.M, st.N, st.K))
       throw std::runtime_error("chain: unsupported GEMM shape");
     if (st.kind == CHAIN_LN && !chain_ln_supported(st.ln_d)) throw std::runtime_error("chain: unsupported LN width");
+    if (st.kind == CHAIN_ATTN && (i != 0 || !chain_attn_supported(st.M, st.aP, st.aH, st.a_d / std::max(1, st.aH))))
+      throw std::runtime_error("chain: unsupported attention phase");
     M = std::max<int64_t>(M, st.M);
   }
   if (M <= 16) launch_chain<16, 10>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);

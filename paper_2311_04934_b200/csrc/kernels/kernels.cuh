@@ -106,7 +106,7 @@ void gemm_tc(const void* A, const void* W_packed, int64_t M, int N, int K, const
 // ---- persistent GEMM / LayerNorm chain (few-token regime, M <= 128) ----
 // One launch runs the phases in order with a grid barrier between them; the packed
 // weights of later phases stream in while earlier phases finish (chain_tc.cu).
-enum ChainKind : int { CHAIN_GEMM = 0, CHAIN_LN = 1 };
+enum ChainKind : int { CHAIN_GEMM = 0, CHAIN_LN = 1, CHAIN_ATTN = 2 };
 struct ChainStep {
   int kind = CHAIN_GEMM;
   int64_t M = 0;             // rows (tokens)
@@ -123,7 +123,20 @@ struct ChainStep {
   float* stats_out = nullptr;
   const float* stats_in = nullptr;
   int stats_tiles = 0, stats_ld = 0, stats_row0 = 0, ln_dim = 0;
+  // attention phase (CHAIN_ATTN; only as the first phase of a chain): M = n <= 128 new rows
+  // of one request, causal against P cached rows; q / out [n][a_d], k / v the layer's cache
+  // planes [P + n][a_d]; a_H heads of 128; a_scratch holds the split partials
+  const void* aq = nullptr;
+  const void* ak = nullptr;
+  const void* av = nullptr;
+  void* aout = nullptr;
+  int64_t aP = 0;
+  int aH = 0, a_d = 0;
+  float* a_scratch = nullptr;
+  size_t a_scratch_bytes = 0;
 };
+// can a chain run this request's attention as its first phase (#SMs >= heads, hd 128)?
+bool chain_attn_supported(int64_t n, int64_t P, int H, int hd);
 bool chain_tc_supported(int64_t M, int N, int K);
 bool chain_ln_supported(int d);
 // debug: chain timeline probe (PCB_CHAIN_PROBE=1): times [n][8 phases][160 CTAs][4]

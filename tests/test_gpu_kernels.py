@@ -114,3 +114,26 @@ def test_chain_and_ln_fold_full_depth():
     for other in ("ln", "kernels"):
         assert rel(out["fold"], out[other]) <= BF16_REL
         assert same_greedy_token(out["fold"], out[other])
+
+
+@pytest.mark.parametrize("doc_len,suffix", [(4096, 64), (700, 128), (37, 1), (0, 40), (130, 120)])
+def test_chain_attention_phase(m7, doc_len, suffix):
+    """The chain's attention phase (first phase of every per-layer chain: (head, key split)
+    items, global-memory split merge) vs the standalone attention kernel between chains, over
+    split counts 1..8 (key blocks), a lone decode-like token, an uncached prompt (P = 0) and a
+    128-row suffix (the whole query tile)."""
+    doc = "".join(chr(97 + (i * 7) % 26) for i in range(doc_len))
+    mod = f'<module name="doc">{doc}</module>' if doc_len else ""
+    schema = pcb.Schema.parse(f'<schema name="ca{doc_len}">{mod}</schema>')
+    store = pcb.ModuleStore(m7)
+    store.encode_schema(schema)
+    tail = ("Question about the text: what letters repeat and why " * 4)[:suffix]
+    prompt = f'<prompt schema="ca{doc_len}">' + ("<doc/>" if doc_len else "") + tail + "</prompt>"
+    out = {}
+    for v in (1, 0):
+        m7.set_option("chain_attn", v)
+        out[v] = pcb.serve(store, schema, prompt, 1).first_token_logits
+    m7.set_option("chain_attn", 1)
+    assert np.isfinite(out[1]).all()
+    assert rel(out[1], out[0]) <= BF16_REL
+    assert same_greedy_token(out[1], out[0])

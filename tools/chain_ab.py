@@ -32,8 +32,9 @@ def dump():
 
 VARIANTS = [
     ("per-GEMM kernels", {"chain": 0}),
-    ("chain", {"chain": 1, "ln_fold": 1}),
-    ("chain, LN phases", {"chain": 1, "ln_fold": 0}),
+    ("chain", {"chain": 1, "ln_fold": 1, "chain_attn": 0}),
+    ("chain+attn", {"chain": 1, "ln_fold": 1, "chain_attn": 1}),
+    ("chain, LN phases", {"chain": 1, "ln_fold": 0, "chain_attn": 0}),
 
 ]
 if os.environ.get("AB_VARIANTS"):
@@ -65,6 +66,7 @@ for name, v in res.items():
 # ---- chain timeline of one request ----
 m.set_option("chain", 1)
 m.set_option("ln_fold", int(os.environ.get("TL_FOLD", "1")))
+m.set_option("chain_attn", int(os.environ.get("TL_ATTN", "1")))
 pcb.serve(st, s, parsed[0], max_new_tokens=1)
 m.sync()
 dump()
@@ -77,7 +79,7 @@ prev_end = None
 for i in range(n):
     npn = int(phases[i])
     t = times[i, :npn, :148].astype(np.int64)  # [ph][cta][ev]
-    names = ["LN1", "QKV"] if npn == 2 else (names6 + ["?"] * 8)[:npn]
+    names = ["LN1", "QKV"] if npn == 2 else (["ATTN", "O", "W1", "W2", "QKV"] if npn == 5 else (names6 + ["?"] * 8)[:npn])
     for ph in range(npn):
         ev = t[ph]
         done = ev[:, 2]
@@ -127,3 +129,22 @@ for key, rows in agg.items():
         if vals:
             out.append(f"{k} {statistics.median(vals):6.1f}")
     print(f"  {str(key):28s} x{len(rows):3d}  " + "  ".join(out))
+
+# ---- attention phase: per-CTA event distribution (us from the earliest phase start) ----
+if os.environ.get("TL_ATTN", "1") != "0":
+    rows = []
+    for i in range(n):
+        if int(phases[i]) != 5:
+            continue
+        ev = times[i, 0, :128].astype(np.int64)
+        t0 = ev[:, 0][ev[:, 0] > 0].min()
+        rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 4, 5, 2)])
+    if rows:
+        a = np.array(rows)  # [chain][event][cta]
+        print("ATTN per-CTA events (median over chains of the percentile), us: start / last PV / a_done / flags / done")
+        for q in (0, 50, 90, 100):
+            print(f"  p{q:3d}  " + "  ".join(f"{np.median(np.percentile(a[:, k, :], q, axis=1)):6.1f}" for k in range(5)))
+        # is the straggler split a fixed one (last split holds the diagonal block)?
+        lastpv = np.median(a[:, 1, :], axis=0).reshape(-1, 4)
+        print("  last PV by split (median over heads):", np.round(np.median(lastpv, axis=0), 1))
+        print("  last PV by head (median over splits):", np.round(np.median(lastpv, axis=1), 1))

@@ -14,13 +14,14 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_r
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $OUT/launches.csv python tools/prof_step.py > $OUT/launches.log 2>&1
 # full captures of the top kernels of the measured cached request (2 layers keep the replay
-# short).  Launch order: precompute (per-GEMM k_gemm_sk, 2 attention), warm-up request (3
-# chains, 2 attention, 1 assembly), measured request -> skip counts below.
+# short).  Launch order: precompute (per-GEMM k_gemm_sk, 2 prefill attention), warm-up request
+# (3 chains -- attention is the first phase of the per-layer chains -- 1 assembly), measured
+# request -> skip counts below (the attention capture is the precompute's prefill kernel).
 cap() {  # kernel-regex skip count
   PROF_LAYERS=2 PROF_WARM=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 \
     -o $OUT/full_$1 python tools/prof_step.py > $OUT/full_$1.log 2>&1
 }
 cap k_chain 3 3
-cap k_attn_tc 4 1
+cap k_attn_tc 0 1
 cap k_assemble 1 1
 ls -la $OUT
