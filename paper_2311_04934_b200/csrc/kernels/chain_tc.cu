@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <type_traits>
 
 #include "gemm_common.cuh"
 
@@ -71,6 +72,7 @@ struct PhaseDev {
   // attention phase: item = (head, key split); partials [items][128][128] then (m, l) [items][128]
   int64_t aP;
   int aH, aS, a_d;
+  int adup;      // n <= 64: queries duplicated in the Q tile, each half of the lanes takes half the keys
   float ascale;  // log2(e) / sqrt(128)
   float* apart;
   __nv_bfloat16* aout;
@@ -307,7 +309,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           tma_prefetch(&p.tma[2]);
           pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
           mbar_expect_tx(a_qfull, 32768);
-          for (int a = 0; a < 2; ++a) tma_load_2d(aQ + a * 16384, &p.tma[0], a_qfull, h * 128 + a * 64, 0);
+          for (int a = 0; a < 2; ++a)  // 64-row boxes: rows [0, 64) twice (dup) or [0, 128)
+            for (int hh = 0; hh < 2; ++hh)
+              tma_load_2d(aQ + a * 16384 + hh * 8192, &p.tma[0], a_qfull, h * 128 + a * 64, A.adup ? 0 : 64 * hh);
           for (int it = 0; it < nb; ++it) {
             const int s = it % AKV;
             mbar_wait(&a_kvempty[s], ((it / AKV) & 1) ^ 1);
@@ -455,125 +459,171 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
       if (P.kind == CHAIN_LN) {
         for (int64_t r = c; r < P.M; r += C) ln_row(P, r, red, et);
       } else if (P.kind == CHAIN_ATTN) {
-        // ---- softmax: query row = TMEM lane (reference model.cpp:401-427, causal by
-        // sequence order: query i sees keys j <= P + i) ----
+        // ---- softmax: one thread per TMEM lane (reference model.cpp:401-427, causal by
+        // sequence order: query i sees keys j <= P + i).  n <= 64 ("dup"): the Q tile holds
+        // the n queries twice, lanes [0, 64) take keys [0, 32) of every block and lanes
+        // [64, 128) keys [32, 64) -- all four warps work, each on half the columns, and the
+        // two halves of a query merge like two more key splits ----
         const int epoch = p.epoch0 + ph;
         int h = 0, sp = 0, b0 = 0, nb = 0;
         if (c < P.items) attn_range(P, h, sp, b0, nb);
         const int64_t n_ = P.M;
-        const int64_t limit = P.aP + row;
+        const bool dup = P.adup;
+        const int qi = dup ? (row & 63) : row;  // query of this lane
+        const int64_t limit = P.aP + qi;
         float m = -INFINITY, l = 0.f;
-        const bool live = q * 32 < n_;  // a warp whose rows are all past n keeps the protocol only
+        const bool live = (dup ? ((q & 1) * 32) : (q * 32)) < n_;  // else the warp keeps the protocol only
         if (et == 0) ctl(p, ph, 0);
-        for (int it = 0; it < nb; ++it) {
-          const int64_t j0 = static_cast<int64_t>(b0 + it) * 64;
-          if (!live) {
+        auto blocks = [&](auto ncols) {
+          constexpr int NC = decltype(ncols)::value;  // score columns per lane: 64, or 32 (dup)
+          const int c0 = NC == 32 ? (row >> 6) * 32 : 0;
+          for (int it = 0; it < nb; ++it) {
+            const int64_t j0 = static_cast<int64_t>(b0 + it) * 64 + c0;
+            if (!live) {
+              if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
+              mbar_arrive(a_pfull);
+              continue;
+            }
+            mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
+            tc_fence_after();
+            float sv[NC];
+            {
+              uint32_t raw[NC];
+#pragma unroll
+              for (int x = 0; x < NC; x += 16) tmem_ld16_nowait(aS0 + (it & 1) * 64 + lane_off + c0 + x, raw + x);
+              tmem_wait_ld();
+#pragma unroll
+              for (int x = 0; x < NC; ++x) sv[x] = __uint_as_float(raw[x]);
+            }
+            if (j0 + NC - 1 > limit) {
+#pragma unroll
+              for (int x = 0; x < NC; ++x)
+                if (j0 + x > limit) sv[x] = -INFINITY;
+            }
+            float mx[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) mx[x] = sv[x];
+#pragma unroll
+            for (int x = 8; x < NC; ++x) mx[x & 7] = fmaxf(mx[x & 7], sv[x]);
+#pragma unroll
+            for (int w = 4; w; w >>= 1)
+#pragma unroll
+              for (int x = 0; x < w; ++x) mx[x] = fmaxf(mx[x], mx[x + w]);
+            const float bm = mx[0];
+            const bool grow = bm > m + kRescaleThreshold / P.ascale || (m == -INFINITY && bm > -INFINITY);
+            if (__any_sync(0xffffffffu, grow) && it > 0) {
+              mbar_wait(&a_pvdone[(it - 1) & 1], ((it - 1) >> 1) & 1);
+              tc_fence_after();
+              const float f = grow ? fast_exp2((m - bm) * P.ascale) : 1.f;
+#pragma unroll 1
+              for (int x = 0; x < 128; x += 16) {
+                float ov[16];
+                tmem_ld16(aO + lane_off + x, ov);
+#pragma unroll
+                for (int y = 0; y < 16; ++y) ov[y] *= f;
+                tmem_st16(aO + lane_off + x, ov);
+              }
+              tmem_st_wait();
+            }
+            if (grow) {
+              l *= fast_exp2((m - bm) * P.ascale);
+              m = bm;
+            }
+            const float mb = (m == -INFINITY) ? 0.f : m * P.ascale;
+            float bs[4] = {0.f, 0.f, 0.f, 0.f};
+            uint32_t packed[NC / 2];
+#pragma unroll
+            for (int x = 0; x < NC; x += 2) {
+              const float p0 = fast_exp2(fmaf(sv[x], P.ascale, -mb));
+              const float p1 = fast_exp2(fmaf(sv[x + 1], P.ascale, -mb));
+              bs[(x >> 1) & 3] += p0 + p1;
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+              packed[x >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
+            if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);  // P buffer free
+            // P row (64 keys, SW128): this lane's columns, zeros in the other half (dup)
+            uint8_t* prow = aPb + (it & 1) * 16384 + row * 128;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {  // 16-byte chunk x holds columns [8x, 8x + 8)
+              const int k = x & (NC / 8 - 1);
+              const bool mine = NC == 64 || (x >> 2) == (row >> 6);
+              const uint4 v4 = mine ? make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3])
+                                    : make_uint4(0u, 0u, 0u, 0u);
+              *reinterpret_cast<uint4*>(prow + ((x ^ (row & 7)) << 4)) = v4;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_fence_before();
             if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
             mbar_arrive(a_pfull);
-            continue;
           }
-          mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
-          tc_fence_after();
-          float sv[64];
-          {
-            uint32_t raw[64];
-#pragma unroll
-            for (int x = 0; x < 64; x += 16) tmem_ld16_nowait(aS0 + (it & 1) * 64 + lane_off + x, raw + x);
-            tmem_wait_ld();
-#pragma unroll
-            for (int x = 0; x < 64; ++x) sv[x] = __uint_as_float(raw[x]);
-          }
-          if (j0 + 63 > limit) {
-#pragma unroll
-            for (int x = 0; x < 64; ++x)
-              if (j0 + x > limit) sv[x] = -INFINITY;
-          }
-          float mx[8];
-#pragma unroll
-          for (int x = 0; x < 8; ++x) mx[x] = sv[x];
-#pragma unroll
-          for (int x = 8; x < 64; ++x) mx[x & 7] = fmaxf(mx[x & 7], sv[x]);
-#pragma unroll
-          for (int w = 4; w; w >>= 1)
-#pragma unroll
-            for (int x = 0; x < w; ++x) mx[x] = fmaxf(mx[x], mx[x + w]);
-          const float bm = mx[0];
-          const bool grow = bm > m + kRescaleThreshold / P.ascale || (m == -INFINITY && bm > -INFINITY);
-          if (__any_sync(0xffffffffu, grow) && it > 0) {
-            mbar_wait(&a_pvdone[(it - 1) & 1], ((it - 1) >> 1) & 1);
-            tc_fence_after();
-            const float f = grow ? fast_exp2((m - bm) * P.ascale) : 1.f;
-#pragma unroll 1
-            for (int x = 0; x < 128; x += 16) {
-              float ov[16];
-              tmem_ld16(aO + lane_off + x, ov);
-#pragma unroll
-              for (int y = 0; y < 16; ++y) ov[y] *= f;
-              tmem_st16(aO + lane_off + x, ov);
-            }
-            tmem_st_wait();
-          }
-          if (grow) {
-            l *= fast_exp2((m - bm) * P.ascale);
-            m = bm;
-          }
-          const float mb = (m == -INFINITY) ? 0.f : m * P.ascale;
-          float bs[4] = {0.f, 0.f, 0.f, 0.f};
-          uint32_t packed[32];
-#pragma unroll
-          for (int x = 0; x < 64; x += 2) {
-            const float p0 = fast_exp2(fmaf(sv[x], P.ascale, -mb));
-            const float p1 = fast_exp2(fmaf(sv[x + 1], P.ascale, -mb));
-            bs[(x >> 1) & 3] += p0 + p1;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            packed[x >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
-          if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);  // P buffer free
-          uint8_t* prow = aPb + (it & 1) * 16384 + row * 128;
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            uint4 v4 = make_uint4(packed[4 * x], packed[4 * x + 1], packed[4 * x + 2], packed[4 * x + 3]);
-            *reinterpret_cast<uint4*>(prow + ((x ^ (row & 7)) << 4)) = v4;
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tc_fence_before();
-          if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
-          mbar_arrive(a_pfull);
-        }
-        float* part = P.apart + (static_cast<int64_t>(c) * 128 + row) * 128;
+        };
+        if (dup) blocks(std::integral_constant<int, 32>{});
+        else blocks(std::integral_constant<int, 64>{});
+        // one partial per (query, split): the dup halves combine first through shared memory
+        // (the K/V stages are idle once the last PV completed); a single split writes O
+        const int nparts = P.aS;
+        const bool out_lane = dup ? row < 64 : true;  // lanes that own a query's result
+        float* part = P.apart + (static_cast<int64_t>(c) * 128 + qi) * 128;
         float2* ml = reinterpret_cast<float2*>(P.apart + static_cast<int64_t>(P.items) * 128 * 128);
         if (nb > 0) {
           mbar_wait(&a_pvdone[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
           tc_fence_after();
-          if (P.aS == 1) {
-            const float inv = 1.f / l;
-            __nv_bfloat16* dst = P.aout + row * P.a_d + h * 128;
+          constexpr int kXld = 132;  // padded fp32 row
+          float* xo = reinterpret_cast<float*>(aKV);
+          float2* xml = reinterpret_cast<float2*>(aKV + 64 * kXld * 4);
+          float w0 = 1.f, w1 = 0.f;
+          // tcgen05.ld is warp-collective: lane conditions only guard the memory operations
+          if (dup) {
+            if (row >= 64) {
+#pragma unroll 1
+              for (int x = 0; x < 128; x += 16) {
+                float ov[16];
+                tmem_ld16(aO + lane_off + x, ov);
+                if (qi < n_)
+#pragma unroll
+                  for (int y = 0; y < 16; y += 4)
+                    *reinterpret_cast<float4*>(xo + qi * kXld + x + y) =
+                        make_float4(ov[y], ov[y + 1], ov[y + 2], ov[y + 3]);
+              }
+              if (qi < n_) xml[qi] = make_float2(m, l);
+            }
+            named_bar(1, 128);
+            if (row < 64 && qi < n_) {
+              const float2 o = xml[qi];
+              const float M = l > 0.f && o.y > 0.f ? fmaxf(m, o.x) : (l > 0.f ? m : o.x);
+              w0 = l > 0.f ? fast_exp2((m - M) * P.ascale) : 0.f;
+              w1 = o.y > 0.f ? fast_exp2((o.x - M) * P.ascale) : 0.f;
+              l = w0 * l + w1 * o.y;
+              m = M;
+            }
+          }
+          if (out_lane) {
+            const float inv = nparts == 1 ? 1.f / l : 1.f;
+            __nv_bfloat16* dst = P.aout + qi * P.a_d + h * 128;
 #pragma unroll 1
             for (int x = 0; x < 128; x += 16) {
               float ov[16];
               tmem_ld16(aO + lane_off + x, ov);
-              if (row < n_) {
+              if (qi >= n_) continue;
+              if (dup) {
+#pragma unroll
+                for (int y = 0; y < 16; ++y) ov[y] = w0 * ov[y] + w1 * xo[qi * kXld + x + y];
+              }
+              if (nparts == 1) {
                 uint4 w2[2];
                 __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w2);
 #pragma unroll
                 for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
                 *reinterpret_cast<uint4*>(dst + x) = w2[0];
                 *reinterpret_cast<uint4*>(dst + x + 8) = w2[1];
-              }
-            }
-          } else {
-            // park the unnormalised O row and (m, l) for the split merge
-#pragma unroll 1
-            for (int x = 0; x < 128; x += 16) {
-              float ov[16];
-              tmem_ld16(aO + lane_off + x, ov);
-              if (row < n_)
+              } else {  // park the unnormalised O row for the split merge
 #pragma unroll
                 for (int y = 0; y < 16; y += 4)
                   __stcg(reinterpret_cast<float4*>(part + x + y), make_float4(ov[y], ov[y + 1], ov[y + 2], ov[y + 3]));
+              }
             }
-            if (row < n_) __stcg(ml + static_cast<int64_t>(c) * 128 + row, make_float2(m, l));
+            if (nparts > 1 && qi < n_) __stcg(ml + static_cast<int64_t>(c) * 128 + qi, make_float2(m, l));
           }
         }
         tc_fence_before();
@@ -581,13 +631,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         // a_done releases the W producer onto the ring (the next phase's weights).  A split
         // CTA publishes its partial first: with the weight prefetch already in flight its
         // flag became visible ~2 us later (tools/chain_ab.py, per-CTA attention events)
-        if (!(c < P.items && P.aS > 1)) mbar_arrive(a_done);
-        if (c < P.items && P.aS > 1) {
-          // the S split CTAs of head h each merge query rows {sp, sp + S, ...} of all S
-          // partials in split order (deterministic):
+        const bool merge = c < P.items && nparts > 1;
+        if (!merge) mbar_arrive(a_done);
+        if (merge) {
+          // the S split CTAs of head h each merge queries {sp, sp + S, ...} of all S partials
+          // in split order (deterministic):
           //   O = sum_s w_s O_s / sum_s w_s l_s,  w_s = 2^((m_s - M) scale),  M = max_s m_s
           named_bar(1, 128);
-          if (et == 0) st_release(p.flags + c, epoch);
+          if (et == 0) {
+            st_release(p.flags + c, epoch);
+            ctl(p, ph, 8);
+          }
           mbar_arrive(a_done);
           const int base = h * P.aS;
           if (et < P.aS)
@@ -599,40 +653,40 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           named_bar(1, 128);
           if (et == 0) ctl(p, ph, 5);
           const int x0 = (et & 7) * 16;
+          auto prow_of = [&](int u, int64_t r2) { return static_cast<int64_t>(base + u) * 128 + r2; };
           for (int64_t r2 = sp + static_cast<int64_t>(et >> 3) * P.aS; r2 < n_; r2 += 16 * P.aS) {
-            float ms[8], ls[8];
+            float ms[16], ls[16];
 #pragma unroll
-            for (int s2 = 0; s2 < 8; ++s2) {
+            for (int u = 0; u < 16; ++u) {
               float2 v2 = make_float2(-INFINITY, 0.f);
-              if (s2 < P.aS) v2 = __ldcg(ml + static_cast<int64_t>(base + s2) * 128 + r2);
-              ms[s2] = v2.x;
-              ls[s2] = v2.y;
+              if (u < nparts) v2 = __ldcg(ml + prow_of(u, r2));
+              ms[u] = v2.x;
+              ls[u] = v2.y;
             }
             float M = -INFINITY;
 #pragma unroll
-            for (int s2 = 0; s2 < 8; ++s2)
-              if (s2 < P.aS && ls[s2] > 0.f) M = fmaxf(M, ms[s2]);
+            for (int u = 0; u < 16; ++u)
+              if (u < nparts && ls[u] > 0.f) M = fmaxf(M, ms[u]);
             float den = 0.f, acc[16];
 #pragma unroll
             for (int x = 0; x < 16; ++x) acc[x] = 0.f;
 #pragma unroll
-            for (int g = 0; g < 8; g += 4) {
-              if (g >= P.aS) break;
+            for (int g = 0; g < 16; g += 4) {
+              if (g >= nparts) break;
               float4 f[4][4];
 #pragma unroll
               for (int u = 0; u < 4; ++u)
-                if (g + u < P.aS) {
-                  const float4* src =
-                      reinterpret_cast<const float4*>(P.apart + (static_cast<int64_t>(base + g + u) * 128 + r2) * 128 + x0);
+                if (g + u < nparts) {
+                  const float4* src = reinterpret_cast<const float4*>(P.apart + prow_of(g + u, r2) * 128 + x0);
 #pragma unroll
                   for (int x = 0; x < 4; ++x) f[u][x] = __ldcg(src + x);
                 }
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const int s2 = g + u;
-                if (s2 >= P.aS || !(ls[s2] > 0.f)) continue;
-                const float w = fast_exp2((ms[s2] - M) * P.ascale);
-                den += w * ls[s2];
+                const int uu = g + u;
+                if (uu >= nparts || !(ls[uu] > 0.f)) continue;
+                const float w = fast_exp2((ms[uu] - M) * P.ascale);
+                den += w * ls[uu];
 #pragma unroll
                 for (int x = 0; x < 4; ++x) {
                   acc[4 * x] += w * f[u][x].x;
@@ -919,14 +973,15 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.aH = st.aH;
       d.a_d = st.a_d;
       const int64_t nblk = (st.aP + st.M + 63) / 64;
-      d.aS = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({C / st.aH, nblk, 8})));
+      d.aS = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({C / st.aH, nblk, 8})));  // <= 16 partials
       d.items = st.aH * d.aS;
       d.ascale = 1.4426950408889634f / sqrtf(128.f);
       d.apart = st.a_scratch;
       d.aout = static_cast<__nv_bfloat16*>(st.aout);
       if (static_cast<size_t>(d.items) * 128 * 130 * sizeof(float) > st.a_scratch_bytes)
         throw std::runtime_error("chain: attention scratch too small");
-      p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 128);
+      d.adup = st.M <= 64 && !std::getenv("PCB_CHAIN_ATTN_NODUP");
+      p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 64);
       p.tma[1] = tmap_bf16_2d(st.ak, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
       p.tma[2] = tmap_bf16_2d(st.av, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
     } else {

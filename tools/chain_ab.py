@@ -138,12 +138,12 @@ if os.environ.get("TL_ATTN", "1") != "0":
             continue
         ev = times[i, 0, :128].astype(np.int64)
         t0 = ev[:, 0][ev[:, 0] > 0].min()
-        rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 4, 5, 2)])
+        rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 4, 8, 5, 2)])
     if rows:
         a = np.array(rows)  # [chain][event][cta]
-        print("ATTN per-CTA events (median over chains of the percentile), us: start / last PV / a_done / flags / done")
+        print("ATTN per-CTA events (median over chains of the percentile), us: start / last PV / a_done / released / flags / done")
         for q in (0, 50, 90, 100):
-            print(f"  p{q:3d}  " + "  ".join(f"{np.median(np.percentile(a[:, k, :], q, axis=1)):6.1f}" for k in range(5)))
+            print(f"  p{q:3d}  " + "  ".join(f"{np.median(np.percentile(a[:, k, :], q, axis=1)):6.1f}" for k in range(6)))
         # is the straggler split a fixed one (last split holds the diagonal block)?
         lastpv = np.median(a[:, 1, :], axis=0).reshape(-1, 4)
         print("  last PV by split (median over heads):", np.round(np.median(lastpv, axis=0), 1))
