@@ -117,8 +117,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* kv_full = bar + 1;                // [KV_STAGES]
   uint64_t* kv_empty = kv_full + KV_STAGES;   // [KV_STAGES]
   uint64_t* s_full = kv_empty + KV_STAGES;    // [2] score buffer b holds blocks it with it&1 == b
+  // [2] P(it) of blocks it with it&1 == b in smem.  Two barriers, not one: with a single
+  // p_full the softmax could complete the phase of block it+1 (S(it+1) is already issued and
+  // its P buffer free) before the MMA thread observed block it's phase -- two completions
+  // restore the parity the MMA waits on and it sleeps forever (seen in the chain version)
   uint64_t* p_full = s_full + 2;
-  uint64_t* pv_done = p_full + 1;             // [2] PV of blocks it with it&1 == b completed
+  uint64_t* pv_done = p_full + 2;             // [2] PV of blocks it with it&1 == b completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -152,7 +156,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
-    mbar_init(p_full, 128);
+    mbar_init(&p_full[0], 128);
+    mbar_init(&p_full[1], 128);
     mbar_init(&pv_done[0], 1);
     mbar_init(&pv_done[1], 1);
     fence_barrier_init();
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // S(it+1) goes to the other buffer; its previous content S(it-1) was consumed
         // before p_full(it-1), which the previous iteration waited for.
         if (it + 1 < nb) issue_qk(it + 1);
-        mbar_wait(p_full, it & 1);  // P(it) in smem (and any O correction done)
+        mbar_wait(&p_full[it & 1], (it >> 1) & 1);  // P(it) in smem (and any O correction done)
         probe(p, 2, it);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sKV + (it % KV_STAGES) * S::kStage + S::kKV);
@@ -253,8 +258,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     for (int it = 0; it < nb; ++it) {
       const int64_t j0 = (b0 + it) * BKV;
       if (!live) {
-        if (it > 0) mbar_wait(p_full, (it - 1) & 1);  // never arrive into an earlier phase
-        mbar_arrive(p_full);
+        // p_full[it&1]'s previous phase (block it-2) completed before PV(it-2) was issued
+        if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
+        mbar_arrive(&p_full[it & 1]);
         continue;
       }
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
@@ -335,8 +341,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       // a fast warp must not arrive for block it while block it-1's phase is still
       // collecting arrivals (its arrival would complete that phase early)
-      if (it > 0) mbar_wait(p_full, (it - 1) & 1);
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[it & 1]);  // the P-buffer wait above ordered it after block it-2's phase
       if (threadIdx.x == 128) probe(p, 1, it);
     }
     if (nb > 0) {

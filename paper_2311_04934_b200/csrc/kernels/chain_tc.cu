@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   uint64_t* a_kvfull = a_qfull + 1;    // [AKV]
   uint64_t* a_kvempty = a_kvfull + 4;  // [AKV]
   uint64_t* a_sfull = a_kvempty + 4;   // [2]
-  uint64_t* a_pfull = a_sfull + 2;
-  uint64_t* a_pvdone = a_pfull + 1;    // [2]
+  uint64_t* a_pfull = a_sfull + 2;     // [2] (two: see attn_tc.cu, one p_full can deadlock)
+  uint64_t* a_pvdone = a_pfull + 2;    // [2]
   uint64_t* a_done = a_pvdone + 2;     // this CTA's attention is off the ring (128 arrivals)
   const uint32_t tcols = has_attn ? 512u : S::kCols;
 
@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         mbar_init(&a_sfull[b], 1);
         mbar_init(&a_pvdone[b], 1);
       }
-      mbar_init(a_pfull, 128);
+      mbar_init(&a_pfull[0], 128);
+      mbar_init(&a_pfull[1], 128);
       mbar_init(a_done, 128);
     }
     fence_barrier_init();
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         issue_qk(0);
         for (int it = 0; it < nb; ++it) {
           if (it + 1 < nb) issue_qk(it + 1);
-          mbar_wait(a_pfull, it & 1);
+          mbar_wait(&a_pfull[it & 1], (it >> 1) & 1);
           tc_fence_after();
           const uint32_t v_addr = smem_u32(aKV + (it % AKV) * 32768 + 16384);
           const uint32_t pb = p_addr + (it & 1) * 16384;
@@ -480,8 +481,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           for (int it = 0; it < nb; ++it) {
             const int64_t j0 = static_cast<int64_t>(b0 + it) * 64 + c0;
             if (!live) {
-              if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
-              mbar_arrive(a_pfull);
+              if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);
+              mbar_arrive(&a_pfull[it & 1]);
               continue;
             }
             mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
@@ -554,8 +555,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc_fence_before();
-            if (it > 0) mbar_wait(a_pfull, (it - 1) & 1);
-            mbar_arrive(a_pfull);
+            mbar_arrive(&a_pfull[it & 1]);  // ordered after block it-2's phase by the P-buffer wait
           }
         };
         if (dup) blocks(std::integral_constant<int, 32>{});
@@ -887,9 +887,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                   v[4 * x + 3] += f[jj][x].w;
                 }
               }
+            if (et == 0 && m0 == s0) ctl(p, ph, 9);
             if (m0 + 16 < lim) epi_prefetch(e, n, P.N, m0 + 16, lim, nxt);
             epi_chunk(e, n, P.N, m0, lim, v, cur, ln);
+            if (et == 0 && m0 == s0) ctl(p, ph, 10);
             if (P.stats_out) stats_chunk(tile, m0, lim);
+            if (et == 0 && m0 == s0) ctl(p, ph, 11);
             cur = nxt;
           }
         }

@@ -137,3 +137,22 @@ def test_chain_attention_phase(m7, doc_len, suffix):
     assert np.isfinite(out[1]).all()
     assert rel(out[1], out[0]) <= BF16_REL
     assert same_greedy_token(out[1], out[0])
+
+
+def test_chain_attention_repeated(m7):
+    """Barrier-protocol stress: many back-to-back cached requests through the chain's attention
+    phase (a single P-ready mbarrier once let the softmax complete two phases before the MMA
+    thread looked -- an intermittent hang, ~2 in 3 runs of tools/chain_ab.py)."""
+    doc = "".join(chr(97 + (i * 5) % 26) for i in range(2000))
+    schema = pcb.Schema.parse(f'<schema name="rep"><module name="doc">{doc}</module></schema>')
+    store = pcb.ModuleStore(m7)
+    store.encode_schema(schema)
+    first = None
+    for i in range(60):
+        tail = ("tell me more about it please " * 3)[: 8 + (i % 5) * 14]
+        r = pcb.serve(store, schema, f'<prompt schema="rep"><doc/>{tail}</prompt>', 1)
+        if i % 5 == 0:
+            if first is None:
+                first = r.first_token_logits
+            else:
+                assert np.array_equal(first, r.first_token_logits)  # same prompt: bitwise repeatable

@@ -106,12 +106,11 @@ for i in range(n):
             if ok5.any():
                 row["flagwait"] = np.median((ev[:, 5] - ev[:, 4])[ok5]) / 1e3
                 row["owner_epi"] = np.median((ev[:, 2] - ev[:, 5])[ok5]) / 1e3
-                ok8 = ok5 & (ev[:, 8] > 0) & (ev[:, 11] > 0)
+                ok8 = ok5 & (ev[:, 9] > 0) & (ev[:, 11] > 0)
                 if ok8.any():
-                    row["o_tmem"] = np.median((ev[:, 8] - ev[:, 5])[ok8]) / 1e3
-                    row["o_partials"] = np.median((ev[:, 9] - ev[:, 8])[ok8]) / 1e3
-                    row["o_epi_g0"] = np.median((ev[:, 10] - ev[:, 9])[ok8]) / 1e3
-                    row["o_rest"] = np.median((ev[:, 11] - ev[:, 10])[ok8]) / 1e3
+                    row["o_partials"] = np.median((ev[:, 9] - ev[:, 5])[ok8]) / 1e3
+                    row["o_epi"] = np.median((ev[:, 10] - ev[:, 9])[ok8]) / 1e3
+                    row["o_stats"] = np.median((ev[:, 11] - ev[:, 10])[ok8]) / 1e3
                     row["o_after"] = np.median((ev[:, 2] - ev[:, 11])[ok8]) / 1e3
         row["phase_span"] = (done.max() - (t[ph - 1][:, 2].max() if ph > 0 else t[0][:, 2].min())) / 1e3
         agg.setdefault((npn, names[ph]), []).append(row)
