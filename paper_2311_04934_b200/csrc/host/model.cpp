@@ -144,6 +144,9 @@ struct Workspace {
   float* logits = nullptr;
   float *part = nullptr, *logits_loc = nullptr, *logits_gath = nullptr;  // tensor parallel
   float* lnstats = nullptr;  // LN fold: [hidden/128 tiles][cap_n][2]
+  float2* rope_tab = nullptr;  // [rope_half + 1][rope_ld] {cos, sin} per (pair, token), few-token forwards
+  int rope_half = 0;
+  int64_t rope_ld = 0;
   int tp = 1, Vl = 0;
   float* gemm_ws = nullptr;
   size_t gemm_ws_bytes = 0;
@@ -163,7 +166,7 @@ struct Workspace {
                     (void*)req,
                     (void*)mask, (void*)h, x, q,
                     attn, mid, (void*)logits, (void*)part, (void*)logits_loc, (void*)logits_gath, (void*)lnstats,
-                    (void*)gemm_ws,
+                    (void*)rope_tab, (void*)gemm_ws,
                     (void*)counters, (void*)attn_scratch})
       if (p) cudaFree(p);
     for (auto& e : staged)
@@ -196,6 +199,10 @@ struct Workspace {
       regrow(mid, c * 4 * d * es);
       if (tp > 1) regrow(part, c * d * 4);
       regrow(lnstats, ((d + 127) / 128) * c * 8);
+      if (rope_half > 0) {
+        rope_ld = (c + 15) / 16 * 16 + 16;  // slack: split slices may read a chunk past n
+        regrow(rope_tab, (rope_half + 1) * rope_ld * sizeof(float2));
+      }
       cap_n = c;
     }
     if (rows > cap_rows) {
@@ -294,6 +301,7 @@ Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_si
   ws_->Vl = vl_;
   ws_->tp = tp_size;
   ws_->dt = dtype;
+  if (c.pos_encoding == PosEncoding::Rope && dtype == BF16) ws_->rope_half = c.head_dim / 2;
 
   const int d = c.hidden;
   const size_t es = dtype == F32 ? 4 : 2;
@@ -690,7 +698,13 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   W.release_staging(s);
 
   prof_begin();
-  kern::embed(W.tok, W.pos, n, w_->embed, w_->abs_table, d, W.h, s);
+  // few-token forwards: the QKV epilogue reads this request's RoPE rows from a compact table
+  const bool rope_tab = W.rope_half > 0 && n <= 128;
+  if (rope_tab)
+    kern::embed(W.tok, W.pos, n, w_->embed, w_->abs_table, d, W.h, s, w_->cos32, w_->sin32, W.rope_half, W.rope_tab,
+                W.rope_ld);
+  else
+    kern::embed(W.tok, W.pos, n, w_->embed, w_->abs_table, d, W.h, s);
   prof_end(PROF_OTHER, 8.0 * n * d, 0);
 
   kern::AttnArgs aa;
@@ -733,6 +747,10 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     e.rope_sin64 = w_->sin64;
     e.rope_cos32 = w_->cos32;
     e.rope_sin32 = w_->sin32;
+    if (rope_tab) {
+      e.rope_tab = W.rope_tab;
+      e.rope_ld = W.rope_ld;
+    }
     return e;
   };
   kern::Epilogue eo;

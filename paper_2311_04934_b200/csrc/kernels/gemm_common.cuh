@@ -30,7 +30,17 @@ __device__ __forceinline__ void epi_prefetch(const Epilogue& ep, int n, int N, i
   } else if (kind == EPI_QKV) {
     const int d = ep.d, hd = ep.head_dim;
     const int seg = n / d, c = n - seg * d;
-    if (seg < 2 && ep.rope) {
+    if (seg < 2 && ep.rope && ep.rope_tab) {
+      const float4* src = reinterpret_cast<const float4*>(ep.rope_tab + ((c % hd) >> 1) * ep.rope_ld + m0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float4 t = src[u];
+        p.a[2 * u] = t.x;
+        p.b[2 * u] = t.y;
+        p.a[2 * u + 1] = t.z;
+        p.b[2 * u + 1] = t.w;
+      }
+    } else if (seg < 2 && ep.rope) {
       const int half = hd >> 1, pi = (c % hd) >> 1;
       const int32_t* pos = ep.pos + m0;
       const float* cs = ep.rope_cos32 + pi;

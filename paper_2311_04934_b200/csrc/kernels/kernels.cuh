@@ -42,6 +42,10 @@ struct Epilogue {
   const double* rope_sin64 = nullptr;
   const float* rope_cos32 = nullptr;   // (BF16 path)
   const float* rope_sin32 = nullptr;
+  // per-request rows of the two tables: rope_tab[pair][m] = {cos, sin} of token m's position
+  // (written by embed; contiguous in m, so a 16-token chunk is 8 vector loads, no pos lookup)
+  const float2* rope_tab = nullptr;
+  int64_t rope_ld = 0;  // multiple of 16
   float* resid = nullptr;
   void* out = nullptr;
   float* outf = nullptr;
@@ -64,8 +68,10 @@ void add_inplace(float* h, const float* part, int64_t n, cudaStream_t s);
 void interleave_shards(const float* in, int T, int64_t rows, int64_t Vl, float* out, cudaStream_t s);
 
 // ---- small ops ----
+// rope_tab (optional): also rope_tab[j * rope_ld + i] = {cos32, sin32}[pos[i] * half + j], j < half
 void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table, const float* abs_table,
-           int d, float* h, cudaStream_t s);
+           int d, float* h, cudaStream_t s, const float* cos32 = nullptr, const float* sin32 = nullptr, int half = 0,
+           float2* rope_tab = nullptr, int64_t rope_ld = 0);
 // out = LN(h) (gamma=1, beta=0, eps 1e-5), rows [row0, row0+n)
 void layernorm(int dtype, const float* h, int64_t n, int d, void* out, cudaStream_t s);
 // out[n] = sum_k W[n][k] of a row-major bf16 [N][K] matrix (fp32, LN-fold weight sums)

@@ -158,7 +158,7 @@ void fill_const(float* d, uint64_t n, float v, cudaStream_t s) {
 // embed (model.cpp:354-362): h[i] = embed[tok[i]] (+ abs_table[pos[i]])
 // ---------------------------------------------------------------------------
 __global__ void k_embed(const int32_t* tok, const int32_t* pos, const float* table, const float* abs_table, int d,
-                        float* h) {
+                        float* h, const float* cos32, const float* sin32, int half, float2* rope_tab, int64_t rope_ld) {
   pdl_trigger();
   pdl_wait();
   int64_t i = blockIdx.x;
@@ -168,12 +168,18 @@ __global__ void k_embed(const int32_t* tok, const int32_t* pos, const float* tab
     if (abs_table) v = __fadd_rn(v, abs_table[static_cast<int64_t>(pos[i]) * d + j]);
     h[i * d + j] = v;
   }
+  if (rope_tab) {
+    const int64_t p = static_cast<int64_t>(pos[i]) * half;
+    for (int j = threadIdx.x; j < half; j += blockDim.x) rope_tab[j * rope_ld + i] = make_float2(cos32[p + j], sin32[p + j]);
+  }
 }
 void embed(const int32_t* tok, const int32_t* pos, int64_t n, const float* table, const float* abs_table, int d,
-           float* h, cudaStream_t s) {
+           float* h, cudaStream_t s, const float* cos32, const float* sin32, int half, float2* rope_tab,
+           int64_t rope_ld) {
   if (n <= 0) return;
   PdlClass pc(PDL_EMBED);
-  launch_k(k_embed, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, tok, pos, table, abs_table, d, h);
+  launch_k(k_embed, dim3(static_cast<unsigned>(n)), dim3(256), 0, s, 1, tok, pos, table, abs_table, d, h, cos32, sin32,
+           half, rope_tab, rope_ld);
   PCB_CUDA(cudaGetLastError());
 }
 
