@@ -762,7 +762,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           named_bar(1, 128);
         };
         const int epoch = p.epoch0 + ph;
-        float* ws = p.ws + (ph & 1) * p.ws_half;  // [items][128][BN] partials
+        // [items][128][BN] fp16 partials (a K-split partial of 1024-4096 products; fp16's
+        // 2^-11 is 8x finer than the bf16 operands' rounding, and half the bytes shorten the
+        // publish -> flag -> reload round trip at every split phase end)
+        __half* ws = reinterpret_cast<__half*>(p.ws + (ph & 1) * p.ws_half);
         for (int i = c; i < P.items; i += C, ++seg) {
           const int tile = i / P.S, j = i - tile * P.S;
           const int n = tile * 128 + row;
@@ -828,13 +831,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           // split tile: park this k-split's partial, then finish a 1/S slice of the
           // token columns from all S partials of the tile
           {
-            float* dst = ws + (static_cast<int64_t>(i) * 128 + row) * BN;
+            __half* dst = ws + (static_cast<int64_t>(i) * 128 + row) * BN;
 #pragma unroll 1
             for (int cc = 0; cc < Mc; cc += 16) {
               tmem_ld16(acc + cc, v);
 #pragma unroll
-              for (int x = 0; x < 16; x += 4)
-                *reinterpret_cast<float4*>(dst + cc + x) = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
+              for (int x = 0; x < 16; x += 8) {
+                const __half2 h0 = __floats2half2_rn(v[x], v[x + 1]), h1 = __floats2half2_rn(v[x + 2], v[x + 3]);
+                const __half2 h2 = __floats2half2_rn(v[x + 4], v[x + 5]), h3 = __floats2half2_rn(v[x + 6], v[x + 7]);
+                *reinterpret_cast<uint4*>(dst + cc + x) =
+                    make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                               *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+              }
             }
           }
           tc_fence_before();
@@ -860,31 +868,28 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 #pragma unroll 1
           for (int m0 = s0; m0 < lim; m0 += 16) {
             // all S partials of these 16 columns in one batch of independent loads
-            float4 f[4][4];
+            uint2 f[4][4];  // 4 halves each (m0 is a multiple of 4)
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj)
               if (jj < P.S) {
-                const float4* src = reinterpret_cast<const float4*>(ws + (static_cast<int64_t>(base + jj) * 128 + row) *
-                                                                              BN + m0);
+                const uint2* src =
+                    reinterpret_cast<const uint2*>(ws + (static_cast<int64_t>(base + jj) * 128 + row) * BN + m0);
 #pragma unroll
                 for (int x = 0; x < 4; ++x) f[jj][x] = __ldcg(src + x);
               }
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-              v[4 * x] = f[0][x].x;
-              v[4 * x + 1] = f[0][x].y;
-              v[4 * x + 2] = f[0][x].z;
-              v[4 * x + 3] = f[0][x].w;
-            }
+            for (int x = 0; x < 16; ++x) v[x] = 0.f;
 #pragma unroll
-            for (int jj = 1; jj < 4; ++jj)
+            for (int jj = 0; jj < 4; ++jj)  // split order: deterministic
               if (jj < P.S) {
 #pragma unroll
                 for (int x = 0; x < 4; ++x) {
-                  v[4 * x] += f[jj][x].x;
-                  v[4 * x + 1] += f[jj][x].y;
-                  v[4 * x + 2] += f[jj][x].z;
-                  v[4 * x + 3] += f[jj][x].w;
+                  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&f[jj][x].x));
+                  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&f[jj][x].y));
+                  v[4 * x] += a.x;
+                  v[4 * x + 1] += a.y;
+                  v[4 * x + 2] += b.x;
+                  v[4 * x + 3] += b.y;
                 }
               }
             if (et == 0 && m0 == s0) ctl(p, ph, 9);
