@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             }
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
+            if (et == 0) ctl(p, ph, 9);
             if (tstore) {
               named_bar(1, 128);
               __nv_bfloat16* base;
@@ -823,6 +824,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 __nv_bfloat16* dst = off ? base + off[m] + q16 * 8 : base + m * ld + q16 * 8;
                 *reinterpret_cast<uint4*>(dst) = val;
               }
+              if (et == 0) ctl(p, ph, 10);
               named_bar(1, 128);  // T is reused by this CTA's next item
             }
             if (et == 0) ctl(p, ph, 5);

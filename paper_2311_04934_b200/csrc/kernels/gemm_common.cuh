@@ -19,10 +19,14 @@ using namespace tc;
 // ---------------------------------------------------------------------------
 struct EpiPre {
   float a[16], b[16];
+  float lnw;  // LN fold: sum_k W[n][k] (prefetched with the chunk's other operands)
 };
 
 __device__ __forceinline__ void epi_prefetch(const Epilogue& ep, int n, int N, int64_t m0, int64_t M, EpiPre& p) {
   const int kind = ep.kind;
+  // an L2 round trip under a saturated memory system is ~1 us: issued before the
+  // accumulator is ready instead of inside the first chunk (tools/chain_ab.py c0_values)
+  if (ep.ln_wsum) p.lnw = __ldg(ep.ln_wsum + n);
   if (kind == EPI_RESID) {
     const float* src = ep.resid + m0 * N + n;
 #pragma unroll
@@ -76,7 +80,7 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int6
   const int kind = ep.kind;
   const int jn = M - m0 >= 16 ? 16 : static_cast<int>(M - m0);
   if (lnst) {  // folded LayerNorm: {mean, rstd} of token m0 + j
-    const float ws = ep.ln_wsum[n];
+    const float ws = pre.lnw;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const float2 st = lnst[j < jn ? m0 + j : m0];
@@ -164,7 +168,7 @@ __device__ __forceinline__ void epi_values(const Epilogue& ep, int n, int64_t m0
                                            const EpiPre& pre, const float2* lnst) {
   const int jn = M - m0 >= 16 ? 16 : static_cast<int>(M - m0);
   if (lnst) {
-    const float ws = ep.ln_wsum[n];
+    const float ws = pre.lnw;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const float2 st = lnst[j < jn ? m0 + j : m0];

@@ -102,6 +102,11 @@ for i in range(n):
             row["pass_minus_lastdone"] = (np.median(ev[:, 7][okk]) - (t[ph - 1][:, 2].max() if ph > 0 else 0)) / 1e3 if ph > 0 else None
             ok4 = (ev[:, 4] > 0) & (ev[:, 1] > 0)
             row["accwait_after_mma"] = np.median((ev[:, 4] - ev[:, 1])[ok4]) / 1e3
+            ok9 = (ev[:, 9] > 0) & (ev[:, 4] > 0) & (ev[:, 10] > 0) & (ev[:, 11] == 0)
+            if ok9.any():  # S == 1 epilogue: chunk loop, staged-store copy, tail
+                row["s1_loop"] = np.median((ev[:, 9] - ev[:, 4])[ok9]) / 1e3
+                row["s1_copy"] = np.median((ev[:, 10] - ev[:, 9])[ok9]) / 1e3
+                row["s1_tail"] = np.median((ev[:, 5] - ev[:, 10])[ok9]) / 1e3
             ok5 = (ev[:, 5] > 0) & (ev[:, 4] > 0)
             if ok5.any():
                 row["flagwait"] = np.median((ev[:, 5] - ev[:, 4])[ok5]) / 1e3
