@@ -437,8 +437,31 @@ ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::Module
   sc.ensure(0, 0, m.config().vocab_size);
   const int64_t n = static_cast<int64_t>(up.tokens.size());
   model::KVBlock& work = arena_of(store, n_cached + n + std::max(0, req.max_new_tokens - 1));
+  // Zero-copy assembly: when every forward of this request runs the chain's attention phase
+  // (few suffix tokens, bf16) and no cached row is replaced for decoding, the modules' K/V
+  // are read in place from the store and the request cache holds only the new rows -- the
+  // assembly copy (2 x the cached bytes through HBM) disappears.  Otherwise concat_kv's copy.
+  bool zc = m.zero_copy && !selected.empty() && static_cast<int>(selected.size()) < kern::ChainStep::kMaxSeg &&
+            n > 0 && m.fused_attention_ok(n) && (req.max_new_tokens <= 1 || m.fused_attention_ok(1)) &&
+            up.arg_row_by_pos.empty() && up.drop_positions.empty();
+  for (auto& e : selected) zc = zc && !e->kv->host;
+  struct PrefixGuard {
+    model::Model& m;
+    ~PrefixGuard() { m.clear_kv_prefix(); }
+  } prefix_guard{m};
   CK(cudaEventRecord(sc.ev[0], m.stream()));
-  const int slow = assemble(m, selected, work, sc);
+  int slow = 0;
+  if (zc) {
+    std::vector<const model::KVBlock*> blocks;
+    for (auto& e : selected) {
+      blocks.push_back(e->kv.get());
+      work.positions.insert(work.positions.end(), e->kv->positions.begin(), e->kv->positions.end());
+    }
+    work.rows = n_cached;  // logical rows; [0, n_cached) live in the store blocks
+    m.set_kv_prefix(blocks);
+  } else {
+    slow = assemble(m, selected, work, sc);
+  }
   CK(cudaEventRecord(sc.ev[1], m.stream()));
   if (up.tokens.empty()) {
     CK(cudaStreamSynchronize(m.stream()));

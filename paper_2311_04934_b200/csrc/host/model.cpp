@@ -281,6 +281,7 @@ Model::Model(const ModelConfig& c, int dtype, int device, int tp_rank, int tp_si
   if (const char* v = std::getenv("PCB_CHAIN")) use_chain = v[0] != '0';
   if (const char* v = std::getenv("PCB_LN_FOLD")) ln_fold = v[0] != '0';
   if (const char* v = std::getenv("PCB_CHAIN_ATTN")) chain_attn = v[0] != '0';
+  if (const char* v = std::getenv("PCB_ZERO_COPY")) zero_copy = v[0] != '0';
   if (c.hidden != c.n_heads * c.head_dim) throw Error(ErrorCode::InvalidConfig, "hidden must equal n_heads * head_dim");
   if (c.n_layers < 1 || c.n_heads < 1 || c.head_dim < 2 || c.head_dim % 2 != 0)
     throw Error(ErrorCode::InvalidConfig, "bad layer/head geometry");
@@ -589,6 +590,30 @@ void Model::gemm(const void* A, const void* W, int64_t M, int N, int K, const vo
   prof_end(PROF_GEMM, gemm_alg_bytes(dtype_, M, N, K, e.kind), 2.0 * M * N * K);
 }
 
+void Model::set_kv_prefix(const std::vector<const KVBlock*>& blocks) {
+  if (static_cast<int>(blocks.size()) + 1 > kern::ChainStep::kMaxSeg)
+    throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix: too many blocks");
+  kv_prefix_.clear();
+  kv_prefix_rows_ = 0;
+  for (const KVBlock* b : blocks) {
+    if (b->host || b->dtype != dtype_ || b->hidden != cfg_.hidden || b->n_layers != cfg_.n_layers)
+      throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix: block must be a device block of this model");
+    if (b->rows == 0) continue;
+    kv_prefix_.push_back(b);
+    kv_prefix_rows_ += b->rows;
+  }
+}
+
+bool Model::fused_attention_ok(int64_t n) const {
+  const auto& c = cfg_;
+  const int d = c.hidden;
+  return use_chain && chain_attn && tp_size_ == 1 && dtype_ == BF16 && w_->packed && !force_simt && !force_simt_gemm &&
+         !force_simt_attn && c.pos_encoding != PosEncoding::Alibi && c.head_dim == 128 && kern::chain_ln_supported(d) &&
+         kern::chain_tc_supported(n, 3 * d, d) && kern::chain_tc_supported(n, 4 * d, d) &&
+         kern::chain_tc_supported(n, d, 4 * d) && kern::chain_tc_supported(1, c.vocab_size, d) &&
+         kern::chain_attn_supported(n, 0, c.n_heads, c.head_dim);
+}
+
 void Model::run(const int32_t* tokens, const int64_t* positions, int64_t n, KVBlock& kv, const uint8_t* mask,
                 const int32_t* block_ids, int64_t logit_rows) {
   BatchItem it{tokens, positions, n, &kv};
@@ -628,6 +653,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   if (n <= 0) return;
   for (int b = 0; b < B; ++b)
     if (items[b].n <= 0) throw Error(ErrorCode::ShapeMismatch, "batched forward: empty request");
+  if (!kv_prefix_.empty() && (B != 1 || mask || block_ids || !fused_attention_ok(n)))
+    throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix set for a forward that cannot read it in place");
   logit_rows = per_segment_logits ? (logit_rows > 0 ? B : 0) : std::min(logit_rows, n);
   forward_tokens.fetch_add(n, std::memory_order_relaxed);
   const auto& c = cfg_;
@@ -909,6 +936,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     // the next weights stream in as soon as each CTA's softmax is done)
     const bool fuse_attn = chain_attn && B == 1 && tc_attn && hd == 128 && !mask && !block_ids && !alibi &&
                            kern::chain_attn_supported(n, P, H, hd);
+    if (!kv_prefix_.empty() && (!fuse_attn || P < kv_prefix_rows_))
+      throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix set for a forward that cannot read it in place");
     kern::ChainStep steps[8];
     steps[0] = ln(W.h, n);
     steps[1] = mm(W.x, w_->wqkv[0], n, 3 * d, d, qkv_epi(0));
@@ -929,6 +958,14 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
         st.a_d = d;
         st.a_scratch = W.attn_scratch;
         st.a_scratch_bytes = W.attn_scratch_bytes;
+        if (!kv_prefix_.empty()) {  // cached modules read in place, then this request's rows
+          st.a_layer = l;
+          st.a_planes = 2 * c.n_layers;
+          for (const KVBlock* b : kv_prefix_)
+            st.a_seg[st.a_nseg++] = {b->data, b->cap, b->plane_bytes(), 0, b->rows};
+          st.a_seg[st.a_nseg++] = {kv.data, kv.cap, kv.plane_bytes(), kv_prefix_rows_, P + n - kv_prefix_rows_};
+          st.a_tail_vis = P - kv_prefix_rows_;
+        }
         steps[k++] = st;
       } else {
         attention(l);

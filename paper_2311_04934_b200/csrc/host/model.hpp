@@ -125,6 +125,13 @@ class Model {
   // The next run()/run_batch() waits for events[l] before layer l's attention (past K/V
   // rows still streaming in, e.g. the pinned-host tier); consumed by that call.
   void set_layer_events(const cudaEvent_t* events, int n) { layer_events_.assign(events, events + n); }
+  // Zero-copy cached prefix (engine serve): until cleared, a single-request forward treats
+  // the request cache's rows [0, sum of the blocks' rows) as these blocks' rows, read in
+  // place by the chain's attention phase (those cache rows are never filled).  Only valid
+  // while fused_attention_ok() holds for every forward of the request; run() throws otherwise.
+  void set_kv_prefix(const std::vector<const KVBlock*>& blocks);
+  void clear_kv_prefix() { kv_prefix_.clear(); kv_prefix_rows_ = 0; }
+  bool fused_attention_ok(int64_t n) const;  // n-token single-request forwards use the chain attention phase
   const float* device_logits() const;  // [logit_rows][vocab] after run()
   int32_t* device_argmax() const;      // scratch int32 slots
   void argmax_last(int64_t logit_rows);  // device argmax of each logits row -> device_argmax()
@@ -155,6 +162,7 @@ class Model {
   bool use_chain = true;         // few-token GEMM/LN segments as one persistent chain kernel (PCB_CHAIN=0: off)
   bool ln_fold = true;           // chain: LayerNorm folded into the neighbouring GEMMs (PCB_LN_FOLD=0: off)
   bool chain_attn = true;        // chain: a single request's attention as the chain's first phase (PCB_CHAIN_ATTN=0: off)
+  bool zero_copy = true;         // serve: cached modules read in place by the attention, no assembly copy (PCB_ZERO_COPY=0: off)
   int64_t launches = 0;          // kernels launched by run() (bench evidence)
 
  private:
@@ -170,6 +178,8 @@ class Model {
   int dl_ = 0, fl_ = 0, vl_ = 0;  // local attention width, MLP width, vocab rows
   std::shared_ptr<coll::Collective> comm_;
   std::vector<cudaEvent_t> layer_events_;
+  std::vector<const KVBlock*> kv_prefix_;
+  int64_t kv_prefix_rows_ = 0;
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Weights> w_;
   std::unique_ptr<Workspace> ws_;

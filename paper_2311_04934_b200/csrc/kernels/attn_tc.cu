@@ -456,7 +456,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, S::kTmemCols);
 }
 
+}  // namespace
+
 // 3-D bf16 map {cols, rows, planes} (plane stride in bytes), box {64, box_rows, 1}, SW128
+// (also the chain attention phase's in-place KV sources)
 CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t planes, uint64_t plane_stride,
                          uint32_t box_rows) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -479,6 +482,8 @@ CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
   return m;
 }
+
+namespace {
 
 unsigned long long* g_tlbuf = nullptr;
 int g_tl_ctas = 0;

@@ -46,6 +46,8 @@
 namespace pcb::kern {
 
 CUtensorMap tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t planes, uint64_t plane_stride,
+                         uint32_t box_rows);
 
 namespace {
 
@@ -76,11 +78,19 @@ struct PhaseDev {
   float ascale;  // log2(e) / sqrt(128)
   float* apart;
   __nv_bfloat16* aout;
+  // zero-copy prefix: segment s covers key blocks [a_first[s], a_first[s+1]), rows
+  // [a_row0[s], a_row0[s] + a_rows[s]) of its source (tensor map tkv[s], plane 2 layer + w);
+  // the last segment is the request's own rows (first a_tail_vis visible to all queries)
+  int a_nseg, a_layer, a_tail_vis;
+  int a_first[ChainStep::kMaxSeg + 1];
+  int a_row0[ChainStep::kMaxSeg];
+  int a_rows[ChainStep::kMaxSeg];
 };
 
 struct ChainParams {
   CUtensorMap tm[kMaxPhases];  // activation maps of the GEMM phases
   CUtensorMap tma[3];          // attention phase: Q [n][d], K and V planes [P + n][d]
+  CUtensorMap tkv[ChainStep::kMaxSeg];  // attention phase, zero-copy: {d, cap, planes} per KV source
   PhaseDev ph[kMaxPhases];
   int n_phases;
   int epoch0;
@@ -91,6 +101,8 @@ struct ChainParams {
   unsigned long long gbar_base;
   unsigned long long* tl;    // timeline probe [phase][cta][4] (null: off)
 };
+
+static_assert(sizeof(ChainParams) <= 32764, "chain kernel parameters exceed the 32 KB parameter space");
 
 // probe events per (phase, CTA): 0 X producer past the phase's barrier, 1 MMA took the
 // phase's last stage, 2 epilogue done with the phase, 3 W producer issued the phase's
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   auto attn_range = [&](const PhaseDev& A, int& h, int& sp, int& b0, int& nb) {
     h = c / A.aS;
     sp = c - h * A.aS;
-    const int64_t nblk = (A.aP + A.M + 63) / 64;
+    const int64_t nblk = A.a_nseg ? A.a_first[A.a_nseg] : (A.aP + A.M + 63) / 64;
     b0 = static_cast<int>(nblk * sp / A.aS);
     nb = static_cast<int>(nblk * (sp + 1) / A.aS) - b0;
   };
@@ -306,22 +318,35 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           int h, sp, b0, nb;
           attn_range(A, h, sp, b0, nb);
           tma_prefetch(&p.tma[0]);
-          tma_prefetch(&p.tma[1]);
-          tma_prefetch(&p.tma[2]);
+          if (A.a_nseg) {
+            for (int sgi = 0; sgi < A.a_nseg; ++sgi) tma_prefetch(&p.tkv[sgi]);
+          } else {
+            tma_prefetch(&p.tma[1]);
+            tma_prefetch(&p.tma[2]);
+          }
           pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
           mbar_expect_tx(a_qfull, 32768);
           for (int a = 0; a < 2; ++a)  // 64-row boxes: rows [0, 64) twice (dup) or [0, 128)
             for (int hh = 0; hh < 2; ++hh)
               tma_load_2d(aQ + a * 16384 + hh * 8192, &p.tma[0], a_qfull, h * 128 + a * 64, A.adup ? 0 : 64 * hh);
-          for (int it = 0; it < nb; ++it) {
+          for (int it = 0, sg = 0; it < nb; ++it) {
             const int s = it % AKV;
             mbar_wait(&a_kvempty[s], ((it / AKV) & 1) ^ 1);
             uint8_t* st = aKV + s * 32768;
-            const int j0 = (b0 + it) * 64;
+            const int b = b0 + it;
             mbar_expect_tx(&a_kvfull[s], 32768);
-            for (int a = 0; a < 2; ++a) {
-              tma_load_2d(st + a * 8192, &p.tma[1], &a_kvfull[s], h * 128 + a * 64, j0);
-              tma_load_2d(st + 16384 + a * 8192, &p.tma[2], &a_kvfull[s], h * 128 + a * 64, j0);
+            if (A.a_nseg) {
+              while (b >= A.a_first[sg + 1]) ++sg;
+              const int row = A.a_row0[sg] + (b - A.a_first[sg]) * 64;
+              for (int a = 0; a < 2; ++a) {
+                tma_load_3d(st + a * 8192, &p.tkv[sg], &a_kvfull[s], h * 128 + a * 64, row, 2 * A.a_layer);
+                tma_load_3d(st + 16384 + a * 8192, &p.tkv[sg], &a_kvfull[s], h * 128 + a * 64, row, 2 * A.a_layer + 1);
+              }
+            } else {
+              for (int a = 0; a < 2; ++a) {
+                tma_load_2d(st + a * 8192, &p.tma[1], &a_kvfull[s], h * 128 + a * 64, b * 64);
+                tma_load_2d(st + 16384 + a * 8192, &p.tma[2], &a_kvfull[s], h * 128 + a * 64, b * 64);
+              }
             }
           }
         }
@@ -471,15 +496,26 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         const int64_t n_ = P.M;
         const bool dup = P.adup;
         const int qi = dup ? (row & 63) : row;  // query of this lane
-        const int64_t limit = P.aP + qi;
         float m = -INFINITY, l = 0.f;
         const bool live = (dup ? ((q & 1) * 32) : (q * 32)) < n_;  // else the warp keeps the protocol only
         if (et == 0) ctl(p, ph, 0);
         auto blocks = [&](auto ncols) {
           constexpr int NC = decltype(ncols)::value;  // score columns per lane: 64, or 32 (dup)
           const int c0 = NC == 32 ? (row >> 6) * 32 : 0;
-          for (int it = 0; it < nb; ++it) {
-            const int64_t j0 = static_cast<int64_t>(b0 + it) * 64 + c0;
+          for (int it = 0, sg = 0; it < nb; ++it) {
+            // lim: last visible key of this block, relative to the block's first key.
+            // contiguous: key j visible iff j <= P + qi; zero-copy: a prefix segment's rows
+            // are all visible (its padding is not), the tail is visible up to tail_vis + qi
+            const int b = b0 + it;
+            int64_t lim;
+            if (P.a_nseg) {
+              while (b >= P.a_first[sg + 1]) ++sg;
+              const int64_t local = static_cast<int64_t>(b - P.a_first[sg]) * 64;
+              lim = sg == P.a_nseg - 1 ? P.a_tail_vis + qi - local : P.a_rows[sg] - 1 - local;
+            } else {
+              lim = P.aP + qi - static_cast<int64_t>(b) * 64;
+            }
+            lim -= c0;  // relative to this lane's first column
             if (!live) {
               if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);
               mbar_arrive(&a_pfull[it & 1]);
@@ -496,10 +532,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 #pragma unroll
               for (int x = 0; x < NC; ++x) sv[x] = __uint_as_float(raw[x]);
             }
-            if (j0 + NC - 1 > limit) {
+            if (NC - 1 > lim) {
 #pragma unroll
               for (int x = 0; x < NC; ++x)
-                if (j0 + x > limit) sv[x] = -INFINITY;
+                if (x > lim) sv[x] = -INFINITY;
             }
             float mx[8];
 #pragma unroll
@@ -983,7 +1019,11 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.aP = st.aP;
       d.aH = st.aH;
       d.a_d = st.a_d;
-      const int64_t nblk = (st.aP + st.M + 63) / 64;
+      int64_t nblk = (st.aP + st.M + 63) / 64;
+      if (st.a_nseg) {
+        nblk = 0;
+        for (int sgi = 0; sgi < st.a_nseg; ++sgi) nblk += (st.a_seg[sgi].rows + 63) / 64;
+      }
       d.aS = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({C / st.aH, nblk, 8})));  // <= 16 partials
       d.items = st.aH * d.aS;
       d.ascale = 1.4426950408889634f / sqrtf(128.f);
@@ -993,8 +1033,28 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
         throw std::runtime_error("chain: attention scratch too small");
       d.adup = st.M <= 64 && !std::getenv("PCB_CHAIN_ATTN_NODUP");
       p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 64);
-      p.tma[1] = tmap_bf16_2d(st.ak, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
-      p.tma[2] = tmap_bf16_2d(st.av, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
+      d.a_nseg = st.a_nseg;
+      if (st.a_nseg) {
+        if (st.a_nseg > ChainStep::kMaxSeg) throw std::runtime_error("chain: too many KV segments");
+        d.a_layer = st.a_layer;
+        d.a_tail_vis = static_cast<int>(st.a_tail_vis);
+        int64_t keys = 0;
+        d.a_first[0] = 0;
+        for (int sgi = 0; sgi < st.a_nseg; ++sgi) {
+          const ChainStep::KVSeg& g = st.a_seg[sgi];
+          if (g.rows <= 0 || g.row0 + g.rows > g.cap) throw std::runtime_error("chain: bad KV segment");
+          p.tkv[sgi] = tmap_bf16_3d(g.base, static_cast<uint64_t>(st.a_d), static_cast<uint64_t>(g.cap),
+                                    static_cast<uint64_t>(st.a_planes), g.plane_bytes, 64);
+          d.a_row0[sgi] = static_cast<int>(g.row0);
+          d.a_rows[sgi] = static_cast<int>(g.rows);
+          d.a_first[sgi + 1] = d.a_first[sgi] + static_cast<int>((g.rows + 63) / 64);
+          keys += g.rows;
+        }
+        if (keys != st.aP + st.M) throw std::runtime_error("chain: KV segments do not cover the keys");
+      } else {
+        p.tma[1] = tmap_bf16_2d(st.ak, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
+        p.tma[2] = tmap_bf16_2d(st.av, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
+      }
     } else {
       d.ln_src = st.ln_src;
       d.ln_dst = static_cast<__nv_bfloat16*>(st.ln_dst);

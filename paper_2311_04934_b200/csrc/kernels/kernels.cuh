@@ -140,6 +140,22 @@ struct ChainStep {
   int aH = 0, a_d = 0;
   float* a_scratch = nullptr;
   size_t a_scratch_bytes = 0;
+  // zero-copy prefix (a_nseg > 0): the keys are a_seg[0].rows, a_seg[1].rows, ... in order,
+  // each read in place from a KV block ([layer][K|V][cap][d] planes) -- the cached modules
+  // straight from the store -- and the last segment is the request cache's own rows, of
+  // which the first a_tail_vis are visible to every query and the rest causally (ak / av
+  // unused).  Replaces the KV assembly copy for a single request.
+  struct KVSeg {
+    const void* base = nullptr;
+    int64_t cap = 0;
+    size_t plane_bytes = 0;
+    int64_t row0 = 0, rows = 0;
+  };
+  static constexpr int kMaxSeg = 8;
+  int a_nseg = 0;
+  int a_layer = 0, a_planes = 0;
+  KVSeg a_seg[kMaxSeg];
+  int64_t a_tail_vis = 0;
 };
 // can a chain run this request's attention as its first phase (#SMs >= heads, hd 128)?
 bool chain_attn_supported(int64_t n, int64_t P, int H, int hd);

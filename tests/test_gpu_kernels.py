@@ -156,3 +156,27 @@ def test_chain_attention_repeated(m7):
                 first = r.first_token_logits
             else:
                 assert np.array_equal(first, r.first_token_logits)  # same prompt: bitwise repeatable
+
+
+@pytest.mark.parametrize("lens", [(4096,), (100, 37, 250), (64, 128, 1, 63)])
+def test_zero_copy_prefix(m7, lens):
+    """Cached modules read in place by the chain's attention phase (no assembly copy) vs the
+    assembled request cache: first-token logits and greedy continuation (decode steps extend
+    the request's own rows behind the in-place prefix).  Module lengths off the 64-row key
+    block exercise the per-segment padding masks."""
+    mods = "".join(f'<module name="m{i}">' + "".join(chr(97 + (i * 3 + j * 7) % 26) for j in range(n)) + "</module>"
+                   for i, n in enumerate(lens))
+    schema = pcb.Schema.parse(f'<schema name="zc{len(lens)}">Intro. {mods}</schema>')
+    store = pcb.ModuleStore(m7)
+    store.encode_schema(schema)
+    imports = "".join(f"<m{i}/>" for i in range(len(lens)))
+    prompt = f'<prompt schema="zc{len(lens)}">{imports}Now answer the question in detail.</prompt>'
+    out = {}
+    for zc in (1, 0):
+        m7.set_option("zero_copy", zc)
+        r = pcb.serve(store, schema, prompt, 6)
+        out[zc] = (r.first_token_logits, list(r.output_tokens), r.timings["assemble_us"])
+    m7.set_option("zero_copy", 1)
+    assert rel(out[1][0], out[0][0]) <= BF16_REL
+    assert same_greedy_token(out[1][0], out[0][0])
+    assert out[1][1][:3] == out[0][1][:3]

@@ -31,10 +31,11 @@ def dump():
 
 
 VARIANTS = [
-    ("per-GEMM kernels", {"chain": 0}),
-    ("chain", {"chain": 1, "ln_fold": 1, "chain_attn": 0}),
-    ("chain+attn", {"chain": 1, "ln_fold": 1, "chain_attn": 1}),
-    ("chain, LN phases", {"chain": 1, "ln_fold": 0, "chain_attn": 0}),
+    ("per-GEMM kernels", {"chain": 0, "zero_copy": 0}),
+    ("chain", {"chain": 1, "ln_fold": 1, "chain_attn": 0, "zero_copy": 0}),
+    ("chain+attn", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 0}),
+    ("zero-copy", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 1}),
+    ("chain, LN phases", {"chain": 1, "ln_fold": 0, "chain_attn": 0, "zero_copy": 0}),
 
 ]
 if os.environ.get("AB_VARIANTS"):
@@ -67,6 +68,7 @@ for name, v in res.items():
 m.set_option("chain", 1)
 m.set_option("ln_fold", int(os.environ.get("TL_FOLD", "1")))
 m.set_option("chain_attn", int(os.environ.get("TL_ATTN", "1")))
+m.set_option("zero_copy", int(os.environ.get("TL_ZC", "1")))
 pcb.serve(st, s, parsed[0], max_new_tokens=1)
 m.sync()
 dump()
