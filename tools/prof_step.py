@@ -16,6 +16,7 @@ layers = int(os.environ.get("PROF_LAYERS", "32"))
 cfg = dict(bench.CFG_7B, n_layers=layers)
 schema_text, prompts = bench.workload(4096, 64, 1)
 m = pcb.Model(cfg, dtype=pcb.BF16)
+m.set_option("zero_copy", int(os.environ.get("PROF_ZC", "1")))  # 0: requests assemble (copy) their cache
 s = pcb.Schema.parse(schema_text)
 st = pcb.ModuleStore(m)
 st.encode_schema(s)

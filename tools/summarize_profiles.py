@@ -56,9 +56,13 @@ def main(tag):
     os.makedirs(dst, exist_ok=True)
     k = read_launches(os.path.join(src, "launches.csv"))
     ids = sorted(k)
-    last_arg = max(i for i in ids if "k_argmax" in k[i]["name"])
-    first_asm = max(i for i in ids if "k_assemble" in k[i]["name"] and i < last_arg)
-    step = [i for i in ids if first_asm <= i <= last_arg]
+    # the measured request: every launch after the previous request's argmax up to its own
+    # (it starts with the assembly copy, or -- zero-copy -- with the embedding)
+    args = [i for i in ids if "k_argmax" in k[i]["name"]]
+    last_arg = args[-1]
+    prev_arg = args[-2] if len(args) > 1 else -1
+    step = [i for i in ids if prev_arg < i <= last_arg]
+    first_asm = step[0]
     with open(os.path.join(dst, f"{tag}_launches.csv"), "w") as f:
         w = csv.writer(f)
         w.writerow(["launch", "kernel", "gpu_time_us", "dram_read_bytes", "dram_write_bytes"])
