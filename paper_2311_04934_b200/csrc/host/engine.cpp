@@ -485,20 +485,27 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
   const layout::LayoutPlan& plan = schema.plan;
   micro_batch = std::max(1, std::min(micro_batch, 1024));
   std::vector<ServeResponse> out(reqs.size());
-  for (size_t b0 = 0; b0 < reqs.size(); b0 += micro_batch) {
-    auto t0 = Clock::now();
-    const size_t b1 = std::min(reqs.size(), b0 + micro_batch);
-    struct Item {
-      size_t idx;
-      std::vector<cache::EntryPtr> sel;
-      UncachedPass up;
-      int64_t n_cached = 0;
-    };
+  struct Item {
+    size_t idx;
+    std::vector<cache::EntryPtr> sel;
+    UncachedPass up;
+    int64_t n_cached = 0;
+  };
+  struct Batch {
+    Clock::time_point t0;
     std::vector<Item> items;
+  };
+  cudaEvent_t segs_busy = nullptr;  // the last launch's assembly segment list, until its H2D ran
+  // host side of micro-batch [b0, b1): resolve, store lookups (misses encode), uncached passes
+  auto prep = [&](size_t b0) {
+    Batch bt;
+    bt.t0 = Clock::now();
+    const size_t b1 = std::min(reqs.size(), b0 + micro_batch);
     for (size_t i = b0; i < b1; ++i) {
       const ServeRequest& req = reqs[i];
       // decode past the first token, baselines and scaffolds take the single-request path
       if (!req.use_cache || req.use_scaffolds || req.max_new_tokens != 1) {
+        if (segs_busy) CK(cudaEventSynchronize(segs_busy));  // serve() reuses the segment list
         out[i] = serve(req, schema, store);
         continue;
       }
@@ -507,7 +514,7 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
       Item it;
       it.idx = i;
       ServeResponse& resp = out[i];
-      resp.timings.parse_us = us_since(t0);
+      resp.timings.parse_us = us_since(bt.t0);
       for (const std::string& name : resolved.cached_imports) {
         cache::EntryPtr e = store.lookup(schema.doc.name, name);
         const layout::ModuleLayout& ml = plan.at(name);
@@ -527,16 +534,56 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
       }
       it.up = build_uncached(resolved, plan, true);
       resp.cache_report.uncached_token_count = it.up.prompt_token_count;
-      items.push_back(std::move(it));
+      bt.items.push_back(std::move(it));
     }
-    if (items.empty()) continue;
+    return bt;
+  };
+  // Per-slot host buffers and events: micro-batch k+1 is launched (queued behind k on the
+  // stream) before k's results are collected, so the device never waits for the host's
+  // resolve/lookup of the next micro-batch (it did: ~20% idle per 32-request micro-batch).
+  struct Slot {
+    float* h_logits = nullptr;
+    int32_t* h_tok = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev[3] = {};
+    cudaEvent_t segs_used = nullptr;  // the assembly's segment list left host memory
+    cudaEvent_t done = nullptr;       // logits and tokens are in this slot's host buffers
+  };
+  Slot slots[2];
+  auto free_slots = [&]() {
+    for (Slot& sl : slots) {
+      if (sl.h_logits) cudaFreeHost(sl.h_logits);
+      if (sl.h_tok) cudaFreeHost(sl.h_tok);
+      for (auto& e : sl.ev)
+        if (e) cudaEventDestroy(e);
+      if (sl.segs_used) cudaEventDestroy(sl.segs_used);
+      if (sl.done) cudaEventDestroy(sl.done);
+    }
+  };
+  AsmScratch& sc = scratch_of(store);
+  sc.ensure(0, 0, V);
+  auto launch = [&](Batch& bt, Slot& sl) {
+    const size_t B = bt.items.size();
+    if (sl.cap < B) {
+      if (sl.h_logits) cudaFreeHost(sl.h_logits);
+      if (sl.h_tok) cudaFreeHost(sl.h_tok);
+      CK(cudaMallocHost(&sl.h_logits, B * V * sizeof(float)));
+      CK(cudaMallocHost(&sl.h_tok, B * sizeof(int32_t)));
+      sl.cap = B;
+    }
+    if (!sl.ev[0]) {
+      for (auto& e : sl.ev) CK(cudaEventCreate(&e));
+      CK(cudaEventCreateWithFlags(&sl.segs_used, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
     // one request cache per item, equal capacity (run_batch addresses them by offset)
     int64_t cap = 0;
-    for (auto& it : items) cap = std::max<int64_t>(cap, it.n_cached + static_cast<int64_t>(it.up.tokens.size()));
-    if (store.batch_arenas.size() < items.size() || (!store.batch_arenas.empty() && store.batch_arenas[0]->cap < cap)) {
+    for (auto& it : bt.items) cap = std::max<int64_t>(cap, it.n_cached + static_cast<int64_t>(it.up.tokens.size()));
+    if (store.batch_arenas.size() < B || (!store.batch_arenas.empty() && store.batch_arenas[0]->cap < cap)) {
       // one allocation, request caches at a uniform stride (one batched attention launch)
       const int64_t c = std::max<int64_t>(cap, store.batch_arenas.empty() ? 64 : store.batch_arenas[0]->cap);
-      const size_t nreq = std::max<size_t>(items.size(), micro_batch);
+      const size_t nreq = std::max<size_t>(B, micro_batch);
+      CK(cudaStreamSynchronize(m.stream()));  // the previous micro-batch still reads the old arenas
       store.batch_arenas.clear();
       store.batch_raw.reset();
       model::KVPtr probe = m.alloc_kv(0);
@@ -555,45 +602,96 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
         store.batch_arenas.push_back(v);
       }
     }
-    AsmScratch& sc = scratch_of(store);
-    sc.ensure(0, 0, static_cast<int64_t>(V) * items.size());
-    CK(cudaEventRecord(sc.ev[0], m.stream()));
+    if (segs_busy) CK(cudaEventSynchronize(segs_busy));  // sc's pinned segment list is reused
+    // zero-copy micro-batch: every request's modules read in place by the batched attention
+    // (device-resident blocks, <= 15 per request, <= 128 suffix tokens); else one assembly launch
+    bool zc = B > 1 && m.batched_zero_copy_ok();
+    for (auto& it : bt.items) {
+      zc = zc && static_cast<int>(it.sel.size()) < kern::kAttnMaxSeg && it.up.tokens.size() <= 128;
+      for (auto& e : it.sel) zc = zc && !e->kv->host;
+    }
+    CK(cudaEventRecord(sl.ev[0], m.stream()));
     int n_segs = 0;
     std::vector<model::Model::BatchItem> bi;
-    for (size_t k = 0; k < items.size(); ++k) {
+    std::vector<std::vector<const model::KVBlock*>> prefixes;
+    for (size_t k = 0; k < B; ++k) {
       model::KVBlock& a = *store.batch_arenas[k];
       a.rows = 0;
       a.positions.clear();
-      append_segments(m, items[k].sel, a, sc, n_segs);
-      bi.push_back({items[k].up.tokens.data(), items[k].up.positions.data(),
-                    static_cast<int64_t>(items[k].up.tokens.size()), &a});
+      if (zc) {
+        std::vector<const model::KVBlock*> blocks;
+        for (auto& e : bt.items[k].sel) {
+          blocks.push_back(e->kv.get());
+          a.positions.insert(a.positions.end(), e->kv->positions.begin(), e->kv->positions.end());
+          a.rows += e->kv->rows;  // logical rows: the blocks, read in place
+        }
+        prefixes.push_back(std::move(blocks));
+      } else {
+        append_segments(m, bt.items[k].sel, a, sc, n_segs);
+      }
+      bi.push_back({bt.items[k].up.tokens.data(), bt.items[k].up.positions.data(),
+                    static_cast<int64_t>(bt.items[k].up.tokens.size()), &a});
     }
     launch_segments(m, sc, n_segs);
+    CK(cudaEventRecord(sl.segs_used, m.stream()));
+    segs_busy = sl.segs_used;
     launch_slow(m, sc);
-    CK(cudaEventRecord(sc.ev[1], m.stream()));
-    m.run_batch(bi, true);
-    const int B = static_cast<int>(items.size());
-    m.argmax_last(B);
-    CK(cudaEventRecord(sc.ev[2], m.stream()));
-    CK(cudaMemcpyAsync(sc.h_logits, m.device_logits(), static_cast<size_t>(B) * V * 4, cudaMemcpyDeviceToHost,
-                       m.stream()));
-    CK(cudaMemcpyAsync(sc.h_tok, m.device_argmax(), B * 4, cudaMemcpyDeviceToHost, m.stream()));
-    CK(cudaStreamSynchronize(m.stream()));
+    CK(cudaEventRecord(sl.ev[1], m.stream()));
+    if (zc) {
+      m.set_kv_prefix_batch(prefixes);
+      try {
+        m.run_batch(bi, true);
+      } catch (...) {
+        m.clear_kv_prefix();
+        throw;
+      }
+      m.clear_kv_prefix();
+    } else {
+      m.run_batch(bi, true);
+    }
+    m.argmax_last(static_cast<int64_t>(B));
+    CK(cudaEventRecord(sl.ev[2], m.stream()));
+    CK(cudaMemcpyAsync(sl.h_logits, m.device_logits(), B * V * sizeof(float), cudaMemcpyDeviceToHost, m.stream()));
+    CK(cudaMemcpyAsync(sl.h_tok, m.device_argmax(), B * sizeof(int32_t), cudaMemcpyDeviceToHost, m.stream()));
+    CK(cudaEventRecord(sl.done, m.stream()));
+  };
+  auto finish = [&](Batch& bt, Slot& sl) {
+    CK(cudaEventSynchronize(sl.done));
     float ms_asm = 0, ms_pre = 0;
-    CK(cudaEventElapsedTime(&ms_asm, sc.ev[0], sc.ev[1]));
-    CK(cudaEventElapsedTime(&ms_pre, sc.ev[1], sc.ev[2]));
-    const double ttft = us_since(t0);
-    for (int k = 0; k < B; ++k) {
-      ServeResponse& resp = out[items[k].idx];
-      resp.first_token_logits.assign(sc.h_logits + static_cast<size_t>(k) * V, sc.h_logits + static_cast<size_t>(k + 1) * V);
-      resp.output_tokens.push_back(sc.h_tok[k]);
+    CK(cudaEventElapsedTime(&ms_asm, sl.ev[0], sl.ev[1]));
+    CK(cudaEventElapsedTime(&ms_pre, sl.ev[1], sl.ev[2]));
+    const double ttft = us_since(bt.t0);
+    for (size_t k = 0; k < bt.items.size(); ++k) {
+      ServeResponse& resp = out[bt.items[k].idx];
+      resp.first_token_logits.assign(sl.h_logits + k * V, sl.h_logits + (k + 1) * V);
+      resp.output_tokens.push_back(sl.h_tok[k]);
       resp.output_text = pml::tok::detokenize(resp.output_tokens);
       resp.timings.assemble_us = ms_asm * 1000.0;
       resp.timings.prefill_device_us = ms_pre * 1000.0;
       resp.timings.uncached_prefill_us = ms_pre * 1000.0;
       resp.timings.ttft_us = ttft;
     }
+  };
+  try {
+    Batch cur = prep(0);
+    int slot = 0;
+    if (!cur.items.empty()) launch(cur, slots[slot]);
+    for (size_t b0 = 0; b0 < reqs.size(); b0 += micro_batch) {
+      Batch nxt;
+      if (b0 + micro_batch < reqs.size()) {
+        nxt = prep(b0 + micro_batch);
+        if (!nxt.items.empty()) launch(nxt, slots[slot ^ 1]);
+      }
+      if (!cur.items.empty()) finish(cur, slots[slot]);
+      cur = std::move(nxt);
+      slot ^= 1;
+    }
+  } catch (...) {
+    cudaStreamSynchronize(m.stream());
+    free_slots();
+    throw;
   }
+  free_slots();
   return out;
 }
 

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "../kernels/kernels.cuh"
@@ -145,6 +146,11 @@ struct Workspace {
   float *part = nullptr, *logits_loc = nullptr, *logits_gath = nullptr;  // tensor parallel
   float* lnstats = nullptr;  // LN fold: [hidden/128 tiles][cap_n][2]
   float2* rope_tab = nullptr;  // [rope_half + 1][rope_ld] {cos, sin} per (pair, token), few-token forwards
+  // batched zero-copy attention tables: one device blob [maps (128 B each)][segs int4 [B][16]][segn int2 [B]]
+  char* segblob = nullptr;
+  size_t segblob_cap = 0;
+  char* seg_host = nullptr;  // pinned staging of the blob
+  cudaEvent_t seg_ev = nullptr;  // the staging's last H2D ran
   int rope_half = 0;
   int64_t rope_ld = 0;
   int tp = 1, Vl = 0;
@@ -166,7 +172,7 @@ struct Workspace {
                     (void*)req,
                     (void*)mask, (void*)h, x, q,
                     attn, mid, (void*)logits, (void*)part, (void*)logits_loc, (void*)logits_gath, (void*)lnstats,
-                    (void*)rope_tab, (void*)gemm_ws,
+                    (void*)rope_tab, (void*)segblob, (void*)gemm_ws,
                     (void*)counters, (void*)attn_scratch})
       if (p) cudaFree(p);
     for (auto& e : staged)
@@ -175,6 +181,8 @@ struct Workspace {
         cudaEventDestroy(e);
       }
     if (host_ints) cudaFreeHost(host_ints);
+    if (seg_host) cudaFreeHost(seg_host);
+    if (seg_ev) cudaEventDestroy(seg_ev);
   }
   template <typename T>
   static void regrow(T*& p, size_t bytes) {
@@ -604,6 +612,31 @@ void Model::set_kv_prefix(const std::vector<const KVBlock*>& blocks) {
   }
 }
 
+void Model::set_kv_prefix_batch(const std::vector<std::vector<const KVBlock*>>& per_request) {
+  kv_prefix_batch_.clear();
+  for (const auto& blocks : per_request) {
+    if (static_cast<int>(blocks.size()) + 1 > kern::kAttnMaxSeg)
+      throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix: too many blocks");
+    std::vector<const KVBlock*> keep;
+    for (const KVBlock* b : blocks) {
+      if (b->host || b->dtype != dtype_ || b->hidden != cfg_.hidden || b->n_layers != cfg_.n_layers)
+        throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix: block must be a device block of this model");
+      if (b->rows) keep.push_back(b);
+    }
+    kv_prefix_batch_.push_back(std::move(keep));
+  }
+}
+
+bool Model::batched_zero_copy_ok() const {
+  const auto& c = cfg_;
+  kern::AttnArgs a;
+  a.hd = c.head_dim;
+  a.d = c.hidden;
+  a.n = 1;
+  return zero_copy && tp_size_ == 1 && dtype_ == BF16 && !force_simt && !force_simt_attn &&
+         c.pos_encoding != PosEncoding::Alibi && kern::attention_tc_supported(a);
+}
+
 bool Model::fused_attention_ok(int64_t n) const {
   const auto& c = cfg_;
   const int d = c.hidden;
@@ -655,6 +688,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     if (items[b].n <= 0) throw Error(ErrorCode::ShapeMismatch, "batched forward: empty request");
   if (!kv_prefix_.empty() && (B != 1 || mask || block_ids || !fused_attention_ok(n)))
     throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix set for a forward that cannot read it in place");
+  if (!kv_prefix_batch_.empty() && (static_cast<int>(kv_prefix_batch_.size()) != B || B < 2 || !batched_zero_copy_ok()))
+    throw Error(ErrorCode::ShapeMismatch, "zero-copy batch prefixes do not match this forward");
   logit_rows = per_segment_logits ? (logit_rows > 0 ? B : 0) : std::min(logit_rows, n);
   forward_tokens.fetch_add(n, std::memory_order_relaxed);
   const auto& c = cfg_;
@@ -822,6 +857,66 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       max_nb = std::max(max_nb, items[b].n);
     }
   }
+  // zero-copy micro-batch: per-request segment tables for the batched attention kernel --
+  // each request's module blocks read in place, then its own rows in the batch arena (one
+  // 3-D map over all request caches, plane = request * 2L + 2 layer + K/V)
+  int64_t seg_max_blocks = 0;
+  const int4* d_segs = nullptr;
+  const int2* d_segn = nullptr;
+  const void* d_maps = nullptr;
+  if (!kv_prefix_batch_.empty()) {
+    if (!batched_attn) throw Error(ErrorCode::ShapeMismatch, "zero-copy batch needs request caches at a uniform stride");
+    const int L2 = 2 * c.n_layers;
+    const KVBlock& a0 = *items[0].kv;
+    if (req_stride != static_cast<int64_t>(a0.plane_bytes()) * L2)
+      throw Error(ErrorCode::ShapeMismatch, "zero-copy batch: request caches must be contiguous blocks");
+    std::vector<CUtensorMap> maps;
+    std::map<const void*, int> map_of;
+    maps.push_back(kern::tmap_bf16_3d(a0.data, d, a0.cap, static_cast<uint64_t>(L2) * B, a0.plane_bytes(), 64));
+    std::vector<int4> tab(static_cast<size_t>(B) * kern::kAttnMaxSeg, make_int4(0, 0, 0, 0));
+    std::vector<int2> segn(B);
+    for (int b = 0; b < B; ++b) {
+      int g = 0;
+      int64_t pre = 0, blocks = 0;
+      for (const KVBlock* blk : kv_prefix_batch_[b]) {
+        auto it = map_of.find(blk->data);
+        if (it == map_of.end()) {
+          it = map_of.emplace(blk->data, static_cast<int>(maps.size())).first;
+          maps.push_back(kern::tmap_bf16_3d(blk->data, d, blk->cap, L2, blk->plane_bytes(), 64));
+        }
+        tab[b * kern::kAttnMaxSeg + g++] = make_int4(it->second, 0, static_cast<int>(blk->rows), 0);
+        pre += blk->rows;
+        blocks += (blk->rows + 63) / 64;
+      }
+      const int64_t Pb = items[b].kv->rows, nb = items[b].n;
+      if (pre > Pb) throw Error(ErrorCode::ShapeMismatch, "zero-copy batch: prefix longer than the cache");
+      tab[b * kern::kAttnMaxSeg + g++] =
+          make_int4(0, static_cast<int>(pre), static_cast<int>(Pb + nb - pre), b * L2);
+      blocks += (Pb + nb - pre + 63) / 64;
+      segn[b] = make_int2(g, static_cast<int>(Pb - pre));
+      seg_max_blocks = std::max(seg_max_blocks, blocks);
+    }
+    const size_t mb = maps.size() * sizeof(CUtensorMap), tb = tab.size() * sizeof(int4), nbb = segn.size() * sizeof(int2);
+    const size_t need = mb + tb + nbb;
+    if (W.seg_ev) CK(cudaEventSynchronize(W.seg_ev));  // the pinned staging's previous H2D ran
+    else CK(cudaEventCreateWithFlags(&W.seg_ev, cudaEventDisableTiming));
+    if (need > W.segblob_cap) {
+      CK(cudaStreamSynchronize(s));
+      if (W.segblob) cudaFree(W.segblob);
+      if (W.seg_host) cudaFreeHost(W.seg_host);
+      W.segblob_cap = std::max<size_t>(need * 2, 64 << 10);
+      CK(cudaMalloc(reinterpret_cast<void**>(&W.segblob), W.segblob_cap));
+      CK(cudaMallocHost(reinterpret_cast<void**>(&W.seg_host), W.segblob_cap));
+    }
+    std::memcpy(W.seg_host, maps.data(), mb);
+    std::memcpy(W.seg_host + mb, tab.data(), tb);
+    std::memcpy(W.seg_host + mb + tb, segn.data(), nbb);
+    CK(cudaMemcpyAsync(W.segblob, W.seg_host, need, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(W.seg_ev, s));
+    d_maps = W.segblob;
+    d_segs = reinterpret_cast<const int4*>(W.segblob + mb);
+    d_segn = reinterpret_cast<const int2*>(W.segblob + mb + tb);
+  }
   std::vector<cudaEvent_t> layer_ev;
   layer_ev.swap(layer_events_);  // consumed by this call
   auto attention = [&](int l) {
@@ -838,6 +933,13 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       ab.kv_cap = kv.cap;
       ab.max_P = max_P;
       ab.max_n = max_nb;
+      if (d_segs) {
+        ab.segs = d_segs;
+        ab.segn = d_segn;
+        ab.maps = d_maps;
+        ab.layer = l;
+        ab.max_blocks = seg_max_blocks;
+      }
       double bytes = 0, flops = 0;
       for (int b = 0; b < B; ++b) {
         const int64_t nb = items[b].n, Pb = items[b].kv->rows;

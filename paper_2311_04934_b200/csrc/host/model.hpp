@@ -130,7 +130,11 @@ class Model {
   // place by the chain's attention phase (those cache rows are never filled).  Only valid
   // while fused_attention_ok() holds for every forward of the request; run() throws otherwise.
   void set_kv_prefix(const std::vector<const KVBlock*>& blocks);
-  void clear_kv_prefix() { kv_prefix_.clear(); kv_prefix_rows_ = 0; }
+  void clear_kv_prefix() { kv_prefix_.clear(); kv_prefix_rows_ = 0; kv_prefix_batch_.clear(); }
+  // the same for run_batch: request b's cache rows [0, its blocks' rows) are its blocks
+  // (batched attention kernel, per-request segment tables); needs batched_zero_copy_ok()
+  void set_kv_prefix_batch(const std::vector<std::vector<const KVBlock*>>& per_request);
+  bool batched_zero_copy_ok() const;
   bool fused_attention_ok(int64_t n) const;  // n-token single-request forwards use the chain attention phase
   const float* device_logits() const;  // [logit_rows][vocab] after run()
   int32_t* device_argmax() const;      // scratch int32 slots
@@ -179,6 +183,7 @@ class Model {
   std::shared_ptr<coll::Collective> comm_;
   std::vector<cudaEvent_t> layer_events_;
   std::vector<const KVBlock*> kv_prefix_;
+  std::vector<std::vector<const KVBlock*>> kv_prefix_batch_;
   int64_t kv_prefix_rows_ = 0;
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Weights> w_;

@@ -32,6 +32,7 @@ constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 #define PCB_ATTN_STAGES 6
 #endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: stale max tolerated up to 2^8
+constexpr int kSeg = 16;                    // K/V segments per request (zero-copy batched mode)
 
 template <int HD>
 struct AttnSmem {
@@ -62,6 +63,14 @@ struct AttnParams {
   // batched requests (one launch for a micro-batch): blockIdx.x = request, per request
   // {first q row, n, P}; K/V come from a 3-D tensor map {d, rows, request}
   const int4* req = nullptr;
+  // batched zero-copy: request r's keys are segments segs[r][0 .. segn[r].x) = {map, row0,
+  // rows, zbase} read in place through maps[map] (3-D {d, cap, planes}, plane zbase + 2 layer
+  // + K/V); the last segment is the request's own rows, the first segn[r].y of them visible
+  // to every query, the rest causal
+  const int4* segs = nullptr;
+  const int2* segn = nullptr;
+  const CUtensorMap* maps = nullptr;
+  int layer = 0;
   unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
   unsigned long long* tl = nullptr;   // per-CTA phase timeline [cta][8] (PCB_ATTN_TL)
 };
@@ -141,7 +150,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int64_t total_ = P_ + n_;
   const int64_t q0 = static_cast<int64_t>(q_tile) * BQ;
   const int64_t key_end = min(total_, P_ + q0 + BQ);  // causal key range of this tile
-  const int64_t nblk = (key_end + BKV - 1) / BKV;
+  // zero-copy segment table of this request (read by every role; small, from L2)
+  int* seg_first = reinterpret_cast<int*>(tmem_slot + 16);  // [kSeg + 1] first key block per segment
+  int nseg = 0, tail_vis = 0;
+  if (p.segs) {
+    const int2 sn = p.segn[breq];
+    nseg = sn.x;
+    tail_vis = sn.y;
+    if (threadIdx.x == 0) {
+      int f = 0;
+      for (int g = 0; g < nseg; ++g) {
+        seg_first[g] = f;
+        f += (p.segs[breq * kSeg + g].z + BKV - 1) / BKV;
+      }
+      seg_first[nseg] = f;
+    }
+    __syncthreads();
+  }
+  const int64_t nblk = p.segs ? seg_first[nseg] : (key_end + BKV - 1) / BKV;
   const int64_t b0 = nblk * split / p.splits, b1 = nblk * (split + 1) / p.splits;
   const int nb = static_cast<int>(b1 - b0);
 
@@ -177,10 +203,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0) {
     if (elect_one() && nb > 0) {
+      // maps written by the host between launches: acquire them for the async proxy
+      for (int g = 0; g < nseg; ++g)
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.maps + p.segs[breq * kSeg + g].x)
+                     : "memory");
       mbar_expect_tx(q_full, S::kQ);
       for (int a = 0; a < S::kAtoms; ++a)
         tma_load_2d(sQ + a * (BQ * 128), &tmQ, q_full, h * HD + a * 64, static_cast<int>(qrow0 + q0));
-      for (int it = 0; it < nb; ++it) {
+      for (int it = 0, sg = 0; it < nb; ++it) {
         const int s = it % KV_STAGES;
         mbar_wait(&kv_empty[s], ((it / KV_STAGES) & 1) ^ 1);
         probe(p, 4, it);
@@ -191,6 +221,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // head-major cache [H][rows][hd]:     x = a*64,        y = h*rows + key row
         const int kx = p.kv_head_major ? 0 : h * HD;
         const int ky = p.kv_head_major ? static_cast<int>(h * p.kv_rows + j0) : j0;
+        if (p.segs) {
+          const int b = static_cast<int>(b0) + it;
+          while (b >= seg_first[sg + 1]) ++sg;
+          const int4 g = p.segs[breq * kSeg + sg];  // {map, row0, rows, zbase}
+          const CUtensorMap* mp = p.maps + g.x;
+          const int row = g.y + (b - seg_first[sg]) * BKV, z = g.w + 2 * p.layer;
+          for (int a = 0; a < S::kAtoms; ++a) {
+            tma_load_3d(st + a * (BKV * 128), mp, &kv_full[s], kx + a * 64, row, z);
+            tma_load_3d(st + S::kKV + a * (BKV * 128), mp, &kv_full[s], kx + a * 64, row, z + 1);
+          }
+          continue;
+        }
         for (int a = 0; a < S::kAtoms; ++a) {
           if (p.req) {
             tma_load_3d(st + a * (BKV * 128), &tmK, &kv_full[s], kx + a * 64, ky, breq);
@@ -255,8 +297,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // a warp whose 32 query rows are all past n (the suffix fills half a 128-row tile)
     // only keeps the barrier protocol: its P rows feed O rows nobody reads
     const bool live = q0 + qd * 32 < n_;
-    for (int it = 0; it < nb; ++it) {
-      const int64_t j0 = (b0 + it) * BKV;
+    for (int it = 0, sg = 0; it < nb; ++it) {
+      int64_t j0 = (b0 + it) * BKV, lim_seg = 0;
+      if (p.segs) {  // zero-copy: mask per segment (module padding rows; causal tail)
+        const int b = static_cast<int>(b0) + it;
+        while (b >= seg_first[sg + 1]) ++sg;
+        const int64_t local = static_cast<int64_t>(b - seg_first[sg]) * BKV;
+        lim_seg = sg == nseg - 1 ? tail_vis + qi - local : p.segs[breq * kSeg + sg].z - 1 - local;
+        j0 = limit - lim_seg;  // so that key c is masked iff c > lim_seg, as below
+      }
       if (!live) {
         // p_full[it&1]'s previous phase (block it-2) completed before PV(it-2) was issued
         if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
@@ -278,7 +327,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (threadIdx.x == 128) probe(p, 6, it);
       // scores stay raw (unscaled); the 1/sqrt(hd) * log2(e) factor is folded into
       // one FFMA per element in front of ex2.approx
-      if (j0 + BKV - 1 > limit) {  // diagonal block only
+      if (j0 + BKV - 1 > limit) {  // diagonal block (or a segment's padding) only
 #pragma unroll
         for (int c = 0; c < BKV; ++c)
           if (j0 + c > limit) sv[c] = -INFINITY;
@@ -512,7 +561,8 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   p.out = static_cast<__nv_bfloat16*>(a.out);
   const bool batched = a.n_req > 0;  // one launch over the requests of a micro-batch
   const int q_tiles = batched ? a.n_req : static_cast<int>((a.n + BQ - 1) / BQ);
-  const int64_t nblk0 = batched ? (a.max_P + a.max_n + BKV - 1) / BKV
+  const int64_t nblk0 = a.segs ? a.max_blocks
+                      : batched ? (a.max_P + a.max_n + BKV - 1) / BKV
                                 : (std::min<int64_t>(p.total, a.P + BQ) + BKV - 1) / BKV;  // tile 0 key blocks
   // one CTA per SM; for single-tile (suffix) launches pick the split count that
   // minimises waves x blocks per CTA (+ a per-split fixed cost)
@@ -554,7 +604,15 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
     p.dbg = dbg;
   }
   CUtensorMap tk, tv;
-  if (batched) {
+  if (a.segs) {  // K/V through the per-segment maps in global memory
+    p.req = a.req;
+    p.segs = a.segs;
+    p.segn = a.segn;
+    p.maps = static_cast<const CUtensorMap*>(a.maps);
+    p.layer = a.layer;
+    tk = tq;
+    tv = tq;
+  } else if (batched) {
     // request r's cache rows: {d, rows, request} with the request stride between planes
     p.req = a.req;
     tk = tmap_bf16_3d(a.k, a.d, a.kv_cap, a.n_req, a.req_stride, BKV);

@@ -10,6 +10,7 @@
 //   residual  fp32 [n][d]; activations in the model dtype.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -191,7 +192,19 @@ struct AttnArgs {
   const int4* req = nullptr;
   int n_req = 0;
   int64_t req_stride = 0, kv_cap = 0, max_P = 0, max_n = 0;
+  // batched zero-copy (k/v unused): per request <= 16 segments {map, row0, rows, zbase}
+  // (segs [n_req][16] int4, segn [n_req] {count, tail visible rows}) over the global
+  // CUtensorMap array maps; layer selects plane zbase + 2 layer (+1 for V)
+  const int4* segs = nullptr;
+  const int2* segn = nullptr;
+  const void* maps = nullptr;
+  int layer = 0;
+  int64_t max_blocks = 0;  // longest request's key blocks (with per-segment padding)
 };
+constexpr int kAttnMaxSeg = 16;
+// 3-D bf16 TMA map {cols, rows, planes} (plane stride in bytes), box {64, box_rows, 1}, SW128
+CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t planes, uint64_t plane_stride,
+                         uint32_t box_rows);
 void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s);
 size_t attention_simt_scratch(const AttnArgs& a);
 bool attention_tc_supported(const AttnArgs& a);

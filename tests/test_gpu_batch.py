@@ -8,7 +8,7 @@ import pytest
 
 import bench
 import paper_2311_04934_b200 as pcb
-from oracle.oracle import TINY
+from oracle.oracle import C1, TINY
 from tests.util import BF16_REL, F32_TOL, rel, same_greedy_token
 
 pytestmark = pytest.mark.gpu
@@ -65,3 +65,28 @@ def test_batch_7b_shape(m7, mb):
     # micro-batch 2 -> 128 suffix rows (chain kernel), 4 -> 256 rows (stream-K tcgen05 GEMMs)
     schema, prompts, _ = bench.workload_c4(16, 256, 6, 8, 64)
     check(m7, schema, prompts, micro_batch=mb, is32=False)
+
+
+@pytest.mark.parametrize("cfg,mod_len", [("c1", 40), ("7b", 100), ("7b", 256)])
+def test_batch_zero_copy_equals_assembled(cfg, mod_len):
+    """Micro-batches whose modules are read in place by the batched attention kernel
+    (per-request segment tables over the store blocks, no assembly launch) vs the same
+    micro-batches assembled into the request caches."""
+    m = pcb.Model(C1 if cfg == "c1" else L7B, dtype=pcb.BF16)  # (TINY's hd 32 has no tcgen05 attention)
+    schema_text, prompts = small_store_case(mod_len=mod_len, n_req=8)
+    schema = pcb.Schema.parse(schema_text)
+    store = pcb.ModuleStore(m)
+    store.encode_schema(schema)
+    out, asm = {}, {}
+    m.set_option("profile", 1)
+    for zc in (1, 0):
+        m.set_option("zero_copy", zc)
+        m.profile()
+        out[zc] = pcb.serve_batch(store, schema, prompts, micro_batch=4)
+        asm[zc] = m.profile()["assembly"]["launches"]
+    m.set_option("profile", 0)
+    m.set_option("zero_copy", 1)
+    assert (asm[1], asm[0]) == (0, 2)  # the copy runs once per micro-batch (8 requests / 4) only when assembled
+    for a, b in zip(out[1], out[0]):
+        assert rel(a.first_token_logits, b.first_token_logits) <= BF16_REL
+        assert same_greedy_token(a.first_token_logits, b.first_token_logits)
