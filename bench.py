@@ -665,7 +665,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--skip-batch", action="store_true")
-    ap.add_argument("--micro-batches", type=lambda v: [int(x) for x in v.split(",")], default=[4, 8, 16, 32])
+    ap.add_argument("--micro-batches", type=lambda v: [int(x) for x in v.split(",")], default=[8, 16, 32, 64])
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3
