@@ -82,7 +82,13 @@ void pcb_group_destroy(pcb_group* g);
 int pcb_model_create_tp(const char* config_json, int dtype, int device, int tp_rank, int tp_size,
                         const uint8_t* nccl_id, pcb_group* group, pcb_model** out);
 void pcb_model_destroy(pcb_model* m);
-int pcb_model_set_option(pcb_model* m, const char* key, int64_t value);  /* "force_simt" (testing), "profile" */
+/* Options (value 0/1 unless noted): "profile" (per-kernel-class CUDA-event timing),
+ * "force_simt" / "force_simt_gemm" / "force_simt_attn" (testing: SIMT kernels only),
+ * "chain" (few-token forwards as persistent chain kernels), "ln_fold" (LayerNorm folded into
+ * the chain's GEMMs), "chain_attn" (a single request's attention as the chain's first phase),
+ * "zero_copy" (serve / serve_batch read cached modules in place instead of the concat_kv copy).
+ * Returns PCB_ERR_INVALID_CONFIG for an unknown key. */
+int pcb_model_set_option(pcb_model* m, const char* key, int64_t value);
 int pcb_model_weight_checksum(pcb_model* m, const char* tensor, uint64_t* out);
 /* Model::forward / forward_masked: logits_out [n][vocab] (host, may be NULL);
  * past may be NULL; mask [n][n] (NULL = causal); new_kv may be NULL. */

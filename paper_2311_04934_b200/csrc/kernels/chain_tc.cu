@@ -100,6 +100,7 @@ struct ChainParams {
   unsigned long long* gbar;  // grid barrier arrival counter (monotonic)
   unsigned long long gbar_base;
   unsigned long long* tl;    // timeline probe [phase][cta][4] (null: off)
+  int pf_dist;               // weight tiles prefetched into L2 ahead of the ring (0: off)
 };
 
 static_assert(sizeof(ChainParams) <= 32764, "chain kernel parameters exceed the 32 KB parameter space");
@@ -354,6 +355,36 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         ctl(p, 0, 3);
       }
       const uint64_t pol_w = policy_evict_first();
+      // optional L2 prefetch of this CTA's weight tiles pf_dist tiles ahead of the issue point
+      // (keeps HBM busy through phase tails, when the ring is full and waits on the barrier)
+      struct Cursor {
+        int ph = -1, i = 0, kb = 0, kb1 = 0, tile = 0;
+      } pf;
+      auto pf_next = [&](Cursor& u) -> bool {  // advance to the next weight tile of this CTA
+        while (true) {
+          if (u.ph >= 0 && ++u.kb < u.kb1) return true;
+          if (u.ph >= 0) u.i += C;
+          while (u.ph < p.n_phases && (u.ph < 0 || p.ph[u.ph].kind != CHAIN_GEMM || u.i >= p.ph[u.ph].items)) {
+            ++u.ph;
+            u.i = c;
+            if (u.ph >= p.n_phases) return false;
+          }
+          int kb0;
+          item_kb(p.ph[u.ph], u.i, u.tile, kb0, u.kb1);
+          u.kb = kb0 - 1;
+        }
+      };
+      int pf_left = p.pf_dist;
+      bool pf_ok = pf_left > 0;
+      auto pf_issue = [&]() {
+        if (!pf_ok) return;
+        if (!(pf_ok = pf_next(pf))) return;
+        const PhaseDev& Q = p.ph[pf.ph];
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Q.w + (static_cast<int64_t>(pf.tile) * Q.kbs + pf.kb) * kWTileC),
+                     "r"(kWTileC)
+                     : "memory");
+      };
+      while (pf_left-- > 0) pf_issue();  // the window: pf_dist tiles ahead
       int it = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
         const PhaseDev& P = p.ph[ph];
@@ -363,6 +394,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           item_kb(P, i, tile, kb0, kb1);
           for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const int s = it % STAGES;
+            pf_issue();
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
             mbar_expect_tx(&full[s], S::kStage);
             // packed tiles of one 128-row block are contiguous along K
@@ -1069,6 +1101,9 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   p.gbar = gbar;
   p.gbar_base = gbar_count;
   p.tl = chain_probe_slot(n);
+  static const char* pfe = std::getenv("PCB_CHAIN_L2PF");
+  p.pf_dist = pfe ? std::atoi(pfe) : 0;
+  if (const char* v = std::getenv("PCB_CHAIN_L2PF_LIVE")) p.pf_dist = std::atoi(v);  // A/B within a process
   gbar_count += static_cast<unsigned long long>(n - 1) * C;  // one arrival per CTA per phase boundary
   PdlClass pc(PDL_GEMM);
   launch_k(k_chain<BN, STAGES>, dim3(C), dim3(kChainThreads), Sm::kBytes, s, 1, p);
