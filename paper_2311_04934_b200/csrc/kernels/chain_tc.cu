@@ -685,10 +685,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
                 *reinterpret_cast<uint4*>(dst + x) = w2[0];
                 *reinterpret_cast<uint4*>(dst + x + 8) = w2[1];
-              } else {  // park the unnormalised O row for the split merge
+              } else {  // park the normalised O row in fp16 (O / l: |values| <= max |V|) for the merge
+                const float il = l > 0.f ? 1.f / l : 0.f;
+                uint32_t hw[8];
 #pragma unroll
-                for (int y = 0; y < 16; y += 4)
-                  __stcg(reinterpret_cast<float4*>(part + x + y), make_float4(ov[y], ov[y + 1], ov[y + 2], ov[y + 3]));
+                for (int y = 0; y < 8; ++y) {
+                  const __half2 t = __floats2half2_rn(ov[2 * y] * il, ov[2 * y + 1] * il);
+                  hw[y] = *reinterpret_cast<const uint32_t*>(&t);
+                }
+                __half* ph = reinterpret_cast<__half*>(part) + x;  // row stride stays 128 floats
+                __stcg(reinterpret_cast<uint4*>(ph), make_uint4(hw[0], hw[1], hw[2], hw[3]));
+                __stcg(reinterpret_cast<uint4*>(ph + 8), make_uint4(hw[4], hw[5], hw[6], hw[7]));
               }
             }
             if (nparts > 1 && qi < n_) __stcg(ml + static_cast<int64_t>(c) * 128 + qi, make_float2(m, l));
@@ -741,26 +748,27 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 #pragma unroll
             for (int g = 0; g < 16; g += 4) {
               if (g >= nparts) break;
-              float4 f[4][4];
+              uint4 f[4][2];  // 16 fp16 values of O / l per partial
 #pragma unroll
               for (int u = 0; u < 4; ++u)
                 if (g + u < nparts) {
-                  const float4* src = reinterpret_cast<const float4*>(P.apart + prow_of(g + u, r2) * 128 + x0);
-#pragma unroll
-                  for (int x = 0; x < 4; ++x) f[u][x] = __ldcg(src + x);
+                  const uint4* src =
+                      reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(P.apart + prow_of(g + u, r2) * 128) + x0);
+                  f[u][0] = __ldcg(src);
+                  f[u][1] = __ldcg(src + 1);
                 }
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int uu = g + u;
                 if (uu >= nparts || !(ls[uu] > 0.f)) continue;
-                const float w = fast_exp2((ms[uu] - M) * P.ascale);
-                den += w * ls[uu];
+                const float wl = fast_exp2((ms[uu] - M) * P.ascale) * ls[uu];  // weight of O_s / l_s
+                den += wl;
+                const __half2* hv = reinterpret_cast<const __half2*>(&f[u][0]);
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                  acc[4 * x] += w * f[u][x].x;
-                  acc[4 * x + 1] += w * f[u][x].y;
-                  acc[4 * x + 2] += w * f[u][x].z;
-                  acc[4 * x + 3] += w * f[u][x].w;
+                for (int x = 0; x < 8; ++x) {
+                  const float2 t = __half22float2(hv[x]);
+                  acc[2 * x] += wl * t.x;
+                  acc[2 * x + 1] += wl * t.y;
                 }
               }
             }
