@@ -1,4 +1,5 @@
 // How many clusters of 2/4/8 CTAs (1 CTA per SM: ~211 KB dynamic smem) can be co-resident?
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -o tools/probe/clusters tools/probe/clusters.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 __global__ void k(int* out) { if (threadIdx.x == 0) out[blockIdx.x] = 1; }
