@@ -722,6 +722,8 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   }
   CK(cudaMemcpyAsync(W.tok, hi, n * 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(W.pos, hi + n, n * 4, cudaMemcpyHostToDevice, s));
+  if (device_token_ && B == 1 && n == 1)  // decode: the previous step's argmax, no host round trip
+    CK(cudaMemcpyAsync(W.tok, device_token_, 4, cudaMemcpyDeviceToDevice, s));
   const bool alibi = c.pos_encoding == PosEncoding::Alibi;
   if (alibi) {
     int32_t* kp = hi + 2 * n;
@@ -1235,29 +1237,41 @@ std::vector<int> Model::generate(KVBlock& kv, int last_token, int64_t last_posit
   std::vector<int> out;
   int32_t cur = last_token;
   int64_t pos = last_position;
+  // Every step's token stays on the device (argmax -> the next step's embedding input), so the
+  // host queues all steps without waiting for any: one device->host copy of the tokens at the
+  // end instead of a round trip per token (reference generate, model.cpp:464-477: fixed count)
   int32_t* host = nullptr;
-  CK(cudaMallocHost(reinterpret_cast<void**>(&host), 4));
-  try {
-    for (int s = 0; s < n_steps; ++s) {
-      if (kv.rows + 1 > kv.cap) {  // grow: reference KVState::append semantics
-        KVPtr bigger = alloc_kv(std::max<int64_t>(kv.cap * 2, kv.rows + n_steps - s));
-        copy_rows(kv, *bigger, 0);
-        std::swap(kv.data, bigger->data);
-        std::swap(kv.cap, bigger->cap);
-      }
-      run(&cur, &pos, 1, kv, nullptr, nullptr, 1);
-      argmax_last(1);
-      CK(cudaMemcpyAsync(host, ws_->argmax, 4, cudaMemcpyDeviceToHost, stream_));
-      CK(cudaStreamSynchronize(stream_));
-      cur = *host;
-      out.push_back(cur);
-      ++pos;
+  int32_t* dev = nullptr;
+  CK(cudaMallocHost(reinterpret_cast<void**>(&host), std::max(1, n_steps) * 4));
+  CK(cudaMalloc(reinterpret_cast<void**>(&dev), std::max(1, n_steps) * 4));
+  struct Reset {
+    Model* m;
+    int32_t *h, *d;
+    ~Reset() {
+      m->device_token_ = nullptr;
+      cudaFreeHost(h);
+      cudaFree(d);
     }
-  } catch (...) {
-    cudaFreeHost(host);
-    throw;
+  } reset{this, host, dev};
+  for (int s = 0; s < n_steps; ++s) {
+    if (kv.rows + 1 > kv.cap) {  // grow: reference KVState::append semantics
+      KVPtr bigger = alloc_kv(std::max<int64_t>(kv.cap * 2, kv.rows + n_steps - s));
+      copy_rows(kv, *bigger, 0);
+      std::swap(kv.data, bigger->data);
+      std::swap(kv.cap, bigger->cap);
+    }
+    device_token_ = s > 0 ? dev + (s - 1) : nullptr;
+    run(&cur, &pos, 1, kv, nullptr, nullptr, 1);  // (cur: the host value only for step 0)
+    argmax_last(1);
+    CK(cudaMemcpyAsync(dev + s, ws_->argmax, 4, cudaMemcpyDeviceToDevice, stream_));
+    ++pos;
   }
-  cudaFreeHost(host);
+  device_token_ = nullptr;
+  if (n_steps > 0) {
+    CK(cudaMemcpyAsync(host, dev, n_steps * 4, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    out.assign(host, host + n_steps);
+  }
   return out;
 }
 

@@ -182,6 +182,7 @@ class Model {
   int dl_ = 0, fl_ = 0, vl_ = 0;  // local attention width, MLP width, vocab rows
   std::shared_ptr<coll::Collective> comm_;
   std::vector<cudaEvent_t> layer_events_;
+  const int32_t* device_token_ = nullptr;  // generate(): this step's token is already on the device
   std::vector<const KVBlock*> kv_prefix_;
   std::vector<std::vector<const KVBlock*>> kv_prefix_batch_;
   int64_t kv_prefix_rows_ = 0;
