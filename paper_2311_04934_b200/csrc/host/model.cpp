@@ -859,41 +859,43 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
       max_nb = std::max(max_nb, items[b].n);
     }
   }
-  // zero-copy micro-batch: per-request segment tables for the batched attention kernel --
-  // each request's module blocks read in place, then its own rows in the batch arena (one
-  // 3-D map over all request caches, plane = request * 2L + 2 layer + K/V)
+  // Batched attention reads every request's keys through per-request segment tables: the
+  // request's own cache rows [0, P + n) (one 3-D map per request, rows ending at its last
+  // valid row so the rest of a 64-row block is TMA zero fill -- a masked key has P = 0 but
+  // 0 * NaN of stale memory in PV is NaN), preceded, on the zero-copy path, by its module
+  // blocks read in place (plane = 2 layer + K/V).
   int64_t seg_max_blocks = 0;
   const int4* d_segs = nullptr;
   const int2* d_segn = nullptr;
   const void* d_maps = nullptr;
-  if (!kv_prefix_batch_.empty()) {
-    if (!batched_attn) throw Error(ErrorCode::ShapeMismatch, "zero-copy batch needs request caches at a uniform stride");
+  if (!kv_prefix_batch_.empty() && !batched_attn)
+    throw Error(ErrorCode::ShapeMismatch, "zero-copy batch needs the batched attention path");
+  if (batched_attn) {
     const int L2 = 2 * c.n_layers;
-    const KVBlock& a0 = *items[0].kv;
-    if (req_stride != static_cast<int64_t>(a0.plane_bytes()) * L2)
-      throw Error(ErrorCode::ShapeMismatch, "zero-copy batch: request caches must be contiguous blocks");
     std::vector<CUtensorMap> maps;
     std::map<const void*, int> map_of;
-    maps.push_back(kern::tmap_bf16_3d(a0.data, d, a0.cap, static_cast<uint64_t>(L2) * B, a0.plane_bytes(), 64));
     std::vector<int4> tab(static_cast<size_t>(B) * kern::kAttnMaxSeg, make_int4(0, 0, 0, 0));
     std::vector<int2> segn(B);
     for (int b = 0; b < B; ++b) {
       int g = 0;
       int64_t pre = 0, blocks = 0;
-      for (const KVBlock* blk : kv_prefix_batch_[b]) {
-        auto it = map_of.find(blk->data);
-        if (it == map_of.end()) {
-          it = map_of.emplace(blk->data, static_cast<int>(maps.size())).first;
-          maps.push_back(kern::tmap_bf16_3d(blk->data, d, blk->cap, L2, blk->plane_bytes(), 64));
+      if (!kv_prefix_batch_.empty())
+        for (const KVBlock* blk : kv_prefix_batch_[b]) {
+          auto it = map_of.find(blk->data);
+          if (it == map_of.end()) {
+            it = map_of.emplace(blk->data, static_cast<int>(maps.size())).first;
+            maps.push_back(kern::tmap_bf16_3d(blk->data, d, blk->rows, L2, blk->plane_bytes(), 64));
+          }
+          tab[b * kern::kAttnMaxSeg + g++] = make_int4(it->second, 0, static_cast<int>(blk->rows), 0);
+          pre += blk->rows;
+          blocks += (blk->rows + 63) / 64;
         }
-        tab[b * kern::kAttnMaxSeg + g++] = make_int4(it->second, 0, static_cast<int>(blk->rows), 0);
-        pre += blk->rows;
-        blocks += (blk->rows + 63) / 64;
-      }
-      const int64_t Pb = items[b].kv->rows, nb = items[b].n;
+      const KVBlock& rk = *items[b].kv;
+      const int64_t Pb = rk.rows, nb = items[b].n;
       if (pre > Pb) throw Error(ErrorCode::ShapeMismatch, "zero-copy batch: prefix longer than the cache");
-      tab[b * kern::kAttnMaxSeg + g++] =
-          make_int4(0, static_cast<int>(pre), static_cast<int>(Pb + nb - pre), b * L2);
+      const int own = static_cast<int>(maps.size());
+      maps.push_back(kern::tmap_bf16_3d(rk.data, d, Pb + nb, L2, rk.plane_bytes(), 64));
+      tab[b * kern::kAttnMaxSeg + g++] = make_int4(own, static_cast<int>(pre), static_cast<int>(Pb + nb - pre), 0);
       blocks += (Pb + nb - pre + 63) / 64;
       segn[b] = make_int2(g, static_cast<int>(Pb - pre));
       seg_max_blocks = std::max(seg_max_blocks, blocks);

@@ -1083,7 +1083,9 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
         for (int sgi = 0; sgi < st.a_nseg; ++sgi) {
           const ChainStep::KVSeg& g = st.a_seg[sgi];
           if (g.rows <= 0 || g.row0 + g.rows > g.cap) throw std::runtime_error("chain: bad KV segment");
-          p.tkv[sgi] = tmap_bf16_3d(g.base, static_cast<uint64_t>(st.a_d), static_cast<uint64_t>(g.cap),
+          // rows end at the segment's last valid row: the rest of a 64-row block is TMA
+          // zero fill, never stale memory (a masked key has P = 0, but 0 * NaN in PV is NaN)
+          p.tkv[sgi] = tmap_bf16_3d(g.base, static_cast<uint64_t>(st.a_d), static_cast<uint64_t>(g.row0 + g.rows),
                                     static_cast<uint64_t>(st.a_planes), g.plane_bytes, 64);
           d.a_row0[sgi] = static_cast<int>(g.row0);
           d.a_rows[sgi] = static_cast<int>(g.rows);

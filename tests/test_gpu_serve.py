@@ -261,3 +261,34 @@ def test_decode_cost_flat(m32):
     b = m32.forward_tokens
     pcb.serve(store, schema, p, 9)
     assert m32.forward_tokens - b - one == 8
+
+
+def test_zero_copy_on_reference_corpus(host_golden, numeric_golden):
+    """Every golden corpus schema / random case (unions, nested and anonymous modules,
+    parameters, scaffolds-free prompts) through a bf16 model with 128-wide heads, so single
+    requests take the chain attention phase and read their modules in place when eligible:
+    tokens and first-token logits vs the same requests with the assembly copy, and the
+    cached path vs the device oracle.  (TINY's 32-wide heads never take that path.)"""
+    cfg = dict(n_layers=2, n_heads=2, head_dim=128, hidden=256, vocab_size=512, pos_encoding="rope",
+               max_position=8192, bytes_per_element=2, seed=42)
+    m = pcb.Model(cfg, dtype=pcb.BF16)
+    worst, n_cases = 0.0, 0
+    for case in numeric_golden["serve"]:
+        s_in, p_in = golden_case_inputs(host_golden, case["name"])
+        schema, prompt = schema_of(s_in), prompt_of(p_in)
+        store = pcb.ModuleStore(m)
+        store.encode_schema(schema)
+        out = {}
+        for zc in (1, 0):
+            m.set_option("zero_copy", zc)
+            out[zc] = pcb.serve(store, schema, prompt, 8)
+        m.set_option("zero_copy", 1)
+        o = pcb.oracle_serve(m, schema, prompt, 8)
+        assert out[1].cache_report == out[0].cache_report, case["name"]
+        assert same_greedy_token(out[1].first_token_logits, out[0].first_token_logits), case["name"]
+        assert same_greedy_token(out[1].first_token_logits, o.first_token_logits), case["name"]
+        worst = max(worst, rel(out[1].first_token_logits, out[0].first_token_logits),
+                    rel(out[1].first_token_logits, o.first_token_logits))
+        n_cases += 1
+    assert n_cases >= 40
+    assert worst <= BF16_REL, worst
