@@ -1111,9 +1111,11 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   p.gbar = gbar;
   p.gbar_base = gbar_count;
   p.tl = chain_probe_slot(n);
-  static const char* pfe = std::getenv("PCB_CHAIN_L2PF");
-  p.pf_dist = pfe ? std::atoi(pfe) : 0;
-  if (const char* v = std::getenv("PCB_CHAIN_L2PF_LIVE")) p.pf_dist = std::atoi(v);  // A/B within a process
+  static const int pf_dist = [] {  // L2 prefetch window (measured slower; off unless asked)
+    const char* v = std::getenv("PCB_CHAIN_L2PF");
+    return v ? std::atoi(v) : 0;
+  }();
+  p.pf_dist = pf_dist;
   gbar_count += static_cast<unsigned long long>(n - 1) * C;  // one arrival per CTA per phase boundary
   PdlClass pc(PDL_GEMM);
   launch_k(k_chain<BN, STAGES>, dim3(C), dim3(kChainThreads), Sm::kBytes, s, 1, p);

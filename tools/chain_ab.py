@@ -35,9 +35,6 @@ VARIANTS = [
     ("chain", {"chain": 1, "ln_fold": 1, "chain_attn": 0, "zero_copy": 0}),
     ("chain+attn", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 0}),
     ("zero-copy", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 1}),
-    ("zc+pf8", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 1, "env:PCB_CHAIN_L2PF_LIVE": 8}),
-    ("zc+pf16", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 1, "env:PCB_CHAIN_L2PF_LIVE": 16}),
-    ("zc+pf32", {"chain": 1, "ln_fold": 1, "chain_attn": 1, "zero_copy": 1, "env:PCB_CHAIN_L2PF_LIVE": 32}),
     ("chain, LN phases", {"chain": 1, "ln_fold": 0, "chain_attn": 0, "zero_copy": 0}),
 
 ]
@@ -56,7 +53,6 @@ parsed = [pcb.Prompt.parse(p) for p in prompts]
 res = {name: [] for name, _ in VARIANTS}
 for r in range(rounds):
     for name, opts in VARIANTS:
-        os.environ["PCB_CHAIN_L2PF_LIVE"] = "0"
         for k, v in opts.items():
             if k.startswith("env:"):
                 os.environ[k[4:]] = str(v)
