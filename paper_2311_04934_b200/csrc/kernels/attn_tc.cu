@@ -581,7 +581,11 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
       }
     }
   }
-  if (const char* ov = std::getenv("PCB_ATTN_SPLITS")) splits = std::max(1, std::atoi(ov));  // tuning
+  static const int splits_env = [] {  // tuning override (environment read once)
+    const char* v = std::getenv("PCB_ATTN_SPLITS");
+    return v ? std::max(1, std::atoi(v)) : 0;
+  }();
+  if (splits_env) splits = splits_env;
   p.splits = splits;
   p.part_o = scratch;
   p.part_ml = scratch + static_cast<size_t>(a.H) * splits * BQ * HD;
@@ -589,15 +593,17 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   if (splits > 8) splits = 8;
   p.splits = splits;
   CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), BQ);
-  p.kv_head_major = std::getenv("PCB_ATTN_HM_PROBE") ? 1 : 0;  // timing probe (values meaningless)
+  static const bool hm_probe = std::getenv("PCB_ATTN_HM_PROBE") != nullptr;  // timing probe (values meaningless)
+  p.kv_head_major = hm_probe ? 1 : 0;
   p.kv_rows = p.total;
-  if (std::getenv("PCB_ATTN_TL")) {  // per-CTA phase timeline of the LAST launch (attn_tl_dump)
+  static const bool tl_on = std::getenv("PCB_ATTN_TL") != nullptr;
+  if (tl_on) {  // per-CTA phase timeline of the LAST launch (attn_tl_dump)
     if (!g_tlbuf) PCB_CUDA(cudaMalloc(&g_tlbuf, 8192 * 8 * sizeof(unsigned long long)));
     p.tl = g_tlbuf;
     g_tl_ctas = q_tiles * a.H * std::min(splits, 8);
   }
   static unsigned long long* dbg = nullptr;
-  const bool probe_on = std::getenv("PCB_ATTN_DBG") != nullptr;  // timeline probe of CTA 0 (debug)
+  static const bool probe_on = std::getenv("PCB_ATTN_DBG") != nullptr;  // timeline probe of CTA 0 (debug)
   if (probe_on) {
     if (!dbg) PCB_CUDA(cudaMallocManaged(&dbg, 12 * 64 * sizeof(unsigned long long)));
     std::memset(dbg, 0, 12 * 64 * sizeof(unsigned long long));

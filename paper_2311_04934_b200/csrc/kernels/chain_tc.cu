@@ -1071,7 +1071,8 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.aout = static_cast<__nv_bfloat16*>(st.aout);
       if (static_cast<size_t>(d.items) * 128 * 130 * sizeof(float) > st.a_scratch_bytes)
         throw std::runtime_error("chain: attention scratch too small");
-      d.adup = st.M <= 64 && !std::getenv("PCB_CHAIN_ATTN_NODUP");
+      static const bool nodup = std::getenv("PCB_CHAIN_ATTN_NODUP") != nullptr;  // A/B switch
+      d.adup = st.M <= 64 && !nodup;
       p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 64);
       d.a_nseg = st.a_nseg;
       if (st.a_nseg) {

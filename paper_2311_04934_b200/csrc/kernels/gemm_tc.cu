@@ -394,7 +394,11 @@ static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, co
   a.epoch = ++g_sk_epoch;
   if (std::getenv("PCB_GEMM_XBULK_PROBE")) a.x_bulk_probe = static_cast<const uint8_t*>(A);
   int C = static_cast<int>(std::min<int64_t>(sms, a.units));
-  if (const char* ov = std::getenv("PCB_GEMM_CTAS")) C = std::max(1, std::min(C, std::atoi(ov)));  // tuning
+  static const int ctas_env = [] {  // tuning override (environment read once)
+    const char* v = std::getenv("PCB_GEMM_CTAS");
+    return v ? std::max(1, std::atoi(v)) : 0;
+  }();
+  if (ctas_env) C = std::min(C, ctas_env);
   if (static_cast<size_t>(C) * 128 * BN * sizeof(float) > ws_bytes) throw std::runtime_error("gemm workspace too small");
   a.tl = probe_slot(M, N, K, C);
   CUtensorMap tx = tmap_bf16_2d(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), BN);
