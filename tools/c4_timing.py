@@ -8,7 +8,7 @@ schema_text, prompts, _ = bench.workload_c4(64, 256, 256, 8, 64)
 schema = pcb.Schema.parse(schema_text)
 store = pcb.ModuleStore(m)
 store.encode_schema(schema)
-ps = [pcb.Prompt.parse(p) for p in prompts[: 8 * mb]]
+ps = [pcb.Prompt.parse(p) for p in prompts[: int(os.environ.get("C4_N", 8 * mb))]]
 pcb.serve_batch(store, schema, ps[: 2 * mb], micro_batch=mb)
 m.sync()
 m.timer_start(); t0 = time.perf_counter()
