@@ -1,5 +1,8 @@
+"""Config 4 micro-batch timeline: device time per micro-batch of serve_batch and each
+micro-batch's assembly / prefill / TTFT split.
+  C4_N=256 python tools/c4_timing.py [micro_batch]"""
 import os, sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 import paper_2311_04934_b200 as pcb
 mb = int(sys.argv[1]) if len(sys.argv) > 1 else 32
