@@ -224,6 +224,7 @@ class Dist:
 
     def __init__(self, backend: str = "nccl"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.dist = self.torch = None
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.backend = backend
@@ -382,11 +383,12 @@ def run_reference(a) -> None:
 # our implementation
 # ---------------------------------------------------------------------------
 def run_batch_c4(D, model, a) -> dict:
-    """256 requests, each 8 of 64 store modules (256 tokens each) + 64 uncached
-    tokens, partitioned over the ranks (no collectives); serve_batch micro-batches per rank."""
+    """256 requests per GPU (256 x N in total, so every rank keeps a steady
+    stream of micro-batches as N grows), each importing 8 of the 64 store modules (256 tokens each)
+    + 64 uncached tokens, partitioned over the ranks (no collectives); serve_batch per rank."""
     import paper_2311_04934_b200 as pcb
 
-    n_req = 256
+    n_req = 256 * D.world
     schema_text, prompts, _ = workload_c4(64, 256, n_req, 8, 64)
     schema = pcb.Schema.parse(schema_text)
     store = pcb.ModuleStore(model)
@@ -406,12 +408,22 @@ def run_batch_c4(D, model, a) -> dict:
                      "ttft_ms_mean": D.max(statistics.mean(r.timings["ttft_us"] for r in res) / 1e3),
                      "device_ms": dev_ms}
     best = max(sweep, key=lambda k: sweep[k]["requests_per_s"])
+    # kernel classes of the best micro-batch size (profiled pass, CUDA events per launch)
+    model.set_option("profile", 1)
+    model.profile()
+    pcb.serve_batch(store, schema, mine, micro_batch=best)
+    prof = model.profile()
+    model.set_option("profile", 0)
+    g, at = prof["gemm"], prof["attention"]
     del store
-    return {"workload": "configs[3]: 256 requests, 8 of 64 store modules (256 tokens each, 2048 cached rows) + "
-                        "64 uncached tokens per request, modules resident in HBM, data-parallel over ranks",
-            "requests": n_req, "n_gpus": D.world, "scaling": "strong", "micro_batch": best,
+    return {"workload": "configs[3]: 256 requests per GPU, each 8 of 64 store modules (256 tokens) + 64 uncached",
+            "requests": n_req, "n_gpus": D.world, "scaling": "weak", "micro_batch": best,
             "requests_per_s": sweep[best]["requests_per_s"], "e2e_requests_per_s": sweep[best]["e2e_requests_per_s"],
-            "ttft_ms_mean": sweep[best]["ttft_ms_mean"], "sweep": sweep}
+            "ttft_ms_mean": round(sweep[best]["ttft_ms_mean"], 2),
+            "gemm_tflops": round(g["flops"] / (g["ms"] / 1e3) / 1e12, 1) if g["ms"] else None,
+            "gemm_ms_per_request": round(g["ms"] / len(mine), 4),
+            "attention_GBps": round(at["bytes"] / (at["ms"] / 1e3) / 1e9, 0) if at["ms"] else None,
+            "sweep_requests_per_s": {mb: round(v["requests_per_s"], 1) for mb, v in sweep.items()}}
 
 
 def run_c5(a) -> None:
@@ -609,6 +621,8 @@ def run_ours(a) -> None:
         del sstore
 
     batch = None if a.skip_batch else run_batch_c4(D, model, a)
+    c3 = None if (a.skip_c3 or a.config != "c2") else run_c3_summary(D, model, a)
+    sweep = None if a.skip_sweep else run_ttft_sweep(D, model)
 
     cpu = None
     if D.rank == 0 and D.world == 1 and not a.skip_cpu:
@@ -618,38 +632,136 @@ def run_ours(a) -> None:
             cpu = {"value": None, "unavailable": str(e)}
 
     if D.rank == 0:
+        r3 = lambda x, k=3: None if x is None else round(x, k)  # noqa: E731
         line = {
             "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": D.world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": region_ms / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (reference synthetic_text generator; random-init weights from the reference's "
-                    "seeded PCG32 streams)",
+            "data": "synthetic (reference synthetic_text text; random-init weights from the reference's PCG32 streams)",
             "config": {"workload": f"configs[{1 if a.config == 'c2' else 2}]: Llama-2-7B shape, {n_cached} cached "
-                                   f"module tokens ({n_mod} module{'s' if n_mod > 1 else ''}) + {n_unc} uncached, "
-                                   "single request per step per GPU, modules resident in HBM",
-                       "model": "llama-2-7b-shape (reference block: LN, MHA, interleaved RoPE, GELU MLP)",
+                                   f"tokens ({n_mod} module{'s' if n_mod > 1 else ''}) + {n_unc} uncached, one request "
+                                   "per step per GPU, modules in HBM",
                        "cached_tokens": n_cached, "uncached_tokens": n_unc, "parallelism": f"dp{D.world}",
                        "l2": "inputs larger than L2 (12.9 GB weights + 2.1 GB KV per step)"},
-            "ttft_ms": ttft_mean, "full_prefill_ttft_ms": full_ms, "ttft_speedup_vs_full_prefill": full_ms / ttft_mean,
-            "device_ms_per_request": dev_ms / a.steps, "ttft_slow_tier_ms": slow,
-            "precompute_ms": precompute_ms, "decode_tpot_ms": decode_tpot_ms,
-            "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "k_chain (persistent tcgen05 chains: every GEMM of a step "
-                                                   "(swap-AB weight streaming) and, as each chain's first phase, "
-                                                   "the layer's attention, reading the cached modules in place)",
-                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": traffic, "traffic_unit": "bytes per step (all chain launches)",
-                         "traffic_source": traffic_src, "peak_source": peak_src,
-                         "alg_bytes_per_step": gemm_bytes_step, "gemm_ms_per_step": gemm_ms_step,
-                         "tensor_peak_tflops": tc_peak},
-            "kernel_classes": classes,
-            "kv_assembly": assembly,
-            "batch": batch,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "kernel_classes": {k: {"ms": r3(v["ms_per_step"]), "launches": v["launches_per_step"],
+                                   "GBps": r3(v["GBps"], 0)} for k, v in classes.items() if v["launches_per_step"]},
+            "batch": batch,
+            "ttft_sweep": sweep,
+            "precompute_ms": r3(precompute_ms), "decode_tpot_ms": r3(decode_tpot_ms), "ttft_slow_tier_ms": r3(slow),
+            "device_ms_per_request": r3(dev_ms / a.steps),
+            "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "kernel": "k_chain (persistent tcgen05 layer chains: attention + GEMMs)",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                         "alg_bytes_per_step": gemm_bytes_step, "kernel_ms_per_step": gemm_ms_step},
+            "kv_assembly": None if not assembly else {k: r3(assembly[k]) for k in ("GBps", "frac_of_hbm",
+                                                                                   "ms_per_request", "ttft_ms_with_copy")},
+            "config3": c3,
+            # headline last: the driver keeps the tail of the line
+            "ttft_ms": ttft_mean, "full_prefill_ttft_ms": full_ms, "ttft_speedup_vs_full_prefill": full_ms / ttft_mean,
         }
         print(json.dumps(line), flush=True)
+    D.close()
+
+
+def run_c3_summary(D, model, a) -> dict:
+    """configs[2] on the same model: 3 document modules, 16,384 cached tokens + 128 uncached; cached
+    TTFT (host clock, modules read in place) vs full prefill of the 16,512-token prompt."""
+    import paper_2311_04934_b200 as pcb
+
+    schema_text, prompts = workload(16384, 128, 3)
+    schema = pcb.Schema.parse(schema_text)
+    store = pcb.ModuleStore(model)
+    store.encode_schema(schema)
+    parsed = [pcb.Prompt.parse(p) for p in prompts]
+    for i in range(3):
+        pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1)
+    model.sync()
+    D.barrier()
+    tt = [pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1).timings["ttft_us"] / 1e3
+          for i in range(max(3, a.steps // 2))]
+    full = [pcb.serve(store, schema, parsed[0], max_new_tokens=1, use_cache=False).timings["ttft_us"] / 1e3
+            for _ in range(3)][1:]
+    del store
+    ttft, full_ms = D.max(statistics.mean(tt)), D.max(statistics.median(full))
+    return {"workload": "configs[2]: 3 modules, 16384 cached + 128 uncached", "ttft_ms": round(ttft, 3),
+            "full_prefill_ttft_ms": round(full_ms, 2), "speedup": round(full_ms / ttft, 2)}
+
+
+def run_ttft_sweep(D, model) -> dict:
+    """GPU version of the reference's TTFT sweep (bench::run_scaling, bench.cpp:48-110): one module of
+    n tokens + a one-token question, cached vs full-prefill TTFT (median of 3 after a warm-up) and the
+    log-log growth exponents over the largest half of the lengths (acceptance check 8)."""
+    import paper_2311_04934_b200 as pcb
+
+    lengths = [256, 512, 1024, 2048, 4096, 8192]
+    rows = {"n": lengths, "cached_ms": [], "full_ms": []}
+    for n in lengths:
+        schema = pcb.Schema.parse(f'<schema name="bench"><module name="m">{synthetic_text(n, 7 * n + 1)}</module></schema>')
+        store = pcb.ModuleStore(model)
+        store.encode_schema(schema)
+        prompt = pcb.Prompt.parse('<prompt schema="bench"><m/>?</prompt>')
+        c, b = [], []
+        for t in range(4):
+            rc = pcb.serve(store, schema, prompt, max_new_tokens=1)
+            rb = pcb.serve(store, schema, prompt, max_new_tokens=1, use_cache=False)
+            if t:
+                c.append(rc.timings["ttft_us"] / 1e3)
+                b.append(rb.timings["ttft_us"] / 1e3)
+        rows["cached_ms"].append(round(D.max(statistics.median(c)), 3))
+        rows["full_ms"].append(round(D.max(statistics.median(b)), 3))
+        del store
+
+    def slope(xs, ys):
+        lx, ly = [math.log(x) for x in xs], [math.log(y) for y in ys]
+        n = len(xs)
+        return (n * sum(a * b for a, b in zip(lx, ly)) - sum(lx) * sum(ly)) / (n * sum(a * a for a in lx) - sum(lx) ** 2)
+
+    h = len(lengths) // 2
+    rows["cached_exp"] = round(slope(lengths[h:], rows["cached_ms"][h:]), 3)
+    rows["full_exp"] = round(slope(lengths[h:], rows["full_ms"][h:]), 3)
+    return rows
+
+
+def relaunch(a) -> int:
+    """`bench.py --gpus N` run directly (no WORLD_SIZE): re-exec under torch.distributed.run, one
+    process per GPU on this node (the driver's own launch sets WORLD_SIZE and lands in main)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def run_dry(a) -> None:
+    """--dry-run: the multi-process plumbing on CPU (gloo) -- launch, barrier, per-rank request
+    partition, max-over-ranks timing and rank 0's single JSON line -- with the host half of a
+    cached request (parse, validate/resolve through the C ABI) as the step; no device work."""
+    D = Dist(backend="gloo")
+    import paper_2311_04934_b200 as pcb
+
+    schema_text, prompts = workload(512, 64, 1)
+    schema = pcb.Schema.parse(schema_text)
+    for i in range(a.warmup):
+        pcb.Prompt.parse(prompts[i % len(prompts)]).resolve(schema)
+    D.barrier()
+    t0 = time.perf_counter()
+    for i in D.requests(a.steps, len(prompts)):
+        pcb.Prompt.parse(prompts[i]).resolve(schema)
+    region = D.max(time.perf_counter() - t0)
+    mine = partition(256 * D.world, D.rank, D.world)
+    if D.rank == 0:
+        print(json.dumps({"metric": METRIC, "value": D.world * a.steps / region, "unit": "requests/s (host half only)",
+                          "n_gpus": D.world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": region / a.steps * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "none",
+                          "data": "synthetic", "dry_run": True, "c4_requests_rank0": len(mine),
+                          "config": {"workload": "dry run: host parse + resolve only", "parallelism": f"dp{D.world}"}}),
+              flush=True)
     D.close()
 
 
@@ -665,11 +777,18 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--skip-batch", action="store_true")
+    ap.add_argument("--skip-c3", action="store_true")
+    ap.add_argument("--skip-sweep", action="store_true")
     ap.add_argument("--micro-batches", type=lambda v: [int(x) for x in v.split(",")], default=[8, 16, 32, 64])
+    ap.add_argument("--dry-run", action="store_true", help="CPU-only plumbing check (gloo), no device work")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3
-    if a.impl == "reference":
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(a))
+    if a.dry_run:
+        run_dry(a)
+    elif a.impl == "reference":
         run_reference(a)
     elif a.config == "c5":
         run_c5(a)

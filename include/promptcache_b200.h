@@ -123,6 +123,11 @@ int pcb_store_set_capacity(pcb_store* s, int tier, int64_t bytes);
 int pcb_store_encode_module(pcb_store* s, const pcb_schema* sc, const char* module, int tier); /* encode_module + insert */
 int pcb_store_encode_schema(pcb_store* s, const pcb_schema* sc, int tier, int* count);        /* encode_schema */
 int pcb_store_encode_scaffold(pcb_store* s, const pcb_schema* sc, const char* members_json, int tier);
+/* Installs precomputed rows as module `module` of the schema (the reference's insert of an
+ * encode_module result, cache.cpp:288-301 + cache.hpp:58; SURVEY §8b pcb_store_put_kv): kv must
+ * hold exactly the module's own rows at its schema positions (PCB_ERR_SHAPE_MISMATCH
+ * otherwise); the block is shared with the store, not copied (slow tier: pinned host copy). */
+int pcb_store_put_kv(pcb_store* s, const pcb_schema* sc, const char* module, const pcb_kv* kv, int tier);
 int pcb_store_lookup(pcb_store* s, const char* schema, const char* name, pcb_kv** out);       /* *out NULL on miss */
 int64_t pcb_store_size(const pcb_store* s);
 char* pcb_store_stats_json(const pcb_store* s);

@@ -94,6 +94,8 @@ class Ref:
             L.pcref_kv_layer.argtypes = [vp, i32, i32, vp]
             L.pcref_kv_synthetic.restype = vp
             L.pcref_kv_synthetic.argtypes = [i32, i32, i64, u64]
+            L.pcref_kv_from_arrays.restype = vp
+            L.pcref_kv_from_arrays.argtypes = [i32, i32, i64, vp, vp, vp]
             L.pcref_kv_concat.restype = vp
             L.pcref_kv_concat.argtypes = [C.POINTER(vp), i32]
             for fn in ("pcref_parse_schema",):
@@ -306,6 +308,15 @@ class RefModel:
         rc = Ref.lib().pcref_store_save(self.h, Ref._b(schema), Ref._is_ast(schema), sc, path.encode())
         if rc:
             raise RefError(rc, Ref.lib().pcref_last_error().decode())
+
+
+def ref_kv(k, v, positions) -> "RefKV":
+    """A reference KVState holding k/v [L][rows][hidden] (fp32) at `positions`."""
+    k = np.ascontiguousarray(k, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    p = np.ascontiguousarray(positions, np.int64)
+    h = Ref.lib().pcref_kv_from_arrays(k.shape[0], k.shape[2], len(p), k.ctypes.data, v.ctypes.data, p.ctypes.data)
+    return RefKV(h, k.shape[0], k.shape[2])
 
 
 def ref_concat(kvs):

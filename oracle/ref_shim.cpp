@@ -281,6 +281,24 @@ void* pcref_kv_synthetic(int n_layers, int hidden, int64_t rows, uint64_t seed) 
   return kv;
 }
 
+// A KVState from caller arrays k/v [n_layers][rows][hidden] + positions (test fixtures:
+// the same synthetic past is uploaded to the device model and handed to the reference).
+void* pcref_kv_from_arrays(int n_layers, int hidden, int64_t rows, const float* k, const float* v,
+                           const int64_t* pos) {
+  auto* kv = new KV;
+  kv->s.n_layers = n_layers;
+  kv->s.hidden = hidden;
+  kv->s.k.resize(n_layers);
+  kv->s.v.resize(n_layers);
+  for (long r = 0; r < rows; ++r) kv->s.position_ids.push_back(pos[r]);
+  const size_t cnt = static_cast<size_t>(rows) * hidden;
+  for (int l = 0; l < n_layers; ++l) {
+    kv->s.k[l].assign(k + l * cnt, k + (l + 1) * cnt);
+    kv->s.v[l].assign(v + l * cnt, v + (l + 1) * cnt);
+  }
+  return kv;
+}
+
 // engine::concat_kv (engine.cpp:174-185) over bare KV states wrapped as entries.
 void* pcref_kv_concat(void** kvs, int n) {
   KV* out = nullptr;

@@ -85,6 +85,7 @@ def lib():
         "pcb_store_encode_schema": (i32, [vp, vp, i32, C.POINTER(i32)]),
         "pcb_store_encode_scaffold": (i32, [vp, vp, cp, i32]),
         "pcb_store_lookup": (i32, [vp, cp, cp, pvp]), "pcb_store_size": (i64, [vp]),
+        "pcb_store_put_kv": (i32, [vp, vp, cp, vp, i32]),
         "pcb_store_stats_json": (vp, [vp]), "pcb_store_save": (i32, [vp, cp]),
         "pcb_store_load": (i32, [vp, cp]),
         "pcb_serve": (i32, [vp, vp, vp, i32, i32, i32, pvp]),
@@ -404,6 +405,10 @@ class ModuleStore(_Handle):
 
     def encode_scaffold(self, schema: Schema, members: list[str], tier: int = FAST):
         _check(lib().pcb_store_encode_scaffold(self._h, schema.handle, _enc(json.dumps(members)), tier))
+
+    def put_kv(self, schema: Schema, name: str, kv: KV, tier: int = FAST):
+        """Install precomputed rows as module `name` (rows/positions must be its schema span)."""
+        _check(lib().pcb_store_put_kv(self._h, schema.handle, _enc(name), kv.handle, tier))
 
     def lookup(self, schema_name: str, name: str) -> KV | None:
         h = C.c_void_p()

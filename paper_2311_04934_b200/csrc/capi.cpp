@@ -11,6 +11,7 @@
 #include "host/cache.hpp"
 #include "host/engine.hpp"
 #include "host/collective.hpp"
+#include "host/cuda_check.hpp"
 #include "host/layout.hpp"
 #include "host/model.hpp"
 #include "host/pml.hpp"
@@ -366,19 +367,19 @@ int pcb_kv_read(const pcb_kv* kvh, int layer, int which, float* out) {
 int pcb_kv_upload(pcb_model* m, const float* k, const float* v, const int64_t* pos, int64_t rows, pcb_kv** out) {
   return guard([&] {
     model::Model& mm = *m->m;
+    CK(cudaSetDevice(mm.device()));
+    if (rows < 0) throw Error(ErrorCode::ShapeMismatch, "negative row count");
     model::KVPtr kv = mm.alloc_kv(rows);
     const int L = mm.config().n_layers, d = mm.kv_width();
     const uint64_t cnt = static_cast<uint64_t>(rows) * d;
-    float* f = nullptr;
-    if (cnt) cudaMalloc(&f, cnt * 4);
-    for (int l = 0; l < L; ++l)
+    DeviceBuffer f(cnt * 4);
+    for (int l = 0; l < L && cnt; ++l)
       for (int w = 0; w < 2; ++w) {
-        if (!cnt) continue;
-        cudaMemcpy(f, (w ? v : k) + l * cnt, cnt * 4, cudaMemcpyHostToDevice);
-        kern::convert(kern::F32, f, mm.dtype(), kv->plane(l, w), cnt, nullptr);
+        CK(cudaMemcpyAsync(f.get(), (w ? v : k) + l * cnt, cnt * 4, cudaMemcpyHostToDevice, mm.stream()));
+        kern::convert(kern::F32, f.get(), mm.dtype(), kv->plane(l, w), cnt, mm.stream());
+        CK(cudaGetLastError());
       }
-    cudaDeviceSynchronize();
-    if (f) cudaFree(f);
+    CK(cudaStreamSynchronize(mm.stream()));
     kv->rows = rows;
     kv->positions.assign(pos, pos + rows);
     *out = new pcb_kv{kv};
@@ -426,6 +427,12 @@ int pcb_store_lookup(pcb_store* s, const char* schema, const char* name, pcb_kv*
   return guard([&] {
     cache::EntryPtr e = s->s->lookup(schema, name);
     *out = e ? new pcb_kv{e->kv} : nullptr;
+  });
+}
+int pcb_store_put_kv(pcb_store* s, const pcb_schema* sc, const char* module, const pcb_kv* kv, int tier) {
+  return guard([&] {
+    if (!kv) throw Error(ErrorCode::ShapeMismatch, "null KV block");
+    s->s->insert(cache::install_module(s->s->model(), sc->P().plan, module, kv->kv, tier_of(tier)));
   });
 }
 int64_t pcb_store_size(const pcb_store* s) { return static_cast<int64_t>(s->s->size()); }

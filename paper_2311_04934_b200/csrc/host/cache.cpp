@@ -9,6 +9,7 @@
 #include <set>
 
 #include "../kernels/kernels.cuh"
+#include "cuda_check.hpp"
 #include "json.hpp"
 
 namespace pcb::cache {
@@ -29,6 +30,11 @@ std::string scaffold_id(const std::vector<std::string>& members) {
 }
 
 void ModuleStore::evict_lru(Tier t, int64_t needed) {
+  std::lock_guard<std::recursive_mutex> g(mu_);
+  evict_locked(t, needed);
+}
+
+void ModuleStore::evict_locked(Tier t, int64_t needed) {
   const int64_t cap = capacity(t);
   if (cap < 0) return;
   while (used(t) + needed > cap) {
@@ -44,6 +50,7 @@ void ModuleStore::evict_lru(Tier t, int64_t needed) {
 }
 
 void ModuleStore::insert(CacheEntry e) {
+  std::lock_guard<std::recursive_mutex> g(mu_);
   const int64_t bytes = entry_bytes(e, model_->config());
   const int64_t cap = capacity(e.tier);
   if (cap >= 0 && bytes > cap)
@@ -55,7 +62,7 @@ void ModuleStore::insert(CacheEntry e) {
     used(old->second->tier) -= entry_bytes(*old->second, model_->config());
     entries_.erase(old);
   }
-  evict_lru(e.tier, bytes);
+  evict_locked(e.tier, bytes);
   e.created_at = ++clock_;
   e.last_used = e.created_at;
   used(e.tier) += bytes;
@@ -63,6 +70,7 @@ void ModuleStore::insert(CacheEntry e) {
 }
 
 EntryPtr ModuleStore::lookup(const std::string& schema, const std::string& name) {
+  std::lock_guard<std::recursive_mutex> g(mu_);
   auto it = entries_.find(key_of(schema, name));
   if (it == entries_.end()) {
     ++stats_.misses;
@@ -74,6 +82,7 @@ EntryPtr ModuleStore::lookup(const std::string& schema, const std::string& name)
 }
 
 EntryPtr ModuleStore::lookup_scaffold(const std::string& schema, const std::vector<std::string>& members) {
+  std::lock_guard<std::recursive_mutex> g(mu_);
   auto it = entries_.find(key_of(schema, scaffold_id(members)));
   if (it == entries_.end()) return nullptr;
   ++stats_.hits;
@@ -82,11 +91,20 @@ EntryPtr ModuleStore::lookup_scaffold(const std::string& schema, const std::vect
 }
 
 void ModuleStore::touch(const std::string& schema, const std::string& name) {
+  std::lock_guard<std::recursive_mutex> g(mu_);
   auto it = entries_.find(key_of(schema, name));
   if (it != entries_.end()) it->second->last_used = ++clock_;
 }
 
+std::vector<std::shared_ptr<const CacheEntry>> ModuleStore::snapshot() const {
+  std::lock_guard<std::recursive_mutex> g(mu_);
+  std::vector<std::shared_ptr<const CacheEntry>> out;
+  for (const auto& kv : entries_) out.push_back(kv.second);
+  return out;
+}
+
 std::string ModuleStore::stats_json() const {
+  std::lock_guard<std::recursive_mutex> g(mu_);
   nlohmann::json j;
   j["entries"] = entries_.size();
   j["bytes_used"] = {{"fast", stats_.bytes_fast}, {"slow", stats_.bytes_slow}};
@@ -119,6 +137,18 @@ CacheEntry encode_module(model::Model& m, const layout::LayoutPlan& plan, const 
   std::vector<int32_t> t32(ml.own_tokens.begin(), ml.own_tokens.end());
   m.run(t32.data(), ml.own_positions.data(), n, *kv, nullptr, nullptr, /*logit_rows=*/0);
   return finish_entry(m, plan.schema_name, name, kv, ml.own_tokens, ml.param_slots, tier);
+}
+
+CacheEntry install_module(model::Model& m, const layout::LayoutPlan& plan, const std::string& name, model::KVPtr kv,
+                          Tier tier) {
+  auto it = plan.entries.find(name);
+  if (it == plan.entries.end()) throw Error(ErrorCode::UnknownModule, "no module \"" + name + "\" in the schema");
+  const layout::ModuleLayout& ml = it->second;
+  if (!kv || kv->host || kv->n_layers != m.config().n_layers || kv->hidden != m.kv_width() || kv->dtype != m.dtype())
+    throw Error(ErrorCode::ShapeMismatch, "install_module: KV block does not belong to this model");
+  if (kv->rows != static_cast<int64_t>(ml.own_tokens.size()) || kv->positions != ml.own_positions)
+    throw Error(ErrorCode::ShapeMismatch, "install_module: KV rows/positions differ from module \"" + name + "\"'s span");
+  return finish_entry(m, plan.schema_name, name, std::move(kv), ml.own_tokens, ml.param_slots, tier);
 }
 
 int encode_schema(model::Model& m, const layout::LayoutPlan& plan, ModuleStore& store, Tier tier) {
@@ -213,15 +243,29 @@ struct In {
 };
 }  // namespace
 
+// Header hash: the config hash (reference format, so files move between implementations);
+// a tensor-parallel shard mixes its (rank, size) in, so a shard never loads into another
+// rank's model (its K/V columns are a different head range).
+static uint64_t file_hash(const model::Model& m) {
+  uint64_t h = m.config().hash();
+  if (m.tp_size() > 1)
+    h ^= model::splitmix64((static_cast<uint64_t>(m.tp_rank()) << 32) | static_cast<uint32_t>(m.tp_size()));
+  return h;
+}
+
 void ModuleStore::save(const std::string& path) const {
   model::Model& m = *model_;
+  CK(cudaSetDevice(m.device()));
   Out w(path);
   w.raw(kMagic, 4);
   w.put<uint32_t>(kVersion);
-  w.put<uint64_t>(m.config().hash());
-  w.put<uint32_t>(static_cast<uint32_t>(entries_.size()));
+  w.put<uint64_t>(file_hash(m));
+  const auto all = snapshot();
+  w.put<uint32_t>(static_cast<uint32_t>(all.size()));
   const int L = m.config().n_layers, d = m.kv_width();
-  for (const auto& [key, ep] : entries_) {
+  DeviceBuffer f32, stage;  // fp32 conversion target; device copy of a pinned-host plane
+  std::vector<float> buf;
+  for (const auto& ep : all) {  // std::map order = the reference's sorted-key order
     const CacheEntry& e = *ep;
     w.str(e.schema);
     w.str(e.name);
@@ -242,35 +286,31 @@ void ModuleStore::save(const std::string& path) const {
     for (int64_t p : e.kv->positions) w.put<int64_t>(p);
     w.put<uint32_t>(static_cast<uint32_t>(L));
     const uint64_t cnt = static_cast<uint64_t>(e.kv->rows) * d;
-    std::vector<float> buf(cnt);
-    float* dtmp = nullptr;
-    if (cnt && cudaMalloc(&dtmp, cnt * 4) != cudaSuccess) throw Error(ErrorCode::CudaError, "save: cudaMalloc");
+    buf.resize(cnt);
+    if (cnt && f32.bytes() < cnt * 4) f32.reset(cnt * 4);
+    if (cnt && e.kv->host && stage.bytes() < cnt * e.kv->elem()) stage.reset(cnt * e.kv->elem());
     for (int l = 0; l < L; ++l)
       for (int which = 0; which < 2; ++which) {
         if (cnt) {
           const void* src = e.kv->plane(l, which);
           if (e.kv->host) {
-            void* stage = nullptr;
-            cudaMalloc(&stage, cnt * e.kv->elem());
-            cudaMemcpy(stage, src, cnt * e.kv->elem(), cudaMemcpyHostToDevice);
-            kern::convert(e.kv->dtype, stage, kern::F32, dtmp, cnt, m.stream());
-            cudaStreamSynchronize(m.stream());
-            cudaFree(stage);
-          } else {
-            kern::convert(e.kv->dtype, src, kern::F32, dtmp, cnt, m.stream());
+            CK(cudaMemcpyAsync(stage.get(), src, cnt * e.kv->elem(), cudaMemcpyHostToDevice, m.stream()));
+            src = stage.get();
           }
-          cudaMemcpyAsync(buf.data(), dtmp, cnt * 4, cudaMemcpyDeviceToHost, m.stream());
-          cudaStreamSynchronize(m.stream());
+          kern::convert(e.kv->dtype, src, kern::F32, f32.get(), cnt, m.stream());
+          CK(cudaGetLastError());
+          CK(cudaMemcpyAsync(buf.data(), f32.get(), cnt * 4, cudaMemcpyDeviceToHost, m.stream()));
+          CK(cudaStreamSynchronize(m.stream()));
         }
         w.put<uint64_t>(cnt);
         w.raw(buf.data(), cnt * 4);
       }
-    if (dtmp) cudaFree(dtmp);
   }
 }
 
 void ModuleStore::load(const std::string& path) {
   model::Model& m = *model_;
+  CK(cudaSetDevice(m.device()));
   In r(path);
   char magic[4];
   r.raw(magic, 4);
@@ -279,11 +319,15 @@ void ModuleStore::load(const std::string& path) {
   if (version != kVersion)
     throw Error(ErrorCode::VersionMismatch,
                 "store version " + std::to_string(version) + ", expected " + std::to_string(kVersion));
-  if (r.get<uint64_t>() != m.config().hash())
-    throw Error(ErrorCode::ConfigHashMismatch, "store was built with a different model config");
+  if (r.get<uint64_t>() != file_hash(m))
+    throw Error(ErrorCode::ConfigHashMismatch,
+                m.tp_size() > 1 ? "store was built with a different model config or tensor-parallel shard"
+                                : "store was built with a different model config");
   const int d = m.kv_width();
   uint32_t count = r.get<uint32_t>();
   std::vector<CacheEntry> loaded;
+  DeviceBuffer f32;
+  std::vector<float> buf;
   for (uint32_t i = 0; i < count; ++i) {
     CacheEntry e;
     e.schema = r.str();
@@ -312,25 +356,24 @@ void ModuleStore::load(const std::string& path) {
     model::KVPtr kv = m.alloc_kv(np);
     kv->rows = np;
     kv->positions = pos;
-    std::vector<float> buf;
-    float* dtmp = nullptr;
+    const uint64_t want = static_cast<uint64_t>(np) * d;
+    buf.resize(want);
+    if (want && f32.bytes() < want * 4) f32.reset(want * 4);
     for (uint32_t l = 0; l < L; ++l)
       for (int which = 0; which < 2; ++which) {
         uint64_t cnt = r.get<uint64_t>();
-        if (cnt != static_cast<uint64_t>(np) * d) throw Error(ErrorCode::IoError, "bad KV plane size in store file");
-        buf.resize(cnt);
-        if (cnt) r.raw(buf.data(), cnt * 4);
-        if (cnt) {
-          if (!dtmp) cudaMalloc(&dtmp, cnt * 4);
-          cudaMemcpyAsync(dtmp, buf.data(), cnt * 4, cudaMemcpyHostToDevice, m.stream());
-          kern::convert(kern::F32, dtmp, kv->dtype, kv->plane(l, which), cnt, m.stream());
-          cudaStreamSynchronize(m.stream());
-        }
+        if (cnt != want) throw Error(ErrorCode::IoError, "bad KV plane size in store file");
+        if (!cnt) continue;
+        r.raw(buf.data(), cnt * 4);
+        CK(cudaMemcpyAsync(f32.get(), buf.data(), cnt * 4, cudaMemcpyHostToDevice, m.stream()));
+        kern::convert(kern::F32, f32.get(), kv->dtype, kv->plane(l, which), cnt, m.stream());
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(m.stream()));  // buf is reused by the next plane
       }
-    if (dtmp) cudaFree(dtmp);
     e.kv = e.tier == Tier::Slow ? m.to_host(*kv) : kv;
     loaded.push_back(std::move(e));
   }
+  std::lock_guard<std::recursive_mutex> g(mu_);
   for (auto& e : loaded) insert(std::move(e));
   stats_.hits = 0;
   stats_.misses = 0;

@@ -10,14 +10,9 @@
 #include <set>
 
 #include "../kernels/kernels.cuh"
+#include "cuda_check.hpp"
 #include "json.hpp"
 
-#define CK(x)                                                                                        \
-  do {                                                                                               \
-    cudaError_t e_ = (x);                                                                            \
-    if (e_ != cudaSuccess)                                                                           \
-      throw ::pcb::Error(::pcb::ErrorCode::CudaError, std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
 
 namespace pcb::engine {
 
@@ -384,7 +379,8 @@ model::KVPtr concat_kv(model::Model& m, const std::vector<cache::EntryPtr>& entr
   return out;
 }
 
-ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::ModuleStore& store) {
+namespace {
+ServeResponse serve_unlocked(const ServeRequest& req, const Schema& schema, cache::ModuleStore& store) {
   auto t0 = Clock::now();
   model::Model& m = store.model();
   CK(cudaSetDevice(m.device()));
@@ -464,6 +460,10 @@ ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::Module
   }
   CK(cudaEventRecord(sc.ev[1], m.stream()));
   if (up.tokens.empty()) {
+    // no forward consumes the slow tier's per-layer events: the side stream's uploads into
+    // the arena must land before the next request reuses it, and the events are dropped
+    if (slow) CK(cudaStreamWaitEvent(m.stream(), sc.layer_ev[m.config().n_layers - 1], 0));
+    m.set_layer_events(nullptr, 0);
     CK(cudaStreamSynchronize(m.stream()));
     resp.timings.ttft_us = us_since(t0);
     return resp;
@@ -476,9 +476,16 @@ ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::Module
   resp.timings.copy_us = slow ? ms * 1000.0 : 0.0;
   return resp;
 }
+}  // namespace
+
+ServeResponse serve(const ServeRequest& req, const Schema& schema, cache::ModuleStore& store) {
+  std::lock_guard<std::mutex> g(store.serve_mutex());
+  return serve_unlocked(req, schema, store);
+}
 
 std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, const Schema& schema,
                                        cache::ModuleStore& store, int micro_batch) {
+  std::lock_guard<std::mutex> g(store.serve_mutex());
   model::Model& m = store.model();
   CK(cudaSetDevice(m.device()));
   const int V = m.config().vocab_size;
@@ -506,7 +513,7 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
       // decode past the first token, baselines and scaffolds take the single-request path
       if (!req.use_cache || req.use_scaffolds || req.max_new_tokens != 1) {
         if (segs_busy) CK(cudaEventSynchronize(segs_busy));  // serve() reuses the segment list
-        out[i] = serve(req, schema, store);
+        out[i] = serve_unlocked(req, schema, store);
         continue;
       }
       require_valid(req.prompt, schema.doc);

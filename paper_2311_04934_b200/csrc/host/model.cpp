@@ -14,14 +14,9 @@
 #include <mutex>
 
 #include "../kernels/kernels.cuh"
+#include "cuda_check.hpp"
 #include "json.hpp"
 
-#define CK(x)                                                                                        \
-  do {                                                                                               \
-    cudaError_t e_ = (x);                                                                            \
-    if (e_ != cudaSuccess)                                                                           \
-      throw ::pcb::Error(::pcb::ErrorCode::CudaError, std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
 
 namespace pcb::model {
 

@@ -15,6 +15,25 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Greedy-token parity accounting (report how many cases used the tie exemption)."""
+    from tests.util import GREEDY, SEQ
+
+    if not GREEDY["checked"] and not SEQ["checked"]:
+        return
+    tr = terminalreporter
+    tr.write_sep("-", "greedy-token parity")
+    tr.write_line(f"first tokens compared: {GREEDY['checked']}, identical: {GREEDY['identical']}, "
+                  f"tie-exempt: {len(GREEDY['exempt'])}")
+    for e in GREEDY["exempt"]:
+        tr.write_line(f"  exempt {e}")
+    if SEQ["checked"]:
+        tr.write_line(f"bf16 decoded sequences compared: {SEQ['checked']}, diverged after the first token: "
+                      f"{len(SEQ['diverged'])}")
+        for e in SEQ["diverged"][:20]:
+            tr.write_line(f"  {e}")
+
+
 def _ensure_built():
     lib = os.path.join(ROOT, "paper_2311_04934_b200", "lib", "libpcb200.so")
     if not os.path.exists(lib):

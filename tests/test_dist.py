@@ -111,3 +111,20 @@ def test_tp_decomposition_gloo_world2():
         assert p.exitcode == 0
     assert all(o[1] for o in out)
     assert [o[2] for o in out] == [(0, 4), (4, 8)]
+
+
+def test_bench_gpus2_relaunches_two_ranks_dry_run():
+    """`bench.py --gpus 2` without torchrun re-launches itself with one process per rank; in the
+    gloo dry run rank 0 prints exactly one JSON line that reports both ranks."""
+    import json
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                          "--steps", "4", "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["dry_run"] and line["steps"] == 4
+    assert line["c4_requests_rank0"] == 256  # config 4 scales with the ranks: 256 requests per GPU

@@ -1,0 +1,231 @@
+"""The benchmarked bf16 head-dim-128 path pinned to the reference (round-2 fixtures).
+
+Every expected value comes from the unmodified reference (tests/golden/make_golden_parity.py):
+  * configs[0] exactly as BASELINE.json states it (fp32 bit-level bar, 32 greedy tokens);
+  * the golden serve corpus through a head-dim-128 bf16 model -- single requests read their
+    modules in place (chain attention phase, zero-copy segments), the copy path, and
+    micro-batches of 4 (batched attention kernel);
+  * configs[2]'s shape at narrow width: three ~5.5K-row modules precomputed by the CTA-pair GEMM +
+    causal tcgen05 attention, served with 128 uncached tokens;
+  * Llama-2-7B width (d 4096, 32 heads, vocab 32000): suffixes of 64 tokens over 2048/4096
+    cached rows through the chain (zero-copy and copy), the standalone attention kernel, and
+    a 4-request micro-batch (CTA-pair GEMMs at M = 256, batched attention); a 320-row prefill.
+Bars (north star): fp32 max-abs <= 1e-3; bf16 logits rel-err <= 2e-2 with the same greedy token
+(tie exemptions are counted and printed in the terminal summary).
+Reference semantics: Model::run model.cpp:304-443, serve engine.cpp:187-258.
+"""
+import base64
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2311_04934_b200 as pcb
+from tests import parity_cases as pc
+from tests.util import BF16_REL, F32_TOL, rel, record_sequence, same_greedy_token
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def f32(b):
+    return np.frombuffer(base64.b64decode(b), np.float32)
+
+
+@pytest.fixture(scope="module")
+def parity():
+    with open(os.path.join(GOLD, "parity.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def w7b_gold():
+    return dict(np.load(os.path.join(GOLD, "parity_w7b.npz")))
+
+
+def check_bf16(got, want, label):
+    r = rel(got, want)
+    assert r <= BF16_REL, f"{label}: rel {r:.3e}"
+    assert same_greedy_token(got, want, label), label
+    return r
+
+
+# ---------------------------------------------------------------------------
+# configs[0] as stated: 68-token system module + 512-token document + 32 uncached
+# ---------------------------------------------------------------------------
+def test_config1_fp32_matches_reference(parity):
+    g = parity["c1"]
+    schema_text, prompt_text = pc.c1_workload()
+    m = pcb.Model(pc.C1, dtype=pcb.F32)
+    schema = pcb.Schema.parse(schema_text)
+    store = pcb.ModuleStore(m)
+    assert store.encode_schema(schema) == 2
+    got = {"cached": pcb.serve(store, schema, prompt_text, 32),
+           "baseline": pcb.serve(store, schema, prompt_text, 32, use_cache=False),
+           "oracle": pcb.oracle_serve(m, schema, prompt_text, 32)}
+    for mode, r in got.items():
+        want = g[mode]
+        assert r.cache_report["cached_token_count"] == want["report"]["cached_token_count"], mode
+        assert r.cache_report["uncached_token_count"] == want["report"]["uncached_token_count"], mode
+        assert r.output_tokens == want["tokens"], mode  # 32 greedy tokens identical
+        err = float(np.max(np.abs(r.first_token_logits - f32(want["logits"]))))
+        assert err <= F32_TOL, (mode, err)
+    assert got["cached"].cache_report["cached_token_count"] == 580
+
+
+def test_config1_bf16_matches_reference(parity):
+    g = parity["c1"]
+    schema_text, prompt_text = pc.c1_workload()
+    m = pcb.Model(pc.C1, dtype=pcb.BF16)
+    schema = pcb.Schema.parse(schema_text)
+    store = pcb.ModuleStore(m)
+    store.encode_schema(schema)
+    for mode, r in (("cached", pcb.serve(store, schema, prompt_text, 32)),
+                    ("baseline", pcb.serve(store, schema, prompt_text, 32, use_cache=False))):
+        check_bf16(r.first_token_logits, f32(g[mode]["logits"]), f"c1 bf16 {mode}")
+        record_sequence(r.output_tokens, g[mode]["tokens"], f"c1 bf16 {mode}")
+
+
+# ---------------------------------------------------------------------------
+# golden corpus through head-dim-128 heads
+# ---------------------------------------------------------------------------
+def _corpus_inputs(host_golden, name):
+    if name.startswith("corpus:"):
+        c = next(c for c in host_golden["corpus"] if c["name"] == name[7:])
+        return pcb.Schema.parse(c["schema_text"]), pcb.Prompt.parse(c["prompt_text"])
+    seed = int(name.split(":")[1])
+    c = next(c for c in host_golden["random_case"] if c["seed"] == seed)
+    return pcb.Schema.from_ast(c["schema"]), pcb.Prompt.from_ast(c["prompt"])
+
+
+def test_hd128_corpus_matches_reference(parity, host_golden):
+    """Zero-copy (modules read in place by the chain attention phase), the assembly copy path,
+    and serve_batch micro-batches of 4 (batched tcgen05 attention), each against the reference."""
+    m = pcb.Model(pc.H128, dtype=pcb.BF16)
+    worst, n_zc = 0.0, 0
+    for case in parity["h128"]:
+        schema, prompt = _corpus_inputs(host_golden, case["name"])
+        want = f32(case["logits"])
+        store = pcb.ModuleStore(m)
+        store.encode_schema(schema)
+        for zc in (1, 0):
+            m.set_option("zero_copy", zc)
+            r = pcb.serve(store, schema, prompt, 8)
+            assert r.cache_report["cached_token_count"] == case["report"]["cached_token_count"]
+            assert r.cache_report["uncached_token_count"] == case["report"]["uncached_token_count"]
+            worst = max(worst, check_bf16(r.first_token_logits, want, f"h128 {case['name']} zc={zc}"))
+            record_sequence(r.output_tokens, case["tokens"], f"h128 {case['name']} zc={zc}")
+        m.set_option("zero_copy", 1)
+        for b in pcb.serve_batch(store, schema, [prompt] * 4, micro_batch=4):
+            worst = max(worst, check_bf16(b.first_token_logits, want, f"h128 {case['name']} batch"))
+        n_zc += 1
+    assert n_zc >= 50
+    print(f"hd128 corpus: {n_zc} cases x (zero-copy, copy, batch of 4): worst rel {worst:.3e}")
+
+
+# ---------------------------------------------------------------------------
+# configs[2] shape: 3 modules, 16,384 cached rows + 128 uncached
+# ---------------------------------------------------------------------------
+def test_long_context_matches_reference(parity):
+    g = parity["long"]
+    schema_text, prompt_text = pc.long_workload()
+    m = pcb.Model(pc.H128_LONG, dtype=pcb.BF16)
+    schema = pcb.Schema.parse(schema_text)
+    store = pcb.ModuleStore(m)
+    assert store.encode_schema(schema) == 3
+    # module precompute (CTA-pair GEMMs + causal tcgen05 attention over ~5.5K rows) vs the reference
+    kv = store.lookup("bench", "doc1")
+    rows = g["doc1_rows"]
+    for which, key in ((0, "doc1_k1"), (1, "doc1_v1")):
+        got = kv.layer(1, which)[rows]
+        want = f32(g[key]).reshape(len(rows), -1)
+        assert rel(got, want) <= BF16_REL, (key, rel(got, want))
+    for zc in (1, 0):
+        m.set_option("zero_copy", zc)
+        r = pcb.serve(store, schema, prompt_text, 4)
+        assert r.cache_report["cached_token_count"] == 16384
+        assert r.cache_report["uncached_token_count"] == 128
+        check_bf16(r.first_token_logits, f32(g["logits"]), f"long zc={zc}")
+        record_sequence(r.output_tokens, g["tokens"], f"long zc={zc}")
+    m.set_option("zero_copy", 1)
+
+
+# ---------------------------------------------------------------------------
+# Llama-2-7B width
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def w7b():
+    m = pcb.Model(pc.W7B, dtype=pcb.BF16)
+    schema = pcb.Schema.parse(pc.W7B_SCHEMA)
+    store = pcb.ModuleStore(m)
+    mods = []
+    for i in range(2):
+        k, v, pos = pc.w7b_module_kv(i)
+        kv = m.upload_kv(k, v, pos)
+        store.put_kv(schema, f"doc{i}", kv)
+        mods.append((k, v, pos, kv))
+    return m, schema, store, mods
+
+
+def test_w7b_store_holds_the_synthetic_rows_exactly(w7b):
+    m, schema, store, mods = w7b
+    for i, (k, v, pos, _) in enumerate(mods):
+        got = store.lookup("w7b", f"doc{i}")
+        assert np.array_equal(got.positions(), pos)
+        assert np.array_equal(got.layer(1, 0), k[1]) and np.array_equal(got.layer(0, 1), v[0])  # bf16-exact
+
+
+def test_w7b_serve_zero_copy_and_copy_match_reference(w7b, w7b_gold):
+    """Single requests: zero-copy (chain attention phase reads doc0/doc1 in place), the assembly
+    copy + chain attention, and the standalone k_attn_tc<128> (chain_attn off)."""
+    m, schema, store, _ = w7b
+    for variant, opts in (("zero-copy", {}), ("copy", {"zero_copy": 0}),
+                          ("standalone-attention", {"zero_copy": 0, "chain_attn": 0})):
+        for k, v in opts.items():
+            m.set_option(k, v)
+        for i, p in enumerate(pc.W7B_PROMPTS):
+            r = pcb.serve(store, schema, p, 1)
+            assert r.cache_report["uncached_token_count"] == 64
+            check_bf16(r.first_token_logits, w7b_gold[f"req{i}_last"], f"w7b {variant} req{i}")
+        for k in opts:
+            m.set_option(k, 1)
+
+
+def test_w7b_forward_all_rows_match_reference(w7b, w7b_gold):
+    """Model::forward over an uploaded 4096-row past: logits of every suffix row are computed
+    (reference semantics); rows 0 and 63 vs the reference."""
+    m, _, _, mods = w7b
+    k = np.concatenate([mods[0][0], mods[1][0]], axis=1)
+    v = np.concatenate([mods[0][1], mods[1][1]], axis=1)
+    pos = np.concatenate([mods[0][2], mods[1][2]])
+    past = m.upload_kv(k, v, pos)
+    logits, new_kv = m.forward(w7b_gold["req0_tokens"], w7b_gold["req0_positions"], past=past)
+    check_bf16(logits[0], w7b_gold["req0_row0"], "w7b forward row0")
+    check_bf16(logits[-1], w7b_gold["req0_last"], "w7b forward row63")
+    assert new_kv.rows == 64
+
+
+def test_w7b_micro_batch_matches_reference(w7b, w7b_gold):
+    """serve_batch of the 4 requests in one micro-batch: M = 256 suffix rows through the CTA-pair
+    GEMMs, batched attention reading each request's modules in place (2 or 1 segments)."""
+    m, schema, store, _ = w7b
+    for zc in (1, 0):
+        m.set_option("zero_copy", zc)
+        res = pcb.serve_batch(store, schema, pc.W7B_PROMPTS, micro_batch=4)
+        for i, r in enumerate(res):
+            check_bf16(r.first_token_logits, w7b_gold[f"req{i}_last"], f"w7b batch zc={zc} req{i}")
+    m.set_option("zero_copy", 1)
+
+
+def test_w7b_prefill_matches_reference(w7b, w7b_gold):
+    """320-row prefill without past (module precompute / full-prefill path): CTA-pair GEMMs with a
+    ragged 64-row tail and causal tcgen05 attention; logits and layer-1 K/V rows."""
+    m, _, _, _ = w7b
+    toks = pc.w7b_prefill_tokens()
+    logits, kv = m.forward(toks, list(range(len(toks))))
+    check_bf16(logits[0], w7b_gold["prefill_row0"], "w7b prefill row0")
+    check_bf16(logits[-1], w7b_gold["prefill_last"], "w7b prefill last")
+    rows = w7b_gold["prefill_kv_rows"]
+    assert rel(kv.layer(1, 0)[rows], w7b_gold["prefill_k1"]) <= BF16_REL
+    assert rel(kv.layer(1, 1)[rows], w7b_gold["prefill_v1"]) <= BF16_REL

@@ -9,7 +9,7 @@ import pytest
 
 import paper_2311_04934_b200 as pcb
 from oracle.oracle import TINY, Ref, RefModel, max_rel_diff
-from tests.util import BF16_REL, F32_TOL, rel, same_greedy_token
+from tests.util import BF16_REL, F32_TOL, record_sequence, rel, same_greedy_token
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -71,8 +71,10 @@ def test_serve_matches_reference_goldens(m32, m16, host_golden, numeric_golden):
                     assert r.output_tokens == want["tokens"], (case["name"], mode)
                 else:
                     worst16 = max(worst16, rel(r.first_token_logits, wl))
-                    assert same_greedy_token(r.first_token_logits, wl), (case["name"], mode)
+                    assert same_greedy_token(r.first_token_logits, wl, f"tiny bf16 {case['name']} {mode}"), \
+                        (case["name"], mode)
                     bad16 += r.output_tokens != want["tokens"]
+                    record_sequence(r.output_tokens, want["tokens"], f"tiny bf16 {case['name']} {mode}")
     assert worst32 <= F32_TOL, worst32
     assert worst16 <= BF16_REL, worst16
     print(f"f32 worst max-abs {worst32:.2e}; bf16 worst rel {worst16:.2e}; bf16 full-sequence mismatches {bad16}")
@@ -285,8 +287,10 @@ def test_zero_copy_on_reference_corpus(host_golden, numeric_golden):
         m.set_option("zero_copy", 1)
         o = pcb.oracle_serve(m, schema, prompt, 8)
         assert out[1].cache_report == out[0].cache_report, case["name"]
-        assert same_greedy_token(out[1].first_token_logits, out[0].first_token_logits), case["name"]
-        assert same_greedy_token(out[1].first_token_logits, o.first_token_logits), case["name"]
+        assert same_greedy_token(out[1].first_token_logits, out[0].first_token_logits,
+                                 f"zc-vs-copy {case['name']}"), case["name"]
+        assert same_greedy_token(out[1].first_token_logits, o.first_token_logits,
+                                 f"zc-vs-device-oracle {case['name']}"), case["name"]
         worst = max(worst, rel(out[1].first_token_logits, out[0].first_token_logits),
                     rel(out[1].first_token_logits, o.first_token_logits))
         n_cases += 1
