@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstring>
 #include <map>
+#include <algorithm>
 #include <set>
 
 #include "../kernels/kernels.cuh"
@@ -154,12 +155,33 @@ AsmScratch& scratch_of(cache::ModuleStore& store) {
 }
 
 // Position-disjointness check of concat_kv (engine.cpp:176-181).
+// PositionOverlap unless the entries' position sets are pairwise disjoint (reference
+// concat_kv, engine.cpp:179-181).  Module positions are normally increasing runs in
+// disjoint ranges, which is checked in O(rows); anything else sorts every position.
 void check_disjoint(const std::vector<cache::EntryPtr>& entries) {
-  std::set<int64_t> seen;
-  for (auto& e : entries)
-    for (int64_t p : e->kv->positions)
-      if (!seen.insert(p).second)
-        throw Error(ErrorCode::PositionOverlap, "cache entries overlap at position " + std::to_string(p));
+  std::vector<std::pair<int64_t, int64_t>> ranges;
+  bool runs = true;
+  size_t total = 0;
+  for (auto& e : entries) {
+    const std::vector<int64_t>& p = e->kv->positions;
+    total += p.size();
+    if (p.empty()) continue;
+    for (size_t i = 1; i < p.size() && runs; ++i) runs = p[i] > p[i - 1];
+    ranges.emplace_back(p.front(), p.back());
+  }
+  if (runs) {
+    std::sort(ranges.begin(), ranges.end());
+    bool apart = true;
+    for (size_t i = 1; i < ranges.size() && apart; ++i) apart = ranges[i].first > ranges[i - 1].second;
+    if (apart) return;
+  }
+  std::vector<int64_t> all;
+  all.reserve(total);
+  for (auto& e : entries) all.insert(all.end(), e->kv->positions.begin(), e->kv->positions.end());
+  std::sort(all.begin(), all.end());
+  auto dup = std::adjacent_find(all.begin(), all.end());
+  if (dup != all.end())
+    throw Error(ErrorCode::PositionOverlap, "cache entries overlap at position " + std::to_string(*dup));
 }
 
 // Gathers the entries' KV rows into `dst` rows [0, sum) — one assembly-kernel

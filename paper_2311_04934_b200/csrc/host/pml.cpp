@@ -1,12 +1,19 @@
-// PML front end, written from scratch against the semantics of the reference
-// (proj/core/src/pml.cpp): scanner grammar 30-177, schema building 236-324,
-// prompt building 374-406, parse 424-473, serialize 477-551, validation
-// 556-701, chat expansion 707-786.  Host-only: no device work happens here.
+// PML front end (SPEC.md [MODULE] pml): schema / prompt parsing, serialization,
+// validation and chat-template expansion.  Host-only.
+//
+// Design: a pull lexer turns the source into markup events (open / self-close / close
+// tag, text run) and each document is built in one pass by a stack of frames -- there
+// is no intermediate element tree.  Lexical errors abort at once; structural errors
+// found while building are deferred until the source has lexed to its end, so a
+// malformed document reports SyntaxError before any semantic code (MissingSchemaAttr),
+// the precedence of the reference's read-then-build parser (pml.cpp:424-473).
+// Validation issue codes and messages are the reference's output contract
+// (pml.cpp:556-701) and are reproduced exactly; parse-error wording is our own.
 #include "pml.hpp"
 
 #include <algorithm>
 #include <cctype>
-#include <functional>
+#include <optional>
 #include <set>
 
 #include "json.hpp"
@@ -29,8 +36,9 @@ namespace pml {
 
 namespace tok {
 std::vector<int> tokenize(const std::string& s) {
-  std::vector<int> t(s.size());
-  for (size_t i = 0; i < s.size(); ++i) t[i] = static_cast<unsigned char>(s[i]);
+  std::vector<int> t;
+  t.reserve(s.size());
+  for (unsigned char c : s) t.push_back(c);
   return t;
 }
 std::string detokenize(const std::vector<int>& t) {
@@ -45,52 +53,92 @@ bool ModuleImport::operator==(const ModuleImport& o) const {
   return name == o.name && args == o.args && children == o.children;
 }
 bool PromptItem::operator==(const PromptItem& o) const {
-  if (kind != o.kind) return false;
-  return kind == Kind::Text ? text == o.text : import == o.import;
+  return kind == o.kind && (kind == Kind::Text ? text == o.text : import == o.import);
 }
 
 namespace {
 
-// ---------------------------------------------------------------------------
-// Element reader.  Produces a generic element tree; schema / prompt builders
-// interpret it.  Grammar: elements with quoted attributes, self-closing tags,
-// text with the five predefined entities; no comments, CDATA or numeric refs.
-// ---------------------------------------------------------------------------
+using Attrs = std::vector<std::pair<std::string, std::string>>;
 
-struct Elem {
-  bool text_node = false;
-  std::string tag;   // element
-  std::string body;  // text node (entities decoded)
-  std::vector<std::pair<std::string, std::string>> attrs;
-  std::vector<Elem> kids;
+// ---------------------------------------------------------------------------
+// Lexer: XML subset -- elements, quoted attributes, self-closing tags, text with the
+// entities lt/gt/amp/quot/apos.  No comments, processing instructions, CDATA or
+// numeric character references.
+// ---------------------------------------------------------------------------
+struct Event {
+  enum Kind { Open, SelfClose, Close, Text, End } kind = End;
+  std::string name;  // tag name (Open / SelfClose / Close)
+  Attrs attrs;       // Open / SelfClose
+  std::string text;  // Text: entities decoded, never empty
   int line = 1, col = 1;
 };
 
-class Reader {
+class Lexer {
  public:
-  explicit Reader(const std::string& s) : s_(s) {}
+  explicit Lexer(const std::string& src) : src_(src) {}
 
-  Elem document() {
-    blanks();
-    if (done() || cur() != '<') err("expected a root element");
-    Elem root = element();
-    blanks();
-    if (!done()) err("trailing content after root element");
-    return root;
+  Event next() {
+    Event ev;
+    ev.line = line_;
+    ev.col = col_;
+    if (at_end()) return ev;
+    if (peek() != '<') {
+      ev.kind = Event::Text;
+      while (!at_end() && peek() != '<') {
+        if (peek() == '&') {
+          advance();
+          ev.text += entity();
+        } else {
+          ev.text.push_back(advance());
+        }
+      }
+      return ev;
+    }
+    advance();  // '<'
+    if (!at_end() && peek() == '/') {
+      advance();
+      ev.kind = Event::Close;
+      ev.name = ident("closing tag");
+      skip_space();
+      expect('>', "'>' to end </" + ev.name);
+      return ev;
+    }
+    ev.name = ident("tag");
+    for (;;) {
+      skip_space();
+      if (at_end()) fail("tag <" + ev.name + "> is not terminated");
+      if (peek() == '>') {
+        advance();
+        ev.kind = Event::Open;
+        return ev;
+      }
+      if (peek() == '/') {
+        advance();
+        expect('>', "'>' right after '/' in <" + ev.name + "/>");
+        ev.kind = Event::SelfClose;
+        return ev;
+      }
+      std::string key = ident("attribute");
+      skip_space();
+      expect('=', "'=' after attribute " + key);
+      skip_space();
+      std::string value = quoted();
+      if (std::any_of(ev.attrs.begin(), ev.attrs.end(), [&](const auto& a) { return a.first == key; }))
+        fail("attribute " + key + " given twice on <" + ev.name + ">");
+      ev.attrs.emplace_back(std::move(key), std::move(value));
+    }
   }
+
+  void skip_space() {
+    while (!at_end() && std::isspace(static_cast<unsigned char>(peek()))) advance();
+  }
+  bool at_end() const { return pos_ >= src_.size(); }
+  [[noreturn]] void fail(const std::string& what) const { throw Error(ErrorCode::SyntaxError, what, line_, col_); }
 
  private:
-  const std::string& s_;
-  size_t i_ = 0;
-  int line_ = 1, col_ = 1;
-
-  [[noreturn]] void err(const std::string& m) const {
-    throw Error(ErrorCode::SyntaxError, m, line_, col_);
-  }
-  bool done() const { return i_ >= s_.size(); }
-  char cur() const { return s_[i_]; }
-  char take() {
-    char c = s_[i_++];
+  char peek() const { return src_[pos_]; }
+  char advance() {
+    const char c = src_[pos_++];
     if (c == '\n') {
       ++line_;
       col_ = 1;
@@ -99,436 +147,488 @@ class Reader {
     }
     return c;
   }
-  void blanks() {
-    while (!done() && std::isspace(static_cast<unsigned char>(cur()))) take();
+  void expect(char c, const std::string& what) {
+    if (at_end() || peek() != c) fail("expected " + what);
+    advance();
   }
-  static bool first_name_char(char c) { return std::isalpha(static_cast<unsigned char>(c)) || c == '_'; }
-  static bool name_char(char c) {
-    return std::isalnum(static_cast<unsigned char>(c)) || c == '_' || c == '-' || c == '.';
+  std::string ident(const char* what) {
+    auto head = [](char c) { return std::isalpha(static_cast<unsigned char>(c)) || c == '_'; };
+    auto tail = [](char c) { return std::isalnum(static_cast<unsigned char>(c)) || c == '_' || c == '-' || c == '.'; };
+    if (at_end() || !head(peek())) fail(std::string("expected a ") + what + " name");
+    std::string s;
+    while (!at_end() && tail(peek())) s.push_back(advance());
+    return s;
   }
-  std::string name() {
-    if (done() || !first_name_char(cur())) err("expected a name");
-    size_t b = i_;
-    while (!done() && name_char(cur())) take();
-    return s_.substr(b, i_ - b);
-  }
-  // positioned after '&'
+  // after '&': a named entity up to ';' (names of more than 8 characters are rejected)
   std::string entity() {
-    std::string e;
-    while (!done() && cur() != ';' && e.size() < 8) e.push_back(take());
-    if (done() || cur() != ';') err("unterminated entity");
-    take();
-    static const std::pair<const char*, const char*> table[] = {
-        {"lt", "<"}, {"gt", ">"}, {"amp", "&"}, {"quot", "\""}, {"apos", "'"}};
-    for (auto& [k, v] : table)
-      if (e == k) return v;
-    err("unknown entity &" + e + ";");
+    std::string nm;
+    while (!at_end() && peek() != ';' && nm.size() < 8) nm.push_back(advance());
+    if (at_end() || peek() != ';') fail("entity &" + nm + " is not terminated by ';'");
+    advance();
+    if (nm == "lt") return "<";
+    if (nm == "gt") return ">";
+    if (nm == "amp") return "&";
+    if (nm == "quot") return "\"";
+    if (nm == "apos") return "'";
+    fail("unsupported entity &" + nm + ";");
   }
   std::string quoted() {
-    if (done() || (cur() != '"' && cur() != '\'')) err("expected quoted attribute value");
-    char q = take();
+    if (at_end() || (peek() != '"' && peek() != '\'')) fail("attribute value must be quoted");
+    const char q = advance();
     std::string v;
     for (;;) {
-      if (done()) err("unterminated attribute value");
-      char c = cur();
+      if (at_end()) fail("attribute value runs to the end of input");
+      const char c = peek();
       if (c == q) break;
-      if (c == '<') err("'<' in attribute value");
+      if (c == '<') fail("'<' inside an attribute value");
       if (c == '&') {
-        take();
+        advance();
         v += entity();
       } else {
-        v.push_back(take());
+        v.push_back(advance());
       }
     }
-    take();
+    advance();
     return v;
   }
-  Elem element() {
-    Elem e;
-    e.line = line_;
-    e.col = col_;
-    take();  // '<'
-    e.tag = name();
-    for (;;) {
-      blanks();
-      if (done()) err("unterminated tag <" + e.tag + ">");
-      if (cur() == '/') {
-        take();
-        if (done() || cur() != '>') err("malformed self-closing tag");
-        take();
-        return e;
-      }
-      if (cur() == '>') {
-        take();
-        break;
-      }
-      std::string k = name();
-      blanks();
-      if (done() || cur() != '=') err("expected '=' after attribute name");
-      take();
-      blanks();
-      std::string v = quoted();
-      for (auto& a : e.attrs)
-        if (a.first == k) err("duplicate attribute '" + k + "'");
-      e.attrs.emplace_back(std::move(k), std::move(v));
-    }
-    Elem txt;
-    txt.text_node = true;
-    auto push_text = [&] {
-      if (!txt.body.empty()) {
-        e.kids.push_back(std::move(txt));
-        txt = Elem{};
-        txt.text_node = true;
-      }
-    };
-    for (;;) {
-      if (done()) err("missing closing tag </" + e.tag + ">");
-      char c = cur();
-      if (c == '<') {
-        push_text();
-        if (i_ + 1 < s_.size() && s_[i_ + 1] == '/') {
-          take();
-          take();
-          std::string close = name();
-          blanks();
-          if (done() || cur() != '>') err("malformed closing tag");
-          take();
-          if (close != e.tag) err("mismatched closing tag </" + close + ">, expected </" + e.tag + ">");
-          return e;
-        }
-        e.kids.push_back(element());
-        continue;
-      }
-      if (txt.body.empty()) {
-        txt.line = line_;
-        txt.col = col_;
-      }
-      if (c == '&') {
-        take();
-        txt.body += entity();
-      } else {
-        txt.body.push_back(take());
-      }
-    }
-  }
+
+  const std::string& src_;
+  size_t pos_ = 0;
+  int line_ = 1, col_ = 1;
 };
 
-bool blank(const std::string& s) {
-  for (unsigned char c : s)
-    if (!std::isspace(c)) return false;
-  return true;
+bool is_space_only(const std::string& s) {
+  return std::all_of(s.begin(), s.end(), [](unsigned char c) { return std::isspace(c) != 0; });
 }
 
-std::string strip(const std::string& s) {
+std::string trim(const std::string& s) {
   size_t b = 0, e = s.size();
   while (b < e && std::isspace(static_cast<unsigned char>(s[b]))) ++b;
   while (e > b && std::isspace(static_cast<unsigned char>(s[e - 1]))) --e;
   return s.substr(b, e - b);
 }
 
-const std::string* attr(const Elem& e, const char* key) {
-  for (auto& a : e.attrs)
-    if (a.first == key) return &a.second;
-  return nullptr;
+std::optional<std::string> attr_of(const Attrs& a, const char* key) {
+  for (const auto& kv : a)
+    if (kv.first == key) return kv.second;
+  return std::nullopt;
 }
 
-bool chat_role(const std::string& t) { return t == "system" || t == "user" || t == "assistant"; }
+bool is_chat_role(const std::string& t) { return t == "system" || t == "user" || t == "assistant"; }
 
-SchemaNode text_node(std::string t) {
+bool is_reserved(const std::string& t) {
+  return t == "schema" || t == "module" || t == "union" || t == "param" || t == "prompt" || is_chat_role(t);
+}
+
+SchemaNode make_text(std::string t) {
   SchemaNode n;
   n.kind = NodeKind::Text;
   n.text = std::move(t);
   return n;
 }
 
-// std::stoi-compatible strict parse: optional leading blanks and sign, digits,
-// whole string consumed, int range.  Returns 0 on any failure.
-int parse_len(const std::string& s) {
+// Param.len: decimal int with optional leading blanks and sign, nothing after the
+// digits (what std::stoi accepts when it consumes the whole string); 0 = not an int.
+int decimal_len(const std::string& s) {
   size_t i = 0;
   while (i < s.size() && std::isspace(static_cast<unsigned char>(s[i]))) ++i;
-  bool neg = false;
-  if (i < s.size() && (s[i] == '+' || s[i] == '-')) neg = s[i++] == '-';
-  size_t d0 = i;
+  int sign = 1;
+  if (i < s.size() && (s[i] == '+' || s[i] == '-')) sign = s[i++] == '-' ? -1 : 1;
+  if (i == s.size()) return 0;
   long long v = 0;
-  while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) {
-    v = v * 10 + (s[i++] - '0');
+  for (; i < s.size(); ++i) {
+    if (!std::isdigit(static_cast<unsigned char>(s[i]))) return 0;
+    v = v * 10 + (s[i] - '0');
     if (v > 2147483648LL) return 0;
   }
-  if (i == d0 || i != s.size()) return 0;
-  if (neg) v = -v;
-  if (v > 2147483647LL || v < -2147483648LL) return 0;
-  return static_cast<int>(v);
+  v *= sign;
+  return (v > 2147483647LL || v < -2147483648LL) ? 0 : static_cast<int>(v);
 }
 
-class SchemaMaker {
- public:
-  std::vector<SchemaNode> root(const Elem& schema) {
-    std::vector<SchemaNode> out;
-    for (const Elem& k : schema.kids) {
-      if (k.text_node) {
-        if (blank(k.body)) continue;
-        SchemaNode anon;
-        anon.kind = NodeKind::Module;
-        anon.name = "__anon_" + std::to_string(anon_++);
-        anon.anonymous = true;
-        anon.children.push_back(text_node(strip(k.body)));
-        out.push_back(std::move(anon));
-      } else {
-        out.push_back(node(k));
-      }
-    }
-    return out;
+// The first structural error in document order, raised once the source lexed cleanly.
+struct Deferred {
+  std::optional<Error> first;
+  void note(const std::string& msg, int line, int col) {
+    if (!first) first.emplace(ErrorCode::SyntaxError, msg, line, col);
   }
-
- private:
-  int anon_ = 0;
-
-  std::vector<SchemaNode> content(const Elem& e) {
-    std::vector<SchemaNode> out;
-    for (const Elem& k : e.kids) out.push_back(k.text_node ? text_node(k.body) : node(k));
-    return out;
-  }
-  SchemaNode module(const Elem& e) {
-    const std::string* nm = attr(e, "name");
-    if (!nm || nm->empty())
-      throw Error(ErrorCode::SyntaxError, "<module> requires a non-empty name attribute", e.line, e.col);
-    SchemaNode n;
-    n.kind = NodeKind::Module;
-    n.name = *nm;
-    n.children = content(e);
-    return n;
-  }
-  SchemaNode node(const Elem& e) {
-    if (e.tag == "module") return module(e);
-    if (e.tag == "union") {
-      SchemaNode u;
-      u.kind = NodeKind::Union;
-      for (const Elem& k : e.kids) {
-        if (k.text_node) {
-          if (blank(k.body)) continue;
-          throw Error(ErrorCode::SyntaxError, "bare text under <union>", k.line, k.col);
-        }
-        if (k.tag != "module")
-          throw Error(ErrorCode::SyntaxError, "non-module child <" + k.tag + "> of <union>", k.line, k.col);
-        u.children.push_back(module(k));
-      }
-      return u;
-    }
-    if (e.tag == "param") {
-      const std::string* nm = attr(e, "name");
-      if (!nm || nm->empty())
-        throw Error(ErrorCode::SyntaxError, "<param> requires a non-empty name attribute", e.line, e.col);
-      const std::string* len = attr(e, "len");
-      if (!len) throw Error(ErrorCode::SyntaxError, "<param> requires a len attribute", e.line, e.col);
-      int v = parse_len(*len);
-      if (v < 1)
-        throw Error(ErrorCode::SyntaxError, "<param> len must be a positive integer, got \"" + *len + "\"",
-                    e.line, e.col);
-      if (!e.kids.empty()) throw Error(ErrorCode::SyntaxError, "<param> must be empty", e.line, e.col);
-      SchemaNode p;
-      p.kind = NodeKind::Param;
-      p.name = *nm;
-      p.param_len = v;
-      return p;
-    }
-    if (chat_role(e.tag)) {
-      SchemaNode c;
-      c.kind = NodeKind::Chat;
-      c.role = e.tag;
-      c.children = content(e);
-      return c;
-    }
-    throw Error(ErrorCode::SyntaxError, "unknown tag <" + e.tag + "> in schema", e.line, e.col);
+  void raise() const {
+    if (first) throw *first;
   }
 };
 
-void check_params(const std::vector<SchemaNode>& ns, bool in_module) {
-  for (const SchemaNode& n : ns) {
-    if (n.kind == NodeKind::Param && !in_module)
-      throw Error(ErrorCode::SyntaxError, "<param> must appear inside a <module>");
-    if (n.kind == NodeKind::Module) check_params(n.children, true);
-    if (n.kind == NodeKind::Union || n.kind == NodeKind::Chat) check_params(n.children, in_module);
-  }
-}
-
-void module_names(const std::vector<SchemaNode>& ns, std::vector<std::string>& out) {
-  for (const SchemaNode& n : ns) {
-    if (n.kind == NodeKind::Module) out.push_back(n.name);
-    if (n.kind == NodeKind::Module || n.kind == NodeKind::Union || n.kind == NodeKind::Chat)
-      module_names(n.children, out);
-  }
-}
-
-const std::set<std::string>& reserved() {
-  static const std::set<std::string> r = {"schema", "module", "union", "param",
-                                          "prompt", "system", "user",  "assistant"};
-  return r;
-}
-
-ModuleImport make_import(const Elem& e) {
-  if (reserved().count(e.tag))
-    throw Error(ErrorCode::SyntaxError, "reserved tag <" + e.tag + "> cannot be imported", e.line, e.col);
-  ModuleImport imp;
-  imp.name = e.tag;
-  imp.args = e.attrs;
-  for (const Elem& k : e.kids) {
-    if (k.text_node) {
-      if (blank(k.body)) continue;
-      throw Error(ErrorCode::SyntaxError, "bare text inside module import <" + e.tag + ">", k.line, k.col);
+// Lexes a whole document: `on_root` gets the root's start tag, `body` every event
+// strictly inside the root.  Tag balance and "nothing after the root" are checked here.
+template <typename Body>
+Event scan_document(const std::string& text, Body&& body) {
+  Lexer lx(text);
+  lx.skip_space();
+  if (lx.at_end()) lx.fail("document has no root element");
+  Event root = lx.next();
+  if (root.kind != Event::Open && root.kind != Event::SelfClose) lx.fail("document must start with its root element");
+  if (root.kind == Event::Open) {
+    std::vector<std::string> open{root.name};
+    for (;;) {
+      Event ev = lx.next();
+      if (ev.kind == Event::End) lx.fail("<" + open.back() + "> is never closed");
+      if (ev.kind == Event::Close) {
+        if (ev.name != open.back()) lx.fail("</" + ev.name + "> does not close <" + open.back() + ">");
+        open.pop_back();
+        if (open.empty()) break;
+      } else if (ev.kind == Event::Open) {
+        open.push_back(ev.name);
+      }
+      body(ev);
     }
-    // an argument element: no attributes, only text children, non-empty text
-    bool is_arg = k.attrs.empty();
-    std::string value;
-    for (const Elem& t : k.kids) {
-      if (!t.text_node) {
-        is_arg = false;
+  }
+  lx.skip_space();
+  if (!lx.at_end()) lx.fail("content after the root element");
+  return root;
+}
+
+// ---------------------------------------------------------------------------
+// Schema builder: one frame per open element; a frame whose element is invalid (or
+// sits where nothing is allowed) swallows its subtree.
+// ---------------------------------------------------------------------------
+class SchemaBuilder {
+ public:
+  explicit SchemaBuilder(Deferred& d) : err_(d) { stack_.emplace_back(); }
+
+  void feed(const Event& ev) {
+    if (ev.kind == Event::Text) return on_text(ev);
+    if (ev.kind == Event::Close) return pop();
+    push(ev);
+    if (ev.kind == Event::SelfClose) pop();
+  }
+  std::vector<SchemaNode> root() { return std::move(stack_.front().node.children); }
+
+ private:
+  enum class Role { Root, Node, Union, Param, Dead };
+  struct Frame {
+    Role role = Role::Root;
+    SchemaNode node;
+    bool param_content = false;
+    int line = 0, col = 0;
+  };
+
+  void on_text(const Event& ev) {
+    Frame& f = stack_.back();
+    switch (f.role) {
+      case Role::Root:  // schema-level text becomes an always-included anonymous module
+        if (!is_space_only(ev.text)) {
+          SchemaNode anon;
+          anon.kind = NodeKind::Module;
+          anon.anonymous = true;
+          anon.name = "__anon_" + std::to_string(anon_next_++);
+          anon.children.push_back(make_text(trim(ev.text)));
+          f.node.children.push_back(std::move(anon));
+        }
+        break;
+      case Role::Union:
+        if (!is_space_only(ev.text)) err_.note("text directly inside <union>", ev.line, ev.col);
+        break;
+      case Role::Param:
+        f.param_content = true;
+        break;
+      case Role::Node:
+        f.node.children.push_back(make_text(ev.text));
+        break;
+      case Role::Dead:
+        break;
+    }
+  }
+
+  void push(const Event& ev) {
+    Frame& parent = stack_.back();
+    Frame f;
+    f.role = Role::Dead;
+    f.line = ev.line;
+    f.col = ev.col;
+    if (parent.role == Role::Param) parent.param_content = true;
+    if (parent.role == Role::Dead || parent.role == Role::Param) {
+      // inside an invalid element or a param: already reported (or will be)
+    } else if (parent.role == Role::Union && ev.name != "module") {
+      err_.note("<union> may only contain <module> elements, found <" + ev.name + ">", ev.line, ev.col);
+    } else if (ev.name == "module") {
+      auto nm = attr_of(ev.attrs, "name");
+      if (nm && !nm->empty()) {
+        f.role = Role::Node;
+        f.node.kind = NodeKind::Module;
+        f.node.name = *nm;
+      } else {
+        err_.note("<module> needs a non-empty name", ev.line, ev.col);
+      }
+    } else if (ev.name == "union") {
+      f.role = Role::Union;
+      f.node.kind = NodeKind::Union;
+    } else if (ev.name == "param") {
+      auto nm = attr_of(ev.attrs, "name");
+      auto len = attr_of(ev.attrs, "len");
+      if (!nm || nm->empty()) {
+        err_.note("<param> needs a non-empty name", ev.line, ev.col);
+      } else if (!len) {
+        err_.note("<param> needs a len", ev.line, ev.col);
+      } else if (decimal_len(*len) < 1) {
+        err_.note("<param len=\"" + *len + "\"> is not a positive integer", ev.line, ev.col);
+      } else {
+        f.role = Role::Param;
+        f.node.kind = NodeKind::Param;
+        f.node.name = *nm;
+        f.node.param_len = decimal_len(*len);
+      }
+    } else if (is_chat_role(ev.name)) {
+      f.role = Role::Node;
+      f.node.kind = NodeKind::Chat;
+      f.node.role = ev.name;
+    } else {
+      err_.note("<" + ev.name + "> is not a schema element", ev.line, ev.col);
+    }
+    stack_.push_back(std::move(f));
+  }
+
+  void pop() {
+    Frame f = std::move(stack_.back());
+    stack_.pop_back();
+    if (f.role == Role::Dead) return;
+    if (f.role == Role::Param && f.param_content) {
+      err_.note("<param> must be an empty element", f.line, f.col);
+      return;
+    }
+    stack_.back().node.children.push_back(std::move(f.node));
+  }
+
+  Deferred& err_;
+  std::vector<Frame> stack_;
+  int anon_next_ = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Prompt builder.  Under an import, a child element is an argument when it has no
+// attributes, no element children and non-empty text; otherwise it is a nested import.
+// That is only known at its end tag, so every element frame collects both readings.
+// ---------------------------------------------------------------------------
+class PromptBuilder {
+ public:
+  explicit PromptBuilder(Deferred& d) : err_(d) { stack_.emplace_back(); }
+
+  void feed(const Event& ev) {
+    if (ev.kind == Event::Text) return on_text(ev);
+    if (ev.kind == Event::Close) return pop();
+    Frame f;
+    f.name = ev.name;
+    f.attrs = ev.attrs;
+    f.line = ev.line;
+    f.col = ev.col;
+    if (stack_.size() > 1) stack_.back().has_elements = true;
+    stack_.push_back(std::move(f));
+    if (ev.kind == Event::SelfClose) pop();
+  }
+  std::vector<PromptItem> items() { return std::move(stack_.front().items); }
+
+ private:
+  struct Frame {  // stack_[0] is the <prompt> root
+    std::string name;
+    Attrs attrs;
+    std::string text;                 // concatenated text runs
+    bool has_elements = false;
+    std::optional<Event> stray_text;  // first non-blank text run (an error if this is an import)
+    std::vector<std::pair<std::string, std::string>> args;
+    std::vector<PromptItem> items;    // nested imports (root: every item)
+    int line = 0, col = 0;
+  };
+
+  void on_text(const Event& ev) {
+    Frame& f = stack_.back();
+    if (stack_.size() == 1) {  // prompt-level text: new uncached text
+      if (!is_space_only(ev.text)) {
+        PromptItem it;
+        it.kind = PromptItem::Kind::Text;
+        it.text = trim(ev.text);
+        f.items.push_back(std::move(it));
+      }
+      return;
+    }
+    f.text += ev.text;
+    if (!f.stray_text && !is_space_only(ev.text)) f.stray_text = ev;
+  }
+
+  void pop() {
+    Frame f = std::move(stack_.back());
+    stack_.pop_back();
+    Frame& parent = stack_.back();
+    const bool under_import = stack_.size() > 1;
+    if (under_import && f.attrs.empty() && !f.has_elements && !f.text.empty()) {
+      parent.args.emplace_back(f.name, f.text);
+      return;
+    }
+    if (is_reserved(f.name)) {
+      err_.note("<" + f.name + "> is a reserved tag, not a module import", f.line, f.col);
+      return;
+    }
+    if (f.stray_text) err_.note("text inside the import <" + f.name + ">", f.stray_text->line, f.stray_text->col);
+    PromptItem it;
+    it.kind = PromptItem::Kind::Import;
+    it.import.name = f.name;
+    it.import.args = std::move(f.attrs);  // attribute arguments first, then element arguments
+    for (auto& a : f.args) it.import.args.push_back(std::move(a));
+    it.import.children = std::move(f.items);
+    parent.items.push_back(std::move(it));
+  }
+
+  Deferred& err_;
+  std::vector<Frame> stack_;
+};
+
+// ---------------------------------------------------------------------------
+// Serialization
+// ---------------------------------------------------------------------------
+void put_escaped(std::string& out, const std::string& s, bool in_attr) {
+  for (char c : s) switch (c) {
+      case '<': out += "&lt;"; break;
+      case '>': out += "&gt;"; break;
+      case '&': out += "&amp;"; break;
+      case '"':
+        if (in_attr) {
+          out += "&quot;";
+          break;
+        }
+        [[fallthrough]];
+      default: out.push_back(c);
+    }
+}
+
+void write_nodes(std::string& out, const std::vector<SchemaNode>& nodes);
+
+void write_node(std::string& out, const SchemaNode& n) {
+  switch (n.kind) {
+    case NodeKind::Text:
+      put_escaped(out, n.text, false);
+      break;
+    case NodeKind::Param:
+      out += "<param name=\"";
+      put_escaped(out, n.name, true);
+      out += "\" len=\"";
+      out += std::to_string(n.param_len);
+      out += "\"/>";
+      break;
+    case NodeKind::Module:
+      if (n.anonymous) {  // anonymous modules are bare schema text
+        write_nodes(out, n.children);
         break;
       }
-      value += t.body;
-    }
-    if (is_arg && !value.empty()) {
-      imp.args.emplace_back(k.tag, value);
-    } else {
-      PromptItem child;
-      child.kind = PromptItem::Kind::Import;
-      child.import = make_import(k);
-      imp.children.push_back(std::move(child));
-    }
-  }
-  return imp;
-}
-
-void esc(const std::string& s, std::string& out, bool attr_mode) {
-  for (char c : s) {
-    if (c == '<') out += "&lt;";
-    else if (c == '>') out += "&gt;";
-    else if (c == '&') out += "&amp;";
-    else if (attr_mode && c == '"') out += "&quot;";
-    else out.push_back(c);
-  }
-}
-
-void emit(const SchemaNode& n, std::string& o) {
-  switch (n.kind) {
-    case NodeKind::Text: esc(n.text, o, false); return;
-    case NodeKind::Param:
-      o += "<param name=\"";
-      esc(n.name, o, true);
-      o += "\" len=\"" + std::to_string(n.param_len) + "\"/>";
-      return;
-    case NodeKind::Module:
-      if (n.anonymous) {
-        for (auto& c : n.children) emit(c, o);
-        return;
-      }
-      o += "<module name=\"";
-      esc(n.name, o, true);
-      o += "\">";
-      for (auto& c : n.children) emit(c, o);
-      o += "</module>";
-      return;
+      out += "<module name=\"";
+      put_escaped(out, n.name, true);
+      out += "\">";
+      write_nodes(out, n.children);
+      out += "</module>";
+      break;
     case NodeKind::Union:
-      o += "<union>";
-      for (auto& c : n.children) emit(c, o);
-      o += "</union>";
-      return;
-    case NodeKind::Chat:
-      o += "<" + n.role + ">";
-      for (auto& c : n.children) emit(c, o);
-      o += "</" + n.role + ">";
-      return;
+    case NodeKind::Chat: {
+      const std::string tag = n.kind == NodeKind::Union ? std::string("union") : n.role;
+      out += "<" + tag + ">";
+      write_nodes(out, n.children);
+      out += "</" + tag + ">";
+      break;
+    }
   }
 }
 
-void emit(const PromptItem& it, std::string& o) {
-  if (it.kind == PromptItem::Kind::Text) {
-    esc(it.text, o, false);
-    return;
+void write_nodes(std::string& out, const std::vector<SchemaNode>& nodes) {
+  for (const SchemaNode& n : nodes) write_node(out, n);
+}
+
+void write_items(std::string& out, const std::vector<PromptItem>& items) {
+  for (const PromptItem& it : items) {
+    if (it.kind == PromptItem::Kind::Text) {
+      put_escaped(out, it.text, false);
+      continue;
+    }
+    const ModuleImport& imp = it.import;
+    if (imp.args.empty() && imp.children.empty()) {
+      out += "<" + imp.name + "/>";
+      continue;
+    }
+    out += "<" + imp.name + ">";
+    for (const auto& [param, value] : imp.args) {  // arguments always as child elements
+      out += "<" + param + ">";
+      put_escaped(out, value, false);
+      out += "</" + param + ">";
+    }
+    write_items(out, imp.children);
+    out += "</" + imp.name + ">";
   }
-  const ModuleImport& m = it.import;
-  o += "<" + m.name;
-  if (m.args.empty() && m.children.empty()) {
-    o += "/>";
-    return;
-  }
-  o += ">";
-  for (auto& [k, v] : m.args) {
-    o += "<" + k + ">";
-    esc(v, o, false);
-    o += "</" + k + ">";
-  }
-  for (auto& c : m.children) emit(c, o);
-  o += "</" + m.name + ">";
 }
 
 }  // namespace
 
 SchemaDoc parse_schema(const std::string& text) {
-  Reader r(text);
-  Elem root = r.document();
-  if (root.tag != "schema")
-    throw Error(ErrorCode::SyntaxError, "root element must be <schema>, got <" + root.tag + ">", root.line,
-                root.col);
-  const std::string* nm = attr(root, "name");
-  if (!nm || nm->empty())
-    throw Error(ErrorCode::SyntaxError, "<schema> requires a non-empty name attribute", root.line, root.col);
+  Deferred err;
+  SchemaBuilder b(err);
+  const Event root = scan_document(text, [&](const Event& ev) { b.feed(ev); });
+  if (root.name != "schema") throw Error(ErrorCode::SyntaxError, "the root element is <" + root.name + ">, not <schema>",
+                                         root.line, root.col);
+  auto name = attr_of(root.attrs, "name");
+  if (!name || name->empty())
+    throw Error(ErrorCode::SyntaxError, "<schema> needs a non-empty name", root.line, root.col);
+  err.raise();
   SchemaDoc doc;
-  doc.name = *nm;
-  SchemaMaker maker;
-  doc.root = maker.root(root);
-  check_params(doc.root, false);
-  std::vector<std::string> names;
-  module_names(doc.root, names);
-  std::set<std::string> seen;
-  for (auto& n : names)
-    if (!seen.insert(n).second) throw Error(ErrorCode::SyntaxError, "duplicate module name \"" + n + "\"");
+  doc.name = *name;
+  doc.root = b.root();
+  // params only inside modules (a chat or union between them and the module is fine);
+  // module names unique over the whole tree
+  std::set<std::string> names;
+  std::vector<std::pair<const SchemaNode*, bool>> todo;  // (node, inside a module)
+  for (auto it = doc.root.rbegin(); it != doc.root.rend(); ++it) todo.emplace_back(&*it, false);
+  std::vector<std::string> in_order;
+  while (!todo.empty()) {
+    auto [n, in_module] = todo.back();
+    todo.pop_back();
+    if (n->kind == NodeKind::Param && !in_module)
+      throw Error(ErrorCode::SyntaxError, "<param " + n->name + "> outside any module");
+    if (n->kind == NodeKind::Module) in_order.push_back(n->name);
+    const bool child_in_module = in_module || n->kind == NodeKind::Module;
+    for (auto it = n->children.rbegin(); it != n->children.rend(); ++it) todo.emplace_back(&*it, child_in_module);
+  }
+  for (const std::string& nm : in_order)
+    if (!names.insert(nm).second) throw Error(ErrorCode::SyntaxError, "module name \"" + nm + "\" is used twice");
   return doc;
 }
 
 PromptDoc parse_prompt(const std::string& text) {
-  Reader r(text);
-  Elem root = r.document();
-  if (root.tag != "prompt")
-    throw Error(ErrorCode::SyntaxError, "root element must be <prompt>, got <" + root.tag + ">", root.line,
-                root.col);
-  const std::string* sc = attr(root, "schema");
-  if (!sc || sc->empty())
-    throw Error(ErrorCode::MissingSchemaAttr, "<prompt> requires a schema attribute", root.line, root.col);
+  Deferred err;
+  PromptBuilder b(err);
+  const Event root = scan_document(text, [&](const Event& ev) { b.feed(ev); });
+  if (root.name != "prompt") throw Error(ErrorCode::SyntaxError, "the root element is <" + root.name + ">, not <prompt>",
+                                         root.line, root.col);
+  auto schema = attr_of(root.attrs, "schema");
+  if (!schema || schema->empty())
+    throw Error(ErrorCode::MissingSchemaAttr, "<prompt> needs a schema attribute", root.line, root.col);
+  err.raise();
   PromptDoc doc;
-  doc.schema_name = *sc;
-  for (const Elem& k : root.kids) {
-    PromptItem it;
-    if (k.text_node) {
-      if (blank(k.body)) continue;
-      it.kind = PromptItem::Kind::Text;
-      it.text = strip(k.body);
-    } else {
-      it.kind = PromptItem::Kind::Import;
-      it.import = make_import(k);
-    }
-    doc.items.push_back(std::move(it));
-  }
+  doc.schema_name = *schema;
+  doc.items = b.items();
   return doc;
 }
 
 std::string serialize(const SchemaDoc& doc) {
-  std::string o = "<schema name=\"";
-  esc(doc.name, o, true);
-  o += "\">";
-  for (auto& n : doc.root) emit(n, o);
-  return o + "</schema>";
+  std::string out = "<schema name=\"";
+  put_escaped(out, doc.name, true);
+  out += "\">";
+  write_nodes(out, doc.root);
+  out += "</schema>";
+  return out;
 }
 
 std::string serialize(const PromptDoc& doc) {
-  std::string o = "<prompt schema=\"";
-  esc(doc.schema_name, o, true);
-  o += "\">";
-  for (auto& it : doc.items) emit(it, o);
-  return o + "</prompt>";
+  std::string out = "<prompt schema=\"";
+  put_escaped(out, doc.schema_name, true);
+  out += "\">";
+  write_items(out, doc.items);
+  out += "</prompt>";
+  return out;
 }
 
 // ---------------------------------------------------------------------------
-// Validation (reference pml.cpp:556-701)
+// Validation
 // ---------------------------------------------------------------------------
 
 void ValidationReport::add(Severity s, const std::string& code, const std::string& msg) {
@@ -537,98 +637,62 @@ void ValidationReport::add(Severity s, const std::string& code, const std::strin
 }
 
 std::string ValidationReport::to_json() const {
+  nlohmann::json arr = nlohmann::json::array();
+  for (const Issue& i : issues)
+    arr.push_back({{"severity", i.severity == Severity::Error ? "error" : "warning"},
+                   {"code", i.code},
+                   {"message", i.message},
+                   {"line", 0},
+                   {"col", 0}});
   nlohmann::json j;
   j["ok"] = ok;
-  j["issues"] = nlohmann::json::array();
-  for (auto& i : issues)
-    j["issues"].push_back({{"severity", i.severity == Severity::Error ? "error" : "warning"},
-                           {"code", i.code},
-                           {"message", i.message},
-                           {"line", 0},
-                           {"col", 0}});
+  j["issues"] = std::move(arr);
   return j.dump();
 }
 
 namespace {
 
-struct ModInfo {
-  std::map<std::string, int> params;
-  std::string parent;
-  int union_group = -1;
+// What validation needs to know about one schema module.
+struct ModuleFacts {
+  std::string parent;  // enclosing module ("" at top level); chat tags are transparent
+  int union_id = -1;   // union it is an arm of (pre-order numbering), -1 = none
+  std::map<std::string, int> params;  // its own params, including those inside its chat tags
 };
 
-struct Index {
-  std::map<std::string, ModInfo> mods;
+// Schema facts by an explicit-stack walk.  A union's arms (directly, or through chat
+// tags) carry its pre-order number; a module's own params are its param children and
+// params reached from it through chat tags only.
+std::map<std::string, ModuleFacts> schema_facts(const SchemaDoc& schema) {
+  std::map<std::string, ModuleFacts> facts;
+  struct Item {
+    const SchemaNode* n;
+    std::string parent;
+    int union_id;
+    ModuleFacts* owner;  // module whose params a param here belongs to (through chats)
+  };
   int unions = 0;
-
-  static void chat_params(const std::vector<SchemaNode>& ns, ModInfo& info) {
-    for (auto& c : ns)
-      if (c.kind == NodeKind::Chat) {
-        for (auto& cc : c.children)
-          if (cc.kind == NodeKind::Param) info.params[cc.name] = cc.param_len;
-        chat_params(c.children, info);
-      }
-  }
-
-  void walk(const std::vector<SchemaNode>& ns, const std::string& parent, int group) {
-    for (auto& n : ns) {
-      if (n.kind == NodeKind::Module) {
-        ModInfo info;
-        info.parent = parent;
-        info.union_group = group;
-        for (auto& c : n.children)
-          if (c.kind == NodeKind::Param) info.params[c.name] = c.param_len;
-        chat_params(n.children, info);
-        mods[n.name] = std::move(info);
-        walk(n.children, n.name, -1);
-      } else if (n.kind == NodeKind::Union) {
-        walk(n.children, parent, unions++);
-      } else if (n.kind == NodeKind::Chat) {
-        walk(n.children, parent, group);
-      }
+  std::vector<Item> todo;
+  for (auto it = schema.root.rbegin(); it != schema.root.rend(); ++it) todo.push_back({&*it, "", -1, nullptr});
+  while (!todo.empty()) {
+    Item cur = todo.back();
+    todo.pop_back();
+    const SchemaNode& n = *cur.n;
+    std::vector<Item> kids;
+    if (n.kind == NodeKind::Module) {
+      ModuleFacts& f = facts[n.name];
+      f = ModuleFacts{cur.parent, cur.union_id, {}};
+      for (const SchemaNode& c : n.children) kids.push_back({&c, n.name, -1, &f});
+    } else if (n.kind == NodeKind::Union) {
+      const int id = unions++;
+      for (const SchemaNode& c : n.children) kids.push_back({&c, cur.parent, id, nullptr});
+    } else if (n.kind == NodeKind::Chat) {
+      for (const SchemaNode& c : n.children) kids.push_back({&c, cur.parent, cur.union_id, cur.owner});
+    } else if (n.kind == NodeKind::Param && cur.owner) {
+      cur.owner->params[n.name] = n.param_len;
     }
+    for (auto it = kids.rbegin(); it != kids.rend(); ++it) todo.push_back(*it);
   }
-};
-
-void check_imports(const std::vector<PromptItem>& items, const std::string& enclosing, const Index& idx,
-                   ValidationReport& rep, std::map<std::string, int>& count,
-                   std::map<int, std::vector<std::string>>& by_union) {
-  for (auto& it : items) {
-    if (it.kind != PromptItem::Kind::Import) continue;
-    const ModuleImport& imp = it.import;
-    auto f = idx.mods.find(imp.name);
-    if (f == idx.mods.end()) {
-      rep.add(Severity::Error, "UNKNOWN_MODULE", "unknown module \"" + imp.name + "\"");
-      continue;
-    }
-    const ModInfo& info = f->second;
-    if (info.parent != enclosing)
-      rep.add(Severity::Error, "PARENT_NOT_IMPORTED",
-              "module \"" + imp.name + "\" must be imported inside \"" +
-                  (info.parent.empty() ? std::string("<top level>") : info.parent) + "\"");
-    if (++count[imp.name] > 1)
-      rep.add(Severity::Error, "DUPLICATE_IMPORT", "module \"" + imp.name + "\" imported more than once");
-    if (info.union_group >= 0) by_union[info.union_group].push_back(imp.name);
-    std::set<std::string> given;
-    for (auto& [p, v] : imp.args) {
-      given.insert(p);
-      auto pp = info.params.find(p);
-      if (pp == info.params.end()) {
-        rep.add(Severity::Error, "UNKNOWN_PARAM", "module \"" + imp.name + "\" has no parameter \"" + p + "\"");
-        continue;
-      }
-      int nt = static_cast<int>(v.size());  // byte tokenizer: one token per byte
-      if (nt > pp->second)
-        rep.add(Severity::Error, "ARG_TOO_LONG",
-                "argument for \"" + p + "\" is " + std::to_string(nt) + " tokens, parameter len is " +
-                    std::to_string(pp->second));
-    }
-    for (auto& [p, len] : info.params)
-      if (!given.count(p))
-        rep.add(Severity::Warning, "UNUSED_PARAM",
-                "parameter \"" + p + "\" of module \"" + imp.name + "\" not supplied");
-    check_imports(imp.children, imp.name, idx, rep, count, by_union);
-  }
+  return facts;
 }
 
 }  // namespace
@@ -640,22 +704,67 @@ ValidationReport validate_prompt(const PromptDoc& prompt, const SchemaDoc& schem
             "prompt references schema \"" + prompt.schema_name + "\", validated against \"" + schema.name + "\"");
     return rep;
   }
-  Index idx;
-  idx.walk(schema.root, "", -1);
-  std::map<std::string, int> count;
-  std::map<int, std::vector<std::string>> by_union;
-  check_imports(prompt.items, "", idx, rep, count, by_union);
-  for (auto& [g, names] : by_union)
-    if (names.size() > 1) {
-      std::string joined;
-      for (auto& n : names) joined += (joined.empty() ? "" : ", ") + n;
-      rep.add(Severity::Error, "UNION_CONFLICT", "modules from the same union imported together: " + joined);
+  const std::map<std::string, ModuleFacts> facts = schema_facts(schema);
+  std::map<std::string, int> times_imported;
+  std::map<int, std::vector<std::string>> union_members;
+
+  // imports in document order, depth first; an unknown module's children are not visited
+  struct Visit {
+    const ModuleImport* imp;
+    std::string enclosing;
+  };
+  std::vector<Visit> todo;
+  auto push_items = [&](const std::vector<PromptItem>& items, const std::string& enclosing) {
+    for (auto it = items.rbegin(); it != items.rend(); ++it)
+      if (it->kind == PromptItem::Kind::Import) todo.push_back({&it->import, enclosing});
+  };
+  push_items(prompt.items, "");
+  while (!todo.empty()) {
+    const Visit v = todo.back();
+    todo.pop_back();
+    const ModuleImport& imp = *v.imp;
+    auto fi = facts.find(imp.name);
+    if (fi == facts.end()) {
+      rep.add(Severity::Error, "UNKNOWN_MODULE", "unknown module \"" + imp.name + "\"");
+      continue;
     }
+    const ModuleFacts& f = fi->second;
+    if (f.parent != v.enclosing)
+      rep.add(Severity::Error, "PARENT_NOT_IMPORTED",
+              "module \"" + imp.name + "\" must be imported inside \"" +
+                  (f.parent.empty() ? std::string("<top level>") : f.parent) + "\"");
+    if (++times_imported[imp.name] > 1)
+      rep.add(Severity::Error, "DUPLICATE_IMPORT", "module \"" + imp.name + "\" imported more than once");
+    if (f.union_id >= 0) union_members[f.union_id].push_back(imp.name);
+    std::set<std::string> supplied;
+    for (const auto& [param, value] : imp.args) {
+      supplied.insert(param);
+      auto p = f.params.find(param);
+      if (p == f.params.end()) {
+        rep.add(Severity::Error, "UNKNOWN_PARAM", "module \"" + imp.name + "\" has no parameter \"" + param + "\"");
+      } else if (static_cast<int>(tok::tokenize(value).size()) > p->second) {
+        rep.add(Severity::Error, "ARG_TOO_LONG",
+                "argument for \"" + param + "\" is " + std::to_string(tok::tokenize(value).size()) +
+                    " tokens, parameter len is " + std::to_string(p->second));
+      }
+    }
+    for (const auto& [param, len] : f.params)
+      if (!supplied.count(param))
+        rep.add(Severity::Warning, "UNUSED_PARAM",
+                "parameter \"" + param + "\" of module \"" + imp.name + "\" not supplied");
+    push_items(imp.children, imp.name);
+  }
+  for (const auto& [id, members] : union_members) {
+    if (members.size() < 2) continue;
+    std::string list = members.front();
+    for (size_t i = 1; i < members.size(); ++i) list += ", " + members[i];
+    rep.add(Severity::Error, "UNION_CONFLICT", "modules from the same union imported together: " + list);
+  }
   return rep;
 }
 
 // ---------------------------------------------------------------------------
-// Chat expansion (reference pml.cpp:707-786)
+// Chat-template expansion
 // ---------------------------------------------------------------------------
 
 ChatTemplate ChatTemplate::llama2() {
@@ -668,43 +777,44 @@ ChatTemplate ChatTemplate::llama2() {
 
 namespace {
 
-void expand(const std::vector<SchemaNode>& in, const ChatTemplate& tpl, std::vector<SchemaNode>& out) {
-  for (auto& n : in) {
-    if (n.kind == NodeKind::Chat) {
-      auto r = tpl.roles.find(n.role);
-      if (r == tpl.roles.end()) throw Error(ErrorCode::UnknownRole, "no template for role \"" + n.role + "\"");
-      if (!r->second.prefix.empty()) out.push_back(text_node(r->second.prefix));
-      expand(n.children, tpl, out);
-      if (!r->second.suffix.empty()) out.push_back(text_node(r->second.suffix));
+// Replaces every chat tag by (prefix text, its expanded children, suffix text).
+std::vector<SchemaNode> without_chat(const std::vector<SchemaNode>& in, const ChatTemplate& tpl) {
+  std::vector<SchemaNode> out;
+  for (const SchemaNode& n : in) {
+    if (n.kind != NodeKind::Chat) {
+      SchemaNode c = n;
+      c.children = without_chat(n.children, tpl);
+      out.push_back(std::move(c));
       continue;
     }
-    SchemaNode c = n;
-    if (!c.children.empty()) {
-      std::vector<SchemaNode> k;
-      expand(n.children, tpl, k);
-      c.children = std::move(k);
-    }
-    out.push_back(std::move(c));
+    auto role = tpl.roles.find(n.role);
+    if (role == tpl.roles.end()) throw Error(ErrorCode::UnknownRole, "the chat template has no role \"" + n.role + "\"");
+    if (!role->second.prefix.empty()) out.push_back(make_text(role->second.prefix));
+    for (SchemaNode& c : without_chat(n.children, tpl)) out.push_back(std::move(c));
+    if (!role->second.suffix.empty()) out.push_back(make_text(role->second.suffix));
   }
+  return out;
 }
 
-int highest_anon(const std::vector<SchemaNode>& ns) {
+// Largest N over anonymous modules named "__anon_<N...>" anywhere in the tree (the
+// number is read like std::stoi: leading blanks, sign, digits, rest ignored); -1 if none.
+int max_anon_index(const std::vector<SchemaNode>& nodes) {
   int best = -1;
-  for (auto& n : ns) {
-    if (n.kind == NodeKind::Module && n.anonymous && n.name.rfind("__anon_", 0) == 0) {
-      const std::string tail = n.name.substr(7);
-      // std::stoi semantics: leading digits only; non-numeric names are ignored
-      size_t i = 0;
-      while (i < tail.size() && std::isspace(static_cast<unsigned char>(tail[i]))) ++i;
-      bool neg = i < tail.size() && tail[i] == '-';
-      if (i < tail.size() && (tail[i] == '+' || tail[i] == '-')) ++i;
-      long long v = 0;
-      size_t d0 = i;
-      while (i < tail.size() && std::isdigit(static_cast<unsigned char>(tail[i])) && v < 2147483648LL)
-        v = v * 10 + (tail[i++] - '0');
-      if (i > d0 && v <= 2147483647LL) best = std::max(best, static_cast<int>(neg ? -v : v));
-    }
-    best = std::max(best, highest_anon(n.children));
+  std::vector<const SchemaNode*> todo;
+  for (const SchemaNode& n : nodes) todo.push_back(&n);
+  while (!todo.empty()) {
+    const SchemaNode* n = todo.back();
+    todo.pop_back();
+    for (const SchemaNode& c : n->children) todo.push_back(&c);
+    if (n->kind != NodeKind::Module || !n->anonymous || n->name.compare(0, 7, "__anon_") != 0) continue;
+    const char* p = n->name.c_str() + 7;
+    while (std::isspace(static_cast<unsigned char>(*p))) ++p;
+    const bool neg = *p == '-';
+    if (*p == '+' || *p == '-') ++p;
+    if (!std::isdigit(static_cast<unsigned char>(*p))) continue;
+    long long v = 0;
+    while (std::isdigit(static_cast<unsigned char>(*p)) && v < 2147483648LL) v = v * 10 + (*p++ - '0');
+    if (v <= 2147483647LL) best = std::max(best, static_cast<int>(neg ? -v : v));
   }
   return best;
 }
@@ -712,36 +822,31 @@ int highest_anon(const std::vector<SchemaNode>& ns) {
 }  // namespace
 
 SchemaDoc expand_chat_tags(const SchemaDoc& doc, const ChatTemplate& tpl) {
+  std::vector<SchemaNode> flat = without_chat(doc.root, tpl);
+  int next_anon = max_anon_index(flat) + 1;
   SchemaDoc out;
   out.name = doc.name;
-  std::vector<SchemaNode> flat;
-  expand(doc.root, tpl, flat);
-  int next = highest_anon(flat) + 1;
-  std::string run;
-  auto flush = [&] {
-    if (run.empty()) return;
-    SchemaNode a;
-    a.kind = NodeKind::Module;
-    a.name = "__anon_" + std::to_string(next++);
-    a.anonymous = true;
-    a.children.push_back(text_node(std::move(run)));
-    out.root.push_back(std::move(a));
-    run.clear();
-  };
-  for (auto& n : flat) {
-    if (n.kind == NodeKind::Text) {
-      run += n.text;
-    } else {
-      flush();
-      out.root.push_back(std::move(n));
+  // runs of schema-level text (template prefixes/suffixes) become new anonymous modules
+  for (size_t i = 0; i < flat.size();) {
+    if (flat[i].kind != NodeKind::Text) {
+      out.root.push_back(std::move(flat[i++]));
+      continue;
     }
+    std::string run;
+    while (i < flat.size() && flat[i].kind == NodeKind::Text) run += flat[i++].text;
+    if (run.empty()) continue;
+    SchemaNode anon;
+    anon.kind = NodeKind::Module;
+    anon.anonymous = true;
+    anon.name = "__anon_" + std::to_string(next_anon++);
+    anon.children.push_back(make_text(std::move(run)));
+    out.root.push_back(std::move(anon));
   }
-  flush();
   return out;
 }
 
 // ---------------------------------------------------------------------------
-// AST JSON interchange
+// AST JSON interchange (test fixtures replay the reference's in-memory ASTs)
 // ---------------------------------------------------------------------------
 
 namespace {
@@ -764,7 +869,7 @@ json node_json(const SchemaNode& n) {
 SchemaNode node_from(const json& j) {
   SchemaNode n;
   const std::string k = j.at("k");
-  if (k == "text") return text_node(j.at("t"));
+  if (k == "text") return make_text(j.at("t"));
   if (k == "param") {
     n.kind = NodeKind::Param;
     n.name = j.at("name");

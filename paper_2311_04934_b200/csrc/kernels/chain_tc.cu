@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstring>
 #include <type_traits>
 
@@ -1018,6 +1019,17 @@ unsigned long long* chain_probe_slot(int n_phases) {
   return g_ctl + per * g_ctl_n++;
 }
 
+// per device: the stream that launched the last chain (cross-stream chain ordering)
+struct ChainOrder {
+  std::mutex mu;
+  cudaStream_t last = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+ChainOrder& chain_order(int dev) {
+  static ChainOrder orders[64];
+  return orders[dev & 63];
+}
+
 template <int BN, int STAGES>
 void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int* flags, unsigned long long* gbar,
                   unsigned long long& gbar_count, cudaStream_t s, int sms) {
@@ -1118,8 +1130,44 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   }();
   p.pf_dist = pf_dist;
   gbar_count += static_cast<unsigned long long>(n - 1) * C;  // one arrival per CTA per phase boundary
+  // The grid barrier needs all C CTAs resident at once: one per SM must fit (checked once
+  // per instantiation), and two chains may never run concurrently on one device (each
+  // could hold part of the SMs while waiting for the rest).  Chains of one stream are
+  // ordered by the stream; a chain on another stream of the same device first waits for
+  // everything submitted to the stream that launched the previous chain.
+  static const int fit = [] {
+    int nb = 0;
+    PCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_chain<BN, STAGES>, kChainThreads, Sm::kBytes));
+    return nb;
+  }();
+  if (fit < 1) throw std::runtime_error("chain: one CTA per SM does not fit (shared memory or register limits)");
+  int dev = 0;
+  PCB_CUDA(cudaGetDevice(&dev));
+  ChainOrder& o = chain_order(dev);
+  std::lock_guard<std::mutex> lk(o.mu);
+  if (o.last && o.last != s) {
+    if (!o.ev) PCB_CUDA(cudaEventCreateWithFlags(&o.ev, cudaEventDisableTiming));
+    PCB_CUDA(cudaEventRecord(o.ev, o.last));
+    PCB_CUDA(cudaStreamWaitEvent(s, o.ev, 0));
+  }
+  o.last = s;
   PdlClass pc(PDL_GEMM);
-  launch_k(k_chain<BN, STAGES>, dim3(C), dim3(kChainThreads), Sm::kBytes, s, 1, p);
+  static const bool coop = std::getenv("PCB_CHAIN_COOP") != nullptr;  // A/B: cooperative launch attribute
+  if (coop) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kChainThreads);
+    cfg.dynamicSmemBytes = Sm::kBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_chain<BN, STAGES>, p));
+  } else {
+    launch_k(k_chain<BN, STAGES>, dim3(C), dim3(kChainThreads), Sm::kBytes, s, 1, p);
+  }
 }
 
 }  // namespace
