@@ -503,6 +503,7 @@ std::string Model::profile_json() {
 Model::~Model() {
   if (stream_) {
     cudaStreamSynchronize(stream_);
+    kern::chain_forget_stream(stream_);
     cudaStreamDestroy(stream_);
   }
 }

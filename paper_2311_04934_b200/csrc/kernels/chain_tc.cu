@@ -252,7 +252,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   uint64_t* a_pfull = a_sfull + 2;     // [2] (two: see attn_tc.cu, one p_full can deadlock)
   uint64_t* a_pvdone = a_pfull + 2;    // [2]
   uint64_t* a_done = a_pvdone + 2;     // this CTA's attention is off the ring (128 arrivals)
-  const uint32_t tcols = has_attn ? 512u : S::kCols;
+  // a QKV phase with a per-request RoPE table stages each tile's {cos, sin} operands in TMEM
+  // columns [256, 384) and [384, 512) while its weights stream (idle there: attention is
+  // phase 0 only; GEMM accumulators use [0, 2 BN) with BN <= 128)
+  bool rope_stage_any = false;
+  for (int ph = 0; ph < p.n_phases; ++ph)
+    rope_stage_any |= p.ph[ph].kind == CHAIN_GEMM && p.ph[ph].e.kind == EPI_QKV && p.ph[ph].e.rope &&
+                      p.ph[ph].e.rope_tab != nullptr && p.ph[ph].S == 1;
+  const uint32_t tcols = (has_attn || rope_stage_any) ? 512u : S::kCols;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -843,13 +850,42 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         // 2^-11 is 8x finer than the bf16 operands' rounding, and half the bytes shorten the
         // publish -> flag -> reload round trip at every split phase end)
         __half* ws = reinterpret_cast<__half*>(p.ws + (ph & 1) * p.ws_half);
+        const bool rope_stage = e.kind == EPI_QKV && e.rope && e.rope_tab != nullptr && P.S == 1;
         for (int i = c; i < P.items; i += C, ++seg) {
           const int tile = i / P.S, j = i - tile * P.S;
           const int n = tile * 128 + row;
           const int buf = seg & 1;
           const uint32_t acc = tmem + buf * BN + lane_off;
           EpiPre cur, nxt;
-          if (P.S == 1) epi_prefetch(e, n, P.N, 0, M, cur);  // before the accumulator is ready
+          // RoPE rows of every chunk into TMEM while the weights stream (per-chunk loads at
+          // epilogue time each cost a loaded-L2 round trip, ~1 us: 4 of them per QKV tile)
+          const bool rot = rope_stage && (tile * 128) / e.d < 2;  // Q and K tiles (warp-uniform)
+          if (rot) {
+            const float4* src = reinterpret_cast<const float4*>(e.rope_tab + (((n % e.d) % e.head_dim) >> 1) * e.rope_ld);
+            const int Mr = (Mc + 15) & ~15;  // rope_ld leaves >= 16 tokens of slack
+#pragma unroll 1
+            for (int cc = 0; cc < Mc; cc += 32) {
+              float4 t[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) t[u] = cc + 2 * u < Mr ? __ldg(src + (cc >> 1) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                if (cc + 16 * h2 >= Mc) break;  // warp-uniform
+                float cs[16], sn[16];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  cs[2 * u] = t[8 * h2 + u].x;
+                  sn[2 * u] = t[8 * h2 + u].y;
+                  cs[2 * u + 1] = t[8 * h2 + u].z;
+                  sn[2 * u + 1] = t[8 * h2 + u].w;
+                }
+                tmem_st16(tmem + 256 + lane_off + cc + 16 * h2, cs);
+                tmem_st16(tmem + 384 + lane_off + cc + 16 * h2, sn);
+              }
+            }
+            tmem_st_wait();
+          }
+          if (P.S == 1) epi_prefetch(e, n, P.N, 0, M, cur, !rope_stage);  // before the accumulator is ready
           mbar_wait(&acc_full[buf], (seg >> 1) & 1);
           tc_fence_after();
           if (et == 0) ctl(p, ph, 4);
@@ -861,7 +897,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             __nv_bfloat16* T = reinterpret_cast<__nv_bfloat16*>(colsum);  // [64 tokens][128 rows]
 #pragma unroll 1
             for (int cc = 0; cc < Mc; cc += 16) {
-              if (cc + 16 < Mc) epi_prefetch(e, n, P.N, cc + 16, M, nxt);
+              if (rope_stage) {  // operands staged in TMEM; the LN-fold weight sum is per row
+                if (rot) {
+                  tmem_ld16(tmem + 256 + lane_off + cc, cur.a);
+                  tmem_ld16(tmem + 384 + lane_off + cc, cur.b);
+                }
+              } else if (cc + 16 < Mc) {
+                epi_prefetch(e, n, P.N, cc + 16, M, nxt, true, false);
+                nxt.lnw = cur.lnw;
+              }
               tmem_ld16(acc + cc, v);
               if (tstore) {
                 epi_values(e, n, cc, M, v, cur, ln);
@@ -871,7 +915,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 epi_chunk(e, n, P.N, cc, M, v, cur, ln);
                 if (P.stats_out) stats_chunk(tile, cc, M);
               }
-              cur = nxt;
+              if (!rope_stage) cur = nxt;
             }
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
@@ -1171,6 +1215,14 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
 }
 
 }  // namespace
+
+void chain_forget_stream(cudaStream_t s) {
+  for (int dev = 0; dev < 64; ++dev) {
+    ChainOrder& o = chain_order(dev);
+    std::lock_guard<std::mutex> lk(o.mu);
+    if (o.last == s) o.last = nullptr;
+  }
+}
 
 bool chain_tc_supported(int64_t M, int N, int K) { return M >= 1 && M <= 128 && weight_packable(N, K); }
 bool chain_ln_supported(int d) { return d % 4 == 0 && d <= 8192; }

@@ -22,11 +22,14 @@ struct EpiPre {
   float lnw;  // LN fold: sum_k W[n][k] (prefetched with the chunk's other operands)
 };
 
-__device__ __forceinline__ void epi_prefetch(const Epilogue& ep, int n, int N, int64_t m0, int64_t M, EpiPre& p) {
+// rope = false: the RoPE operands come from elsewhere (staged in TMEM by the chain)
+__device__ __forceinline__ void epi_prefetch(const Epilogue& ep, int n, int N, int64_t m0, int64_t M, EpiPre& p,
+                                             bool rope = true, bool lnw = true) {
   const int kind = ep.kind;
   // an L2 round trip under a saturated memory system is ~1 us: issued before the
   // accumulator is ready instead of inside the first chunk (tools/chain_ab.py c0_values)
-  if (ep.ln_wsum) p.lnw = __ldg(ep.ln_wsum + n);
+  if (ep.ln_wsum && lnw) p.lnw = __ldg(ep.ln_wsum + n);
+  if (kind == EPI_QKV && !rope) return;
   if (kind == EPI_RESID) {
     const float* src = ep.resid + m0 * N + n;
 #pragma unroll

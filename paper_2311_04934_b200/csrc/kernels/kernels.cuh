@@ -166,6 +166,8 @@ bool chain_ln_supported(int d);
 int chain_probe_dump(unsigned long long* times, int max_launches, int* phases);
 // flags: >= #SMs ints (zeroed once, private to the chain); gbar: one zeroed u64 whose
 // arrival count the caller tracks in gbar_count (advanced by this call).
+// a stream that launched chains is going away: drop it from the cross-stream chain ordering
+void chain_forget_stream(cudaStream_t s);
 void chain_tc(const ChainStep* steps, int n_steps, float* ws, size_t ws_bytes, int* flags,
               unsigned long long* gbar, unsigned long long& gbar_count, cudaStream_t s);
 
