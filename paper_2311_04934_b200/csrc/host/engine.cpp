@@ -532,8 +532,10 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
     const size_t b1 = std::min(reqs.size(), b0 + micro_batch);
     for (size_t i = b0; i < b1; ++i) {
       const ServeRequest& req = reqs[i];
-      // decode past the first token, baselines and scaffolds take the single-request path
-      if (!req.use_cache || req.use_scaffolds || req.max_new_tokens != 1) {
+      // decode past the first token, baselines, scaffolds and ALiBi models (per-request key
+      // positions in the attention) take the single-request path
+      if (!req.use_cache || req.use_scaffolds || req.max_new_tokens != 1 ||
+          m.config().pos_encoding == model::PosEncoding::Alibi) {
         if (segs_busy) CK(cudaEventSynchronize(segs_busy));  // serve() reuses the segment list
         out[i] = serve_unlocked(req, schema, store);
         continue;

@@ -210,7 +210,8 @@ struct Workspace {
     }
     if (rows > cap_rows) {
       int64_t c = std::max<int64_t>(rows, 256);
-      regrow(kvpos, c * 4);
+      // ALiBi key positions: per-segment padding to 64-key blocks + one block of slack
+      regrow(kvpos, (c + 64 * (kern::ChainStep::kMaxSeg + 2)) * 4);
       cap_rows = c;
     }
     if (logit_rows > cap_logit) {
@@ -233,7 +234,7 @@ struct Workspace {
       regrow(counters, 65536 * 4);
       CK(cudaMemset(counters, 0, 65536 * 4));
     }
-    int64_t need_ints = 10 * n + rows + 32;
+    int64_t need_ints = 10 * n + rows + 64 * (kern::ChainStep::kMaxSeg + 2) + 32;
     if (need_ints > host_ints_cap) {
       for (int sl = 0; sl < 2; ++sl)
         if (staged[sl]) CK(cudaEventSynchronize(staged[sl]));
@@ -637,7 +638,7 @@ bool Model::fused_attention_ok(int64_t n) const {
   const auto& c = cfg_;
   const int d = c.hidden;
   return use_chain && chain_attn && tp_size_ == 1 && dtype_ == BF16 && w_->packed && !force_simt && !force_simt_gemm &&
-         !force_simt_attn && c.pos_encoding != PosEncoding::Alibi && c.head_dim == 128 && kern::chain_ln_supported(d) &&
+         !force_simt_attn && c.head_dim == 128 && kern::chain_ln_supported(d) &&
          kern::chain_tc_supported(n, 3 * d, d) && kern::chain_tc_supported(n, 4 * d, d) &&
          kern::chain_tc_supported(n, d, 4 * d) && kern::chain_tc_supported(1, c.vocab_size, d) &&
          kern::chain_attn_supported(n, 0, c.n_heads, c.head_dim);
@@ -721,15 +722,33 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   if (device_token_ && B == 1 && n == 1)  // decode: the previous step's argmax, no host round trip
     CK(cudaMemcpyAsync(W.tok, device_token_, 4, cudaMemcpyDeviceToDevice, s));
   const bool alibi = c.pos_encoding == PosEncoding::Alibi;
+  int64_t kp_len = 0;
   if (alibi) {
+    // every key's position in key order; with a zero-copy prefix in key-BLOCK order (each
+    // segment -- a store block read in place, then the request's own rows -- padded to whole
+    // 64-key blocks, as the chain's attention phase walks them).  Zero slack after the last
+    // block: the attention kernels copy whole blocks of positions.
     int32_t* kp = hi + 2 * n;
-    for (int64_t j = 0; j < P; ++j) kp[j] = static_cast<int32_t>(kv.positions[j]);
-    for (int64_t i = 0; i < n; ++i) kp[P + i] = static_cast<int32_t>(positions[i]);
-    CK(cudaMemcpyAsync(W.kvpos, kp, total * 4, cudaMemcpyHostToDevice, s));
+    auto pad = [&]() {
+      while (kp_len % 64) kp[kp_len++] = 0;
+    };
+    if (!kv_prefix_.empty()) {
+      for (const KVBlock* b : kv_prefix_) {
+        for (int64_t p : b->positions) kp[kp_len++] = static_cast<int32_t>(p);
+        pad();
+      }
+      for (int64_t j = kv_prefix_rows_; j < P; ++j) kp[kp_len++] = static_cast<int32_t>(kv.positions[j]);
+    } else {
+      for (int64_t j = 0; j < P; ++j) kp[kp_len++] = static_cast<int32_t>(kv.positions[j]);
+    }
+    for (int64_t i = 0; i < n; ++i) kp[kp_len++] = static_cast<int32_t>(positions[i]);
+    pad();
+    for (int i = 0; i < 64; ++i) kp[kp_len++] = 0;
+    CK(cudaMemcpyAsync(W.kvpos, kp, kp_len * 4, cudaMemcpyHostToDevice, s));
   }
   if (mask) CK(cudaMemcpyAsync(W.mask, mask, n * n, cudaMemcpyHostToDevice, s));
   if (block_ids) {
-    int32_t* bp = hi + 2 * n + (alibi ? total : 0);
+    int32_t* bp = hi + 2 * n + kp_len;
     std::memcpy(bp, block_ids, n * 4);
     CK(cudaMemcpyAsync(W.block, bp, n * 4, cudaMemcpyHostToDevice, s));
   }
@@ -1036,7 +1055,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
     };
     // one request's attention joins the chain as its first phase (no launch, no prologue,
     // the next weights stream in as soon as each CTA's softmax is done)
-    const bool fuse_attn = chain_attn && B == 1 && tc_attn && hd == 128 && !mask && !block_ids && !alibi &&
+    const bool fuse_attn = chain_attn && B == 1 && tc_attn && hd == 128 && !mask && !block_ids &&
                            kern::chain_attn_supported(n, P, H, hd);
     if (!kv_prefix_.empty() && (!fuse_attn || P < kv_prefix_rows_))
       throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix set for a forward that cannot read it in place");
@@ -1060,6 +1079,11 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
         st.a_d = d;
         st.a_scratch = W.attn_scratch;
         st.a_scratch_bytes = W.attn_scratch_bytes;
+        if (alibi) {
+          st.a_alibi = w_->alibi;
+          st.a_kpos = W.kvpos;
+          st.a_qpos = W.pos;
+        }
         if (!kv_prefix_.empty()) {  // cached modules read in place, then this request's rows
           st.a_layer = l;
           st.a_planes = 2 * c.n_layers;

@@ -34,18 +34,19 @@ constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: stale max tolerated up to 2^8
 constexpr int kSeg = 16;                    // K/V segments per request (zero-copy batched mode)
 
-template <int HD>
+template <int HD, bool AL>
 struct AttnSmem {
   static constexpr int kAtoms = HD / 64;
   static constexpr int kQ = BQ * HD * 2;
   static constexpr int kKV = BKV * HD * 2;
   static constexpr int kStage = 2 * kKV;  // K + V
   static constexpr int kP = BQ * BKV * 2;  // one P buffer (two are used)
+  static constexpr int kPos = AL ? BKV * 4 : 0;  // ALiBi: the stage's key positions (int32)
   // as many K/V stages as fit next to Q and the two P buffers (a stage is held from its
   // TMA load through the PV MMA, so depth is what keeps HBM busy on long caches)
-  static constexpr int kStagesFit = (kSmemMax - kQ - 2 * kP - 2048) / kStage;
+  static constexpr int kStagesFit = (kSmemMax - kQ - 2 * kP - 2048) / (kStage + kPos);
   static constexpr int kStages = kStagesFit > PCB_ATTN_STAGES ? PCB_ATTN_STAGES : kStagesFit;
-  static constexpr int kBytes = kQ + kStages * kStage + 2 * kP + 1024 + 1024;
+  static constexpr int kBytes = kQ + kStages * (kStage + kPos) + 2 * kP + 1024 + 1024;
   static constexpr uint32_t kTmemCols = 2 * BKV + HD <= 256 ? 256 : 512;
 };
 
@@ -71,6 +72,11 @@ struct AttnParams {
   const int2* segn = nullptr;
   const CUtensorMap* maps = nullptr;
   int layer = 0;
+  // ALiBi (reference model.cpp:231-235, 410-411): score += slope_h (pos_key - pos_query);
+  // kv_pos[P + n] holds every key's position in key order (the queries are keys P..P+n-1),
+  // readable up to the last 64-key block (the producer copies whole blocks)
+  const float* alibi = nullptr;
+  const int32_t* kv_pos = nullptr;
   unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
   unsigned long long* tl = nullptr;   // per-CTA phase timeline [cta][8] (PCB_ATTN_TL)
 };
@@ -108,11 +114,11 @@ __device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) =
   return y;
 }
 
-template <int HD>
+template <int HD, bool AL>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnParams p) {
-  using S = AttnSmem<HD>;
+  using S = AttnSmem<HD, AL>;
   constexpr int KV_STAGES = S::kStages;
   constexpr int kRedRow = HD + 4;  // padded fp32 row of a parked partial O
   static_assert(BQ * (kRedRow + 2) * 4 <= KV_STAGES * S::kStage, "split merge buffer must fit the K/V stages");
@@ -121,7 +127,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + S::kQ;
   uint8_t* sP = sKV + KV_STAGES * S::kStage;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * S::kP);
+  int32_t* sPos = reinterpret_cast<int32_t*>(sP + 2 * S::kP);  // [KV_STAGES][BKV] (ALiBi)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * S::kP + KV_STAGES * S::kPos);
   uint64_t* q_full = bar;
   uint64_t* kv_full = bar + 1;                // [KV_STAGES]
   uint64_t* kv_empty = kv_full + KV_STAGES;   // [KV_STAGES]
@@ -216,7 +223,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         probe(p, 4, it);
         uint8_t* st = sKV + s * S::kStage;
         const int j0 = static_cast<int>((b0 + it) * BKV);
-        mbar_expect_tx(&kv_full[s], S::kStage);
+        mbar_expect_tx(&kv_full[s], S::kStage + S::kPos);
+        if constexpr (AL)  // the block's 64 key positions ride on the same barrier
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sPos + s * BKV)),
+              "l"(p.kv_pos + j0), "r"(S::kPos), "r"(smem_u32(&kv_full[s]))
+              : "memory");
         // head-interleaved cache [rows][H*hd]: x = h*hd + a*64, y = key row;
         // head-major cache [H][rows][hd]:     x = a*64,        y = h*rows + key row
         const int kx = p.kv_head_major ? 0 : h * HD;
@@ -297,6 +310,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // a warp whose 32 query rows are all past n (the suffix fills half a 128-row tile)
     // only keeps the barrier protocol: its P rows feed O rows nobody reads
     const bool live = q0 + qd * 32 < n_;
+    // ALiBi in raw score units: (s + slope sqrt(hd) (pk - pq)) * log2(e)/sqrt(hd)
+    //   = (s / sqrt(hd) + slope (pk - pq)) log2(e)
+    int32_t qpos = 0;
+    float slope_raw = 0.f;
+    if constexpr (AL) {
+      qpos = qi < n_ ? p.kv_pos[P_ + qi] : 0;
+      slope_raw = p.alibi[h] * sqrtf(static_cast<float>(HD));
+    }
     for (int it = 0, sg = 0; it < nb; ++it) {
       int64_t j0 = (b0 + it) * BKV, lim_seg = 0;
       if (p.segs) {  // zero-copy: mask per segment (module padding rows; causal tail)
@@ -325,6 +346,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int c = 0; c < BKV; ++c) sv[c] = __uint_as_float(raw[c]);
       }
       if (threadIdx.x == 128) probe(p, 6, it);
+      if constexpr (AL) {
+        const int s = it % KV_STAGES;
+        mbar_wait(&kv_full[s], (it / KV_STAGES) & 1);  // the positions' bulk copy (already complete)
+        const int4* kp = reinterpret_cast<const int4*>(sPos + s * BKV);
+#pragma unroll
+        for (int c = 0; c < BKV; c += 4) {
+          const int4 k4 = kp[c >> 2];
+          sv[c] = fmaf(slope_raw, static_cast<float>(k4.x - qpos), sv[c]);
+          sv[c + 1] = fmaf(slope_raw, static_cast<float>(k4.y - qpos), sv[c + 1]);
+          sv[c + 2] = fmaf(slope_raw, static_cast<float>(k4.z - qpos), sv[c + 2]);
+          sv[c + 3] = fmaf(slope_raw, static_cast<float>(k4.w - qpos), sv[c + 3]);
+        }
+      }
       // scores stay raw (unscaled); the 1/sqrt(hd) * log2(e) factor is folded into
       // one FFMA per element in front of ex2.approx
       if (j0 + BKV - 1 > limit) {  // diagonal block (or a segment's padding) only
@@ -537,11 +571,11 @@ namespace {
 unsigned long long* g_tlbuf = nullptr;
 int g_tl_ctas = 0;
 
-template <int HD>
+template <int HD, bool AL>
 void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s) {
-  using Sm = AttnSmem<HD>;
+  using Sm = AttnSmem<HD, AL>;
   static bool attr = [] {
-    PCB_CUDA(cudaFuncSetAttribute(k_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
+    PCB_CUDA(cudaFuncSetAttribute(k_attn_tc<HD, AL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
     return true;
   }();
   (void)attr;
@@ -559,6 +593,8 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   p.d = a.d;
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   p.out = static_cast<__nv_bfloat16*>(a.out);
+  p.alibi = a.alibi;
+  p.kv_pos = a.kv_pos;
   const bool batched = a.n_req > 0;  // one launch over the requests of a micro-batch
   const int q_tiles = batched ? a.n_req : static_cast<int>((a.n + BQ - 1) / BQ);
   const int64_t nblk0 = a.segs ? a.max_blocks
@@ -631,7 +667,7 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   }
   dim3 grid(q_tiles, a.H, splits);
   PdlClass pc(PDL_ATTN);
-  launch_k(k_attn_tc<HD>, grid, dim3(kAttnThreads), Sm::kBytes, s, splits, tq, tk, tv, p);  // cluster = splits
+  launch_k(k_attn_tc<HD, AL>, grid, dim3(kAttnThreads), Sm::kBytes, s, splits, tq, tk, tv, p);  // cluster = splits
   if (probe_on) {
     PCB_CUDA(cudaDeviceSynchronize());
     const unsigned long long t0 = dbg[4 * 64];
@@ -660,13 +696,20 @@ int attn_tl_dump(unsigned long long* out, int max_ctas) {
 }
 
 bool attention_tc_supported(const AttnArgs& a) {
-  return (a.hd == 128 || a.hd == 64) && !a.mask && !a.block_id && !a.alibi && a.n >= 1 && a.d % 64 == 0 &&
+  // ALiBi: single request, contiguous key positions (kv_pos padded to whole 64-key blocks)
+  const bool alibi_ok = !a.alibi || (a.kv_pos && !a.segs && !a.req && a.n_req == 0);
+  return (a.hd == 128 || a.hd == 64) && !a.mask && !a.block_id && alibi_ok && a.n >= 1 && a.d % 64 == 0 &&
          (a.P + a.n) < (1LL << 31);
 }
 
 void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s) {
-  if (a.hd == 128) launch_attn<128>(a, scratch, scratch_bytes, s);
-  else launch_attn<64>(a, scratch, scratch_bytes, s);
+  if (a.alibi) {
+    if (a.hd == 128) launch_attn<128, true>(a, scratch, scratch_bytes, s);
+    else launch_attn<64, true>(a, scratch, scratch_bytes, s);
+  } else {
+    if (a.hd == 128) launch_attn<128, false>(a, scratch, scratch_bytes, s);
+    else launch_attn<64, false>(a, scratch, scratch_bytes, s);
+  }
 }
 
 }  // namespace pcb::kern

@@ -83,6 +83,9 @@ struct PhaseDev {
   // [a_row0[s], a_row0[s] + a_rows[s]) of its source (tensor map tkv[s], plane 2 layer + w);
   // the last segment is the request's own rows (first a_tail_vis visible to all queries)
   int a_nseg, a_layer, a_tail_vis;
+  const float* a_alibi;   // ALiBi slopes [aH] (null: off); key positions by key block, query positions
+  const int32_t* a_kpos;
+  const int32_t* a_qpos;
   int a_first[ChainStep::kMaxSeg + 1];
   int a_row0[ChainStep::kMaxSeg];
   int a_rows[ChainStep::kMaxSeg];
@@ -343,7 +346,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             mbar_wait(&a_kvempty[s], ((it / AKV) & 1) ^ 1);
             uint8_t* st = aKV + s * 32768;
             const int b = b0 + it;
-            mbar_expect_tx(&a_kvfull[s], 32768);
+            mbar_expect_tx(&a_kvfull[s], A.a_alibi ? 32768 + 256 : 32768);
+            if (A.a_alibi)  // the block's 64 key positions into the (idle) LN-fold scratch
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      smem_u32(reinterpret_cast<int32_t*>(colsum) + s * 64)),
+                  "l"(A.a_kpos + static_cast<int64_t>(b) * 64), "r"(256), "r"(smem_u32(&a_kvfull[s]))
+                  : "memory");
             if (A.a_nseg) {
               while (b >= A.a_first[sg + 1]) ++sg;
               const int row = A.a_row0[sg] + (b - A.a_first[sg]) * 64;
@@ -539,6 +548,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         float m = -INFINITY, l = 0.f;
         const bool live = (dup ? ((q & 1) * 32) : (q * 32)) < n_;  // else the warp keeps the protocol only
         if (et == 0) ctl(p, ph, 0);
+        // ALiBi in raw score units (the exponent scale is log2(e)/sqrt(128)):
+        //   s + slope sqrt(128) (pos_key - pos_query)
+        const bool alibi = P.a_alibi != nullptr;
+        const int32_t qpos = alibi && c < P.items && qi < n_ ? P.a_qpos[qi] : 0;
+        const float slope_raw = alibi && c < P.items ? P.a_alibi[h] * 11.313708498984761f : 0.f;
         auto blocks = [&](auto ncols) {
           constexpr int NC = decltype(ncols)::value;  // score columns per lane: 64, or 32 (dup)
           const int c0 = NC == 32 ? (row >> 6) * 32 : 0;
@@ -571,6 +585,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               tmem_wait_ld();
 #pragma unroll
               for (int x = 0; x < NC; ++x) sv[x] = __uint_as_float(raw[x]);
+            }
+            if (alibi) {
+              mbar_wait(&a_kvfull[it % AKV], (it / AKV) & 1);  // the positions' bulk copy (complete)
+              const int4* kp = reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(colsum) +
+                                                             (it % AKV) * 64 + c0);
+#pragma unroll
+              for (int x = 0; x < NC; x += 4) {
+                const int4 k4 = kp[x >> 2];
+                sv[x] = fmaf(slope_raw, static_cast<float>(k4.x - qpos), sv[x]);
+                sv[x + 1] = fmaf(slope_raw, static_cast<float>(k4.y - qpos), sv[x + 1]);
+                sv[x + 2] = fmaf(slope_raw, static_cast<float>(k4.z - qpos), sv[x + 2]);
+                sv[x + 3] = fmaf(slope_raw, static_cast<float>(k4.w - qpos), sv[x + 3]);
+              }
             }
             if (NC - 1 > lim) {
 #pragma unroll
@@ -1115,6 +1142,10 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.aP = st.aP;
       d.aH = st.aH;
       d.a_d = st.a_d;
+      d.a_alibi = st.a_alibi;
+      d.a_kpos = st.a_kpos;
+      d.a_qpos = st.a_qpos;
+      if (st.a_alibi && (!st.a_kpos || !st.a_qpos)) throw std::runtime_error("chain: ALiBi needs key and query positions");
       int64_t nblk = (st.aP + st.M + 63) / 64;
       if (st.a_nseg) {
         nblk = 0;

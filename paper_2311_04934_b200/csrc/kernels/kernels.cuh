@@ -153,6 +153,12 @@ struct ChainStep {
     int64_t row0 = 0, rows = 0;
   };
   static constexpr int kMaxSeg = 8;
+  // ALiBi (a_alibi = slopes [a_H]): a_kpos holds the keys' positions in key-block order (each
+  // segment padded to whole 64-key blocks; readable through the last block), a_qpos the n
+  // queries' positions
+  const float* a_alibi = nullptr;
+  const int32_t* a_kpos = nullptr;
+  const int32_t* a_qpos = nullptr;
   int a_nseg = 0;
   int a_layer = 0, a_planes = 0;
   KVSeg a_seg[kMaxSeg];

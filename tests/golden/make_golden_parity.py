@@ -48,12 +48,12 @@ def job_c1(_):
     return "c1", {mode: serve_entry(m.serve(s, p, max_new=32, mode=mode)) for mode in ("cached", "baseline", "oracle")}
 
 
-def job_h128(_):
+def job_h128(alibi=0):
     with open(os.path.join(HERE, "numeric.json")) as f:
         names = [c["name"] for c in json.load(f)["serve"]]
     with open(os.path.join(HERE, "host.json")) as f:
         host = json.load(f)
-    m = RefModel(pc.H128)
+    m = RefModel(pc.H128_ALIBI if alibi else pc.H128)
     out = []
     for name in names:
         if name.startswith("corpus:"):
@@ -64,7 +64,7 @@ def job_h128(_):
             c = next(c for c in host["random_case"] if c["seed"] == seed)
             s, p = c["schema"], c["prompt"]
         out.append(dict(name=name, **serve_entry(m.serve(s, p, max_new=8, mode="cached"))))
-    return "h128", out
+    return ("h128_alibi" if alibi else "h128"), out
 
 
 def job_long(_):
@@ -79,8 +79,8 @@ def job_long(_):
     return "long", r
 
 
-def job_w7b_request(i):
-    m = RefModel(pc.W7B)
+def job_w7b_request(i, alibi=False):
+    m = RefModel(pc.W7B_ALIBI if alibi else pc.W7B)
     res = Ref.resolve(pc.W7B_SCHEMA, pc.W7B_PROMPTS[i])
     toks = [t for u in res["uncached"] for t in u["seg"]["tokens"]]
     pos = [q for u in res["uncached"] for q in u["seg"]["positions"]]
@@ -89,8 +89,12 @@ def job_w7b_request(i):
     v = np.concatenate([x[1] for x in mods], axis=1)
     pp = np.concatenate([x[2] for x in mods])
     logits, _ = m.forward(toks, pos, past=ref_kv(k, v, pp))
-    return f"req{i}", {"tokens": np.array(toks, np.int32), "positions": np.array(pos, np.int64),
-                       "row0": logits[0], "last": logits[-1]}
+    return f"{'alibi_' if alibi else ''}req{i}", {"tokens": np.array(toks, np.int32), "positions": np.array(pos, np.int64),
+                                                   "row0": logits[0], "last": logits[-1]}
+
+
+def job_w7b_alibi(i):
+    return job_w7b_request(i, alibi=True)
 
 
 def job_w7b_prefill(_):
@@ -113,24 +117,35 @@ def run(job):
     return key, val
 
 
-def main():
-    jobs = [(job_w7b_prefill, 0)] + [(job_w7b_request, i) for i in range(len(pc.W7B_PROMPTS))] + \
-           [(job_long, 0), (job_h128, 0), (job_c1, 0)]
+JOBS = {
+    "prefill": [(job_w7b_prefill, 0)],
+    "requests": [(job_w7b_request, i) for i in range(len(pc.W7B_PROMPTS))],
+    "long": [(job_long, 0)], "h128": [(job_h128, 0)], "c1": [(job_c1, 0)],
+    # ALiBi on the tensor-core paths: head-dim-128 corpus, 7B-width suffixes
+    "h128_alibi": [(job_h128, 1)], "alibi_requests": [(job_w7b_alibi, i) for i in (0, 1)],
+}
+
+
+def main(groups):
+    """Regenerates the named job groups (all by default), keeping the other fixtures."""
+    jobs = [j for g in groups for j in JOBS[g]]
     with mp.get_context("fork").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
         results = dict(pool.map(run, jobs))
     failed = {k: v for k, v in results.items() if isinstance(v, Exception)}
     if failed:
         raise SystemExit(f"reference jobs failed: {failed}")
-    parity = {k: results[k] for k in ("c1", "h128", "long")}
-    with open(os.path.join(HERE, "parity.json"), "w") as f:
+    jpath, npath = os.path.join(HERE, "parity.json"), os.path.join(HERE, "parity_w7b.npz")
+    parity = json.load(open(jpath)) if os.path.exists(jpath) else {}
+    parity.update({k: v for k, v in results.items() if k in ("c1", "h128", "long", "h128_alibi")})
+    with open(jpath, "w") as f:
         json.dump(parity, f, separators=(",", ":"))
-    flat = {}
-    for key in [k for k in results if k.startswith("req") or k == "prefill"]:
+    flat = dict(np.load(npath)) if os.path.exists(npath) else {}
+    for key in [k for k in results if "req" in k or k == "prefill"]:
         for name, arr in results[key].items():
             flat[f"{key}_{name}"] = arr
-    np.savez(os.path.join(HERE, "parity_w7b.npz"), **flat)
-    print("wrote parity.json, parity_w7b.npz")
+    np.savez(npath, **flat)
+    print("wrote", jpath, npath)
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or list(JOBS))

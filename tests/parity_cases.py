@@ -31,6 +31,10 @@ H128_LONG = dict(H128, max_position=32768)
 W7B = dict(n_layers=2, n_heads=32, head_dim=128, hidden=4096, vocab_size=32000, pos_encoding="rope",
            max_position=8192, bytes_per_element=2, seed=42)
 
+# ALiBi variants: no RoPE, per-head linear position bias in the attention
+H128_ALIBI = dict(H128, pos_encoding="alibi")
+W7B_ALIBI = dict(W7B, pos_encoding="alibi")
+
 # configs[0]: a 68-token system module + a 512-token document + 32 uncached tokens
 C1_SYSTEM = "You are a careful assistant. Answer only from the document; cite it."
 assert len(C1_SYSTEM) == 68

@@ -229,3 +229,56 @@ def test_w7b_prefill_matches_reference(w7b, w7b_gold):
     rows = w7b_gold["prefill_kv_rows"]
     assert rel(kv.layer(1, 0)[rows], w7b_gold["prefill_k1"]) <= BF16_REL
     assert rel(kv.layer(1, 1)[rows], w7b_gold["prefill_v1"]) <= BF16_REL
+
+
+# ---------------------------------------------------------------------------
+# ALiBi on the tensor-core attention (reference model.cpp:231-235, 410-411):
+# the chain's attention phase (zero-copy segments: per-block key positions, incl. the
+# non-monotonic positions of the corpus), the copy path and the standalone kernel
+# ---------------------------------------------------------------------------
+def test_alibi_hd128_corpus_matches_reference(parity, host_golden):
+    m = pcb.Model(pc.H128_ALIBI, dtype=pcb.BF16)
+    worst = 0.0
+    variants = (("zero-copy", {}), ("copy", {"zero_copy": 0}), ("standalone", {"zero_copy": 0, "chain_attn": 0}))
+    for case in parity["h128_alibi"]:
+        schema, prompt = _corpus_inputs(host_golden, case["name"])
+        want = f32(case["logits"])
+        store = pcb.ModuleStore(m)
+        store.encode_schema(schema)
+        for variant, opts in variants:
+            for k, v in opts.items():
+                m.set_option(k, v)
+            r = pcb.serve(store, schema, prompt, 8)
+            for k in opts:
+                m.set_option(k, 1)
+            assert r.cache_report["uncached_token_count"] == case["report"]["uncached_token_count"]
+            worst = max(worst, check_bf16(r.first_token_logits, want, f"alibi h128 {case['name']} {variant}"))
+            record_sequence(r.output_tokens, case["tokens"], f"alibi h128 {case['name']} {variant}")
+        b = pcb.serve_batch(store, schema, [prompt] * 2, micro_batch=2)  # ALiBi: single-request path
+        worst = max(worst, check_bf16(b[1].first_token_logits, want, f"alibi h128 {case['name']} batch"))
+    print(f"ALiBi hd128 corpus: worst rel {worst:.3e}")
+
+
+def test_alibi_w7b_matches_reference(w7b_gold):
+    m = pcb.Model(pc.W7B_ALIBI, dtype=pcb.BF16)
+    schema = pcb.Schema.parse(pc.W7B_SCHEMA)
+    store = pcb.ModuleStore(m)
+    mods = [pc.w7b_module_kv(i) for i in range(2)]
+    for i, (k, v, pos) in enumerate(mods):
+        store.put_kv(schema, f"doc{i}", m.upload_kv(k, v, pos))
+    for i in (0, 1):
+        want = w7b_gold[f"alibi_req{i}_last"]
+        for variant, opts in (("zero-copy", {}), ("copy", {"zero_copy": 0}),
+                              ("standalone", {"zero_copy": 0, "chain_attn": 0})):
+            for k, v in opts.items():
+                m.set_option(k, v)
+            r = pcb.serve(store, schema, pc.W7B_PROMPTS[i], 1)
+            for k in opts:
+                m.set_option(k, 1)
+            check_bf16(r.first_token_logits, want, f"alibi w7b req{i} {variant}")
+    k = np.concatenate([mods[0][0], mods[1][0]], axis=1)
+    v = np.concatenate([mods[0][1], mods[1][1]], axis=1)
+    past = m.upload_kv(k, v, np.concatenate([mods[0][2], mods[1][2]]))
+    logits, _ = m.forward(w7b_gold["alibi_req0_tokens"], w7b_gold["alibi_req0_positions"], past=past)
+    check_bf16(logits[0], w7b_gold["alibi_req0_row0"], "alibi w7b forward row0")
+    check_bf16(logits[-1], w7b_gold["alibi_req0_last"], "alibi w7b forward row63")
