@@ -437,8 +437,12 @@ def run_c5(a) -> None:
     n_mod = a.c5_modules
     cfg = dict(n_layers=a.c5_layers, n_heads=64, head_dim=128, hidden=8192, vocab_size=32000, pos_encoding="rope",
                max_position=n_mod * 1024 + 256, bytes_per_element=2, seed=42)
-    nid = pcb.share_nccl_id(D.dist) if D.world > 1 else None
-    model = pcb.Model(cfg, dtype=pcb.BF16, device=D.local, tp_rank=D.rank, tp_size=D.world, nccl_id=nid)
+    if D.world > 1 and a.tp_transport == "peer":  # CUDA-IPC peer memory, one-shot collectives
+        peer = pcb.peer_group(D.dist, device=D.local, cap_floats=1024 * cfg["hidden"])
+        model = pcb.Model(cfg, dtype=pcb.BF16, peer=peer)
+    else:
+        nid = pcb.share_nccl_id(D.dist) if D.world > 1 else None
+        model = pcb.Model(cfg, dtype=pcb.BF16, device=D.local, tp_rank=D.rank, tp_size=D.world, nccl_id=nid)
     schema_text, prompts, _ = workload_c4(n_mod, 1024, 16, 4, 64)
     schema = pcb.Schema.parse(schema_text)
     store = pcb.ModuleStore(model)
@@ -466,7 +470,8 @@ def run_c5(a) -> None:
                     "seeded PCG32 streams, sharded by rank)",
             "config": {"workload": f"configs[4]: Llama-2-70B shape ({a.c5_layers} layers), {n_mod} x 1024-token "
                                    "module store head-sharded, 4 modules (4096 cached) + 64 uncached per request",
-                       "parallelism": f"tp{D.world}", "cached_tokens": 4096, "uncached_tokens": 64},
+                       "parallelism": f"tp{D.world}", "tp_transport": a.tp_transport if D.world > 1 else None,
+                       "cached_tokens": 4096, "uncached_tokens": 64},
             "ttft_ms": D.max(statistics.mean(ttfts)), "precompute_s": precompute_s,
             "store_gb_per_gpu": n_mod * 1024 * 2 * a.c5_layers * 8192 * 2 / D.world / 1e9}), flush=True)
     D.close()
@@ -774,6 +779,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
     ap.add_argument("--c5-layers", type=int, default=80)
     ap.add_argument("--c5-modules", type=int, default=64)
+    ap.add_argument("--tp-transport", default="nccl", choices=["nccl", "peer"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--skip-batch", action="store_true")

@@ -42,6 +42,7 @@ typedef struct pcb_kv pcb_kv;             /* pc::model::KVState, device resident
 typedef struct pcb_store pcb_store;       /* pc::cache::ModuleStore */
 typedef struct pcb_response pcb_response; /* pc::engine::ServeResponse */
 typedef struct pcb_group pcb_group;       /* tensor-parallel ranks as threads of one process (tests) */
+typedef struct pcb_peer pcb_peer;         /* this rank's CUDA-IPC region of a peer-memory TP group */
 
 const char* pcb_last_error(void);
 int pcb_last_error_code(void);
@@ -81,6 +82,16 @@ int pcb_group_create(int size, pcb_group** out);
 void pcb_group_destroy(pcb_group* g);
 int pcb_model_create_tp(const char* config_json, int dtype, int device, int tp_rank, int tp_size,
                         const uint8_t* nccl_id, pcb_group* group, pcb_model** out);
+/* Peer-memory transport (one process per rank; no NCCL): each rank creates its region
+ * (cap_floats >= the largest collective: n_tokens * hidden for the all-reduces, n_tokens *
+ * vocab/tp for the logits gather) and receives its 64-byte CUDA IPC handle; after every
+ * rank has exchanged handles out of band (handles [tp_size][64] in rank order),
+ * pcb_peer_open maps the peers and pcb_model_create_tp_peer builds the rank's model.
+ * Collectives are one-shot kernels over the mapped slots (NVLink loads between GPUs). */
+int pcb_peer_create(int tp_rank, int tp_size, int device, int64_t cap_floats, uint8_t* handle_out_64, pcb_peer** out);
+int pcb_peer_open(pcb_peer* p, const uint8_t* handles);
+void pcb_peer_destroy(pcb_peer* p);
+int pcb_model_create_tp_peer(const char* config_json, int dtype, pcb_peer* peer, pcb_model** out);
 void pcb_model_destroy(pcb_model* m);
 /* Options (value 0/1 unless noted): "profile" (per-kernel-class CUDA-event timing),
  * "force_simt" / "force_simt_gemm" / "force_simt_attn" (testing: SIMT kernels only),

@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = [
     "PromptCacheError", "Schema", "Prompt", "Model", "KV", "ModuleStore", "ServeResponse",
-    "serve", "serve_batch", "oracle_serve", "TPGroup", "nccl_unique_id", "tp_shard_plan", "share_nccl_id", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
+    "serve", "serve_batch", "oracle_serve", "TPGroup", "PeerRegion", "peer_group", "nccl_unique_id", "tp_shard_plan", "share_nccl_id", "concat_kv", "config_hash", "config_canonical", "per_token_bytes",
     "F32", "BF16", "FAST", "SLOW", "lib", "LIB_PATH",
 ]
 
@@ -95,6 +95,8 @@ def lib():
         "pcb_group_create": (i32, [i32, pvp]),
         "pcb_group_destroy": (None, [vp]),
         "pcb_model_create_tp": (i32, [C.c_char_p, i32, i32, i32, i32, vp, vp, pvp]),
+        "pcb_peer_create": (i32, [i32, i32, i32, i64, vp, pvp]), "pcb_peer_open": (i32, [vp, vp]),
+        "pcb_peer_destroy": (None, [vp]), "pcb_model_create_tp_peer": (i32, [cp, i32, vp, pvp]),
         "pcb_response_json": (vp, [vp]), "pcb_response_tokens": (i32, [vp, vp, i32]),
         "pcb_response_first_logits": (i32, [vp, vp, i32]), "pcb_response_destroy": (None, [vp]),
     }
@@ -290,14 +292,47 @@ class TPGroup(_Handle):
         self.size = size
 
 
+class PeerRegion(_Handle):
+    """This rank's CUDA-IPC region of a peer-memory tensor-parallel group (one process per
+    rank, no NCCL): create, exchange ``handle`` with every rank out of band, then ``open``
+    with all handles in rank order (see ``peer_group``)."""
+    _destroy = "pcb_peer_destroy"
+
+    def __init__(self, tp_rank: int, tp_size: int, device: int = 0, cap_floats: int = 1 << 22):
+        h = C.c_void_p()
+        buf = C.create_string_buffer(64)
+        _check(lib().pcb_peer_create(tp_rank, tp_size, device, cap_floats, buf, C.byref(h)))
+        super().__init__(h.value)
+        self.handle_bytes = buf.raw
+        self.tp_rank, self.tp_size, self.device = tp_rank, tp_size, device
+
+    def open(self, handles: list[bytes]):
+        blob = b"".join(handles)
+        _check(lib().pcb_peer_open(self._h, C.create_string_buffer(blob, len(blob))))
+
+
+def peer_group(dist, device: int = 0, cap_floats: int = 1 << 22) -> PeerRegion:
+    """Every rank of a torch.distributed group: its region, opened over all ranks' handles."""
+    r = PeerRegion(dist.get_rank(), dist.get_world_size(), device, cap_floats)
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, r.handle_bytes)
+    r.open(handles)
+    return r
+
+
 class Model(_Handle):
     _destroy = "pcb_model_destroy"
 
     def __init__(self, config: dict, dtype: int = BF16, device: int = 0, tp_rank: int = 0, tp_size: int = 1,
-                 nccl_id: bytes | None = None, group: "TPGroup | None" = None):
-        """tp_size > 1: head-sharded rank over NCCL (nccl_id) or a TPGroup."""
+                 nccl_id: bytes | None = None, group: "TPGroup | None" = None, peer: "PeerRegion | None" = None):
+        """tp_size > 1: head-sharded rank over NCCL (nccl_id), a TPGroup
+        (threads), or a PeerRegion (processes sharing CUDA-IPC buffers)."""
         h = C.c_void_p()
-        if tp_size == 1:
+        if peer is not None:
+            tp_rank, tp_size, device = peer.tp_rank, peer.tp_size, peer.device
+            _check(lib().pcb_model_create_tp_peer(_enc(json.dumps(config)), dtype, peer.handle, C.byref(h)))
+            self._peer = peer  # the region outlives the model's collectives
+        elif tp_size == 1:
             _check(lib().pcb_model_create(_enc(json.dumps(config)), dtype, device, C.byref(h)))
         else:
             nid = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)

@@ -42,6 +42,9 @@ struct pcb_kv {
 struct pcb_store {
   std::unique_ptr<cache::ModuleStore> s;
 };
+struct pcb_peer {
+  std::shared_ptr<coll::PeerRegion> r;
+};
 struct pcb_response {
   engine::ServeResponse r;
 };
@@ -164,6 +167,24 @@ int pcb_group_create(int size, pcb_group** out) {
   });
 }
 void pcb_group_destroy(pcb_group* g) { delete g; }
+int pcb_peer_create(int tp_rank, int tp_size, int device, int64_t cap_floats, uint8_t* handle_out, pcb_peer** out) {
+  return guard([&] {
+    auto r = std::make_shared<coll::PeerRegion>(tp_rank, tp_size, device, static_cast<size_t>(cap_floats));
+    r->handle(handle_out);
+    *out = new pcb_peer{r};
+  });
+}
+int pcb_peer_open(pcb_peer* p, const uint8_t* handles) {
+  return guard([&] { p->r->open(handles); });
+}
+void pcb_peer_destroy(pcb_peer* p) { delete p; }
+int pcb_model_create_tp_peer(const char* cfg, int dtype, pcb_peer* peer, pcb_model** out) {
+  return guard([&] {
+    auto& r = *peer->r;
+    *out = new pcb_model{std::make_unique<model::Model>(model::ModelConfig::from_json(cfg), dtype, r.device, r.rank,
+                                                         r.size, coll::make_peer(peer->r))};
+  });
+}
 int pcb_model_create_tp(const char* cfg, int dtype, int device, int tp_rank, int tp_size, const uint8_t* nccl_id,
                         pcb_group* group, pcb_model** out) {
   return guard([&] {

@@ -33,6 +33,29 @@ constexpr int kNcclIdBytes = 128;
 void nccl_unique_id(uint8_t out[kNcclIdBytes]);
 std::shared_ptr<Collective> make_nccl(const uint8_t id[kNcclIdBytes], int rank, int size, int device);
 
+// ---- peer memory: one process per rank, buffers shared through CUDA IPC ----
+// Each rank owns one device region [flags][2 slots of cap floats]; every rank maps every
+// peer's region (cudaIpcOpenMemHandle: NVLink/NVSwitch loads between GPUs, or plain device
+// memory when several ranks share one GPU).  A collective is one-shot: publish into this
+// rank's slot (generation parity), release the generation flag at system scope, then every
+// rank reads all slots in rank order (deterministic sums) once every peer's flag has it.
+constexpr int kIpcHandleBytes = 64;
+class PeerRegion {
+ public:
+  PeerRegion(int rank, int size, int device, size_t cap_floats);
+  ~PeerRegion();
+  PeerRegion(const PeerRegion&) = delete;
+  PeerRegion& operator=(const PeerRegion&) = delete;
+  void handle(uint8_t out[kIpcHandleBytes]) const;                    // this rank's IPC handle
+  void open(const uint8_t* handles /* [size][kIpcHandleBytes] */);    // map every peer
+  int rank, size, device;
+  size_t cap;                 // floats per slot
+  char* local = nullptr;      // this rank's region
+  std::vector<char*> peers;   // every rank's region (local for r == rank)
+  char** d_peers = nullptr;   // the same table on the device
+};
+std::shared_ptr<Collective> make_peer(std::shared_ptr<PeerRegion> region);
+
 // ---- one process, ranks as threads on one device ----
 class LocalGroup {
  public:

@@ -282,3 +282,51 @@ def test_alibi_w7b_matches_reference(w7b_gold):
     logits, _ = m.forward(w7b_gold["alibi_req0_tokens"], w7b_gold["alibi_req0_positions"], past=past)
     check_bf16(logits[0], w7b_gold["alibi_req0_row0"], "alibi w7b forward row0")
     check_bf16(logits[-1], w7b_gold["alibi_req0_last"], "alibi w7b forward row63")
+
+
+# ---------------------------------------------------------------------------
+# PCST persistence of a bf16 store (reference cache.cpp:178-271): fp32 on
+# disk, bf16 on upload -- bf16 values survive the round trip exactly, in both tiers
+# ---------------------------------------------------------------------------
+def test_bf16_pcst_round_trip_and_tiers(parity, host_golden, tmp_path):
+    m = pcb.Model(pc.H128, dtype=pcb.BF16)
+    case = parity["h128"][0]
+    schema, prompt = _corpus_inputs(host_golden, case["name"])
+    store = pcb.ModuleStore(m)
+    store.encode_schema(schema)
+    a, b = str(tmp_path / "a.pcst"), str(tmp_path / "b.pcst")
+    store.save(a)
+    fast = pcb.ModuleStore(m)
+    fast.load(a)
+    fast.save(b)
+    assert open(a, "rb").read() == open(b, "rb").read()  # bf16 -> fp32 -> bf16 is exact
+    for name in (e for e in schema.plan()["order"]):
+        x, y = store.lookup(schema.name, name), fast.lookup(schema.name, name)
+        assert np.array_equal(x.k(), y.k()) and np.array_equal(x.v(), y.v())
+    r0 = pcb.serve(store, schema, prompt, 4)
+    r1 = pcb.serve(fast, schema, prompt, 4)
+    assert np.array_equal(r0.first_token_logits, r1.first_token_logits) and r0.output_tokens == r1.output_tokens
+    check_bf16(r1.first_token_logits, f32(case["logits"]), "pcst bf16 reload")
+
+
+def test_pcst_shard_identity_is_checked(tmp_path):
+    """A head-sharded rank's store file carries its (rank, size): another rank of the same
+    config refuses it with ConfigHashMismatch instead of loading the wrong heads."""
+    import threading
+
+    cfg = dict(pc.H128, n_heads=2)
+    group = pcb.TPGroup(2)
+    models = [pcb.Model(cfg, dtype=pcb.BF16, device=0, tp_rank=r, tp_size=2, group=group) for r in range(2)]
+    schema = pcb.Schema.parse('<schema name="s"><module name="m">sharded module text</module></schema>')
+    stores = [pcb.ModuleStore(mm) for mm in models]
+    th = [threading.Thread(target=stores[r].encode_schema, args=(schema,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    path = str(tmp_path / "rank0.pcst")
+    stores[0].save(path)
+    pcb.ModuleStore(models[0]).load(path)  # its own rank: fine
+    with pytest.raises(pcb.PromptCacheError) as e:
+        pcb.ModuleStore(models[1]).load(path)
+    assert e.value.code == "ConfigHashMismatch"
