@@ -497,14 +497,17 @@ def serve(store: ModuleStore, schema: Schema, prompt, max_new_tokens: int = 16, 
     return ServeResponse._from(h.value, store.model.vocab)
 
 
-def serve_batch(store: ModuleStore, schema: Schema, prompts, micro_batch: int = 4) -> list:
+def serve_batch(store: ModuleStore, schema: Schema, prompts, micro_batch: int = 4, after=None) -> list:
     """engine::serve_batch: first tokens of many requests, micro_batch requests per assembly
-    launch and suffix prefill."""
+    launch and suffix prefill.  ``after`` (optional) is called as soon
+    as the native call returns, before the Python response objects are built (timing)."""
     ps = [_prompt(p) for p in prompts]
     n = len(ps)
     arr = (C.c_void_p * max(n, 1))(*[p.handle for p in ps])
     outs = (C.c_void_p * max(n, 1))()
     _check(lib().pcb_serve_batch(store.handle, schema.handle, arr, n, micro_batch, outs))
+    if after is not None:
+        after()
     return [ServeResponse._from(outs[i], store.model.vocab) for i in range(n)]
 
 

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <algorithm>
+#include <cstdio>
 #include <set>
 
 #include "../kernels/kernels.cuh"
@@ -148,6 +149,34 @@ struct AsmScratch {
     }
   }
 };
+
+// serve_batch's two pipelined result slots (pinned logits / tokens, events)
+struct BatchSlot {
+  float* h_logits = nullptr;
+  int32_t* h_tok = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev[3] = {};
+  cudaEvent_t segs_used = nullptr;  // the assembly's segment list left host memory
+  cudaEvent_t done = nullptr;       // logits and tokens are in this slot's host buffers
+};
+struct BatchSlots {
+  BatchSlot s[2];
+  ~BatchSlots() {
+    for (BatchSlot& sl : s) {
+      if (sl.done) cudaEventSynchronize(sl.done);
+      if (sl.h_logits) cudaFreeHost(sl.h_logits);
+      if (sl.h_tok) cudaFreeHost(sl.h_tok);
+      for (auto& e : sl.ev)
+        if (e) cudaEventDestroy(e);
+      if (sl.segs_used) cudaEventDestroy(sl.segs_used);
+      if (sl.done) cudaEventDestroy(sl.done);
+    }
+  }
+};
+BatchSlots& batch_slots_of(cache::ModuleStore& store) {
+  if (!store.batch_slots) store.batch_slots = std::make_shared<BatchSlots>();
+  return *static_cast<BatchSlots*>(store.batch_slots.get());
+}
 
 AsmScratch& scratch_of(cache::ModuleStore& store) {
   if (!store.assembly_scratch) store.assembly_scratch = std::make_shared<AsmScratch>();
@@ -569,31 +598,15 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
     }
     return bt;
   };
-  // Per-slot host buffers and events: micro-batch k+1 is launched (queued behind k on the
+  // Per-slot host buffers and events (store-owned, reused across calls: pinned allocations
+  // and frees synchronise the device): micro-batch k+1 is launched (queued behind k on the
   // stream) before k's results are collected, so the device never waits for the host's
   // resolve/lookup of the next micro-batch (it did: ~20% idle per 32-request micro-batch).
-  struct Slot {
-    float* h_logits = nullptr;
-    int32_t* h_tok = nullptr;
-    size_t cap = 0;
-    cudaEvent_t ev[3] = {};
-    cudaEvent_t segs_used = nullptr;  // the assembly's segment list left host memory
-    cudaEvent_t done = nullptr;       // logits and tokens are in this slot's host buffers
-  };
-  Slot slots[2];
-  auto free_slots = [&]() {
-    for (Slot& sl : slots) {
-      if (sl.h_logits) cudaFreeHost(sl.h_logits);
-      if (sl.h_tok) cudaFreeHost(sl.h_tok);
-      for (auto& e : sl.ev)
-        if (e) cudaEventDestroy(e);
-      if (sl.segs_used) cudaEventDestroy(sl.segs_used);
-      if (sl.done) cudaEventDestroy(sl.done);
-    }
-  };
+  BatchSlots& bs = batch_slots_of(store);
+  BatchSlot* slots = bs.s;
   AsmScratch& sc = scratch_of(store);
   sc.ensure(0, 0, V);
-  auto launch = [&](Batch& bt, Slot& sl) {
+  auto launch = [&](Batch& bt, BatchSlot& sl) {
     const size_t B = bt.items.size();
     if (sl.cap < B) {
       if (sl.h_logits) cudaFreeHost(sl.h_logits);
@@ -686,7 +699,7 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
     CK(cudaMemcpyAsync(sl.h_tok, m.device_argmax(), B * sizeof(int32_t), cudaMemcpyDeviceToHost, m.stream()));
     CK(cudaEventRecord(sl.done, m.stream()));
   };
-  auto finish = [&](Batch& bt, Slot& sl) {
+  auto finish = [&](Batch& bt, BatchSlot& sl) {
     CK(cudaEventSynchronize(sl.done));
     float ms_asm = 0, ms_pre = 0;
     CK(cudaEventElapsedTime(&ms_asm, sl.ev[0], sl.ev[1]));
@@ -703,26 +716,38 @@ std::vector<ServeResponse> serve_batch(const std::vector<ServeRequest>& reqs, co
       resp.timings.ttft_us = ttft;
     }
   };
+  static const bool trace = std::getenv("PCB_BATCH_TRACE") != nullptr;  // host-side phase times (debug)
+  auto stamp = [&](const char* what, Clock::time_point t) {
+    if (trace) std::fprintf(stderr, "[serve_batch] %-8s %9.3f ms\n", what, us_since(t) / 1e3);
+  };
   try {
+    auto t = Clock::now();
     Batch cur = prep(0);
+    stamp("prep", t);
     int slot = 0;
+    t = Clock::now();
     if (!cur.items.empty()) launch(cur, slots[slot]);
+    stamp("launch", t);
     for (size_t b0 = 0; b0 < reqs.size(); b0 += micro_batch) {
       Batch nxt;
       if (b0 + micro_batch < reqs.size()) {
+        t = Clock::now();
         nxt = prep(b0 + micro_batch);
+        stamp("prep", t);
+        t = Clock::now();
         if (!nxt.items.empty()) launch(nxt, slots[slot ^ 1]);
+        stamp("launch", t);
       }
+      t = Clock::now();
       if (!cur.items.empty()) finish(cur, slots[slot]);
+      stamp("finish", t);
       cur = std::move(nxt);
       slot ^= 1;
     }
   } catch (...) {
     cudaStreamSynchronize(m.stream());
-    free_slots();
     throw;
   }
-  free_slots();
   return out;
 }
 

@@ -77,6 +77,11 @@ struct AttnParams {
   // readable up to the last 64-key block (the producer copies whole blocks)
   const float* alibi = nullptr;
   const int32_t* kv_pos = nullptr;
+  // duplicated queries (batched requests of <= 64 rows, one split): the Q tile holds the
+  // request's rows twice; TMEM lanes [0, 64) take keys [0, 32) of every 64-key block and
+  // lanes [64, 128) keys [32, 64), and the two halves of a query merge at the end -- all
+  // four softmax warps work, each on half a block (with one copy, half the lanes idled)
+  int dup = 0;
   unsigned long long* dbg = nullptr;  // timeline probe (CTA 0): [event][iteration] globaltimer ns
   unsigned long long* tl = nullptr;   // per-CTA phase timeline [cta][8] (PCB_ATTN_TL)
 };
@@ -215,8 +220,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.maps + p.segs[breq * kSeg + g].x)
                      : "memory");
       mbar_expect_tx(q_full, S::kQ);
-      for (int a = 0; a < S::kAtoms; ++a)
-        tma_load_2d(sQ + a * (BQ * 128), &tmQ, q_full, h * HD + a * 64, static_cast<int>(qrow0 + q0));
+      for (int a = 0; a < S::kAtoms; ++a)  // 64-row boxes: rows [q0, q0 + 128), or [q0, q0 + 64) twice (dup)
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(sQ + a * (BQ * 128) + hh * (64 * 128), &tmQ, q_full, h * HD + a * 64,
+                      static_cast<int>(qrow0 + q0 + (p.dup ? 0 : 64 * hh)));
       for (int it = 0, sg = 0; it < nb; ++it) {
         const int s = it % KV_STAGES;
         mbar_wait(&kv_empty[s], ((it / KV_STAGES) & 1) ^ 1);
@@ -303,13 +310,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // ---- softmax warps: query row = TMEM lane ----
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
-    const int64_t qi = q0 + r;       // query index within the n new rows
-    const int64_t limit = P_ + qi;  // last visible key (sequence order)
+    const bool dup = p.dup != 0;
+    const int64_t qi = dup ? (r & 63) : q0 + r;  // query index within the n new rows
+    const int64_t limit = P_ + qi;              // last visible key (sequence order)
+    const int c0 = dup ? (r >> 6) * 32 : 0;     // dup: this lane's half of every key block
     const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
     float m = -INFINITY, l = 0.f;
     // a warp whose 32 query rows are all past n (the suffix fills half a 128-row tile)
     // only keeps the barrier protocol: its P rows feed O rows nobody reads
-    const bool live = q0 + qd * 32 < n_;
+    const bool live = (dup ? (qd & 1) * 32 : q0 + qd * 32) < n_;
     // ALiBi in raw score units: (s + slope sqrt(hd) (pk - pq)) * log2(e)/sqrt(hd)
     //   = (s / sqrt(hd) + slope (pk - pq)) log2(e)
     int32_t qpos = 0;
@@ -318,132 +327,176 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       qpos = qi < n_ ? p.kv_pos[P_ + qi] : 0;
       slope_raw = p.alibi[h] * sqrtf(static_cast<float>(HD));
     }
-    for (int it = 0, sg = 0; it < nb; ++it) {
-      int64_t j0 = (b0 + it) * BKV, lim_seg = 0;
-      if (p.segs) {  // zero-copy: mask per segment (module padding rows; causal tail)
-        const int b = static_cast<int>(b0) + it;
-        while (b >= seg_first[sg + 1]) ++sg;
-        const int64_t local = static_cast<int64_t>(b - seg_first[sg]) * BKV;
-        lim_seg = sg == nseg - 1 ? tail_vis + qi - local : p.segs[breq * kSeg + sg].z - 1 - local;
-        j0 = limit - lim_seg;  // so that key c is masked iff c > lim_seg, as below
-      }
-      if (!live) {
-        // p_full[it&1]'s previous phase (block it-2) completed before PV(it-2) was issued
-        if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
-        mbar_arrive(&p_full[it & 1]);
-        continue;
-      }
-      mbar_wait(&s_full[it & 1], (it >> 1) & 1);
-      if (threadIdx.x == 128) probe(p, 0, it);
-      tc_fence_after();
-      float sv[BKV];
-      {
-        uint32_t raw[BKV];
-#pragma unroll
-        for (int c = 0; c < BKV; c += 16) tmem_ld16_nowait(tmem + (it & 1) * BKV + lane_off + c, raw + c);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < BKV; ++c) sv[c] = __uint_as_float(raw[c]);
-      }
-      if (threadIdx.x == 128) probe(p, 6, it);
-      if constexpr (AL) {
-        const int s = it % KV_STAGES;
-        mbar_wait(&kv_full[s], (it / KV_STAGES) & 1);  // the positions' bulk copy (already complete)
-        const int4* kp = reinterpret_cast<const int4*>(sPos + s * BKV);
-#pragma unroll
-        for (int c = 0; c < BKV; c += 4) {
-          const int4 k4 = kp[c >> 2];
-          sv[c] = fmaf(slope_raw, static_cast<float>(k4.x - qpos), sv[c]);
-          sv[c + 1] = fmaf(slope_raw, static_cast<float>(k4.y - qpos), sv[c + 1]);
-          sv[c + 2] = fmaf(slope_raw, static_cast<float>(k4.z - qpos), sv[c + 2]);
-          sv[c + 3] = fmaf(slope_raw, static_cast<float>(k4.w - qpos), sv[c + 3]);
+    // one key block: NC score columns of this lane ([c0, c0 + NC) of the block; NC = 32 in dup mode)
+    auto blocks = [&](auto ncols) {
+      constexpr int NC = decltype(ncols)::value;
+      for (int it = 0, sg = 0; it < nb; ++it) {
+        int64_t j0 = (b0 + it) * BKV, lim_seg = 0;
+        if (p.segs) {  // zero-copy: mask per segment (module padding rows; causal tail)
+          const int b = static_cast<int>(b0) + it;
+          while (b >= seg_first[sg + 1]) ++sg;
+          const int64_t local = static_cast<int64_t>(b - seg_first[sg]) * BKV;
+          lim_seg = sg == nseg - 1 ? tail_vis + qi - local : p.segs[breq * kSeg + sg].z - 1 - local;
+          j0 = limit - lim_seg;  // so that key c is masked iff c > lim_seg, as below
         }
-      }
-      // scores stay raw (unscaled); the 1/sqrt(hd) * log2(e) factor is folded into
-      // one FFMA per element in front of ex2.approx
-      if (j0 + BKV - 1 > limit) {  // diagonal block (or a segment's padding) only
-#pragma unroll
-        for (int c = 0; c < BKV; ++c)
-          if (j0 + c > limit) sv[c] = -INFINITY;
-      }
-      // 8 independent max chains + a 3-level tree (a single chain is 63 dependent FMNMX)
-      float mx[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) mx[c] = sv[c];
-#pragma unroll
-      for (int c = 8; c < BKV; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
-#pragma unroll
-      for (int w = 4; w; w >>= 1)
-#pragma unroll
-        for (int c = 0; c < w; ++c) mx[c] = fmaxf(mx[c], mx[c + w]);
-      const float bm = mx[0];
-      // lazy max update: move the reference max only when it grows by > 2^8
-      const bool grow = bm > m + kRescaleThreshold / p.scale_log2 || (m == -INFINITY && bm > -INFINITY);
-      if (__any_sync(0xffffffffu, grow) && it > 0) {
-        // O holds blocks < it: wait for PV(it-1), then scale the rows that grow
-        mbar_wait(&pv_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        j0 += c0;  // first key of this lane's columns
+        if (!live) {
+          // p_full[it&1]'s previous phase (block it-2) completed before PV(it-2) was issued
+          if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
+          mbar_arrive(&p_full[it & 1]);
+          continue;
+        }
+        mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+        if (threadIdx.x == 128) probe(p, 0, it);
         tc_fence_after();
-        const float f = grow ? fast_exp2((m - bm) * p.scale_log2) : 1.f;  // m = -inf -> 0
-#pragma unroll 1
-        for (int c = 0; c < HD; c += 16) {
-          float ov[16];
-          tmem_ld16(tO + lane_off + c, ov);
+        float sv[NC];
+        {
+          uint32_t raw[NC];
 #pragma unroll
-          for (int x = 0; x < 16; ++x) ov[x] *= f;
-          tmem_st16(tO + lane_off + c, ov);
+          for (int c = 0; c < NC; c += 16) tmem_ld16_nowait(tmem + (it & 1) * BKV + lane_off + c0 + c, raw + c);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < NC; ++c) sv[c] = __uint_as_float(raw[c]);
         }
-        tmem_st_wait();
-      }
-      if (grow) {
-        l *= fast_exp2((m - bm) * p.scale_log2);
-        m = bm;
-      }
-      const float mb = (m == -INFINITY) ? 0.f : m * p.scale_log2;  // all scores -inf when m is
-      float bs[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
-      uint32_t packed[BKV / 2];
+        if (threadIdx.x == 128) probe(p, 6, it);
+        if constexpr (AL) {
+          const int s = it % KV_STAGES;
+          mbar_wait(&kv_full[s], (it / KV_STAGES) & 1);  // the positions' bulk copy (already complete)
+          const int4* kp = reinterpret_cast<const int4*>(sPos + s * BKV + c0);
 #pragma unroll
-      for (int c = 0; c < BKV; c += 2) {
-        const float p0 = fast_exp2(fmaf(sv[c], p.scale_log2, -mb));
-        const float p1 = fast_exp2(fmaf(sv[c + 1], p.scale_log2, -mb));
-        bs[(c >> 1) & 3] += p0 + p1;
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-        packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-      }
-      l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
-      if (threadIdx.x == 128) probe(p, 7, it);
-      // P buffer it&1 is free once PV(it-2) completed
-      if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
-      if (threadIdx.x == 128) probe(p, 8, it);
-      uint8_t* prow = sP + (it & 1) * S::kP + r * 128;
+          for (int c = 0; c < NC; c += 4) {
+            const int4 k4 = kp[c >> 2];
+            sv[c] = fmaf(slope_raw, static_cast<float>(k4.x - qpos), sv[c]);
+            sv[c + 1] = fmaf(slope_raw, static_cast<float>(k4.y - qpos), sv[c + 1]);
+            sv[c + 2] = fmaf(slope_raw, static_cast<float>(k4.z - qpos), sv[c + 2]);
+            sv[c + 3] = fmaf(slope_raw, static_cast<float>(k4.w - qpos), sv[c + 3]);
+          }
+        }
+        // scores stay raw (unscaled); the 1/sqrt(hd) * log2(e) factor is folded into
+        // one FFMA per element in front of ex2.approx
+        if (j0 + NC - 1 > limit) {  // diagonal block (or a segment's padding) only
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4 v = make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = v;
+          for (int c = 0; c < NC; ++c)
+            if (j0 + c > limit) sv[c] = -INFINITY;
+        }
+        // 8 independent max chains + a 3-level tree (a single chain is 63 dependent FMNMX)
+        float mx[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mx[c] = sv[c];
+#pragma unroll
+        for (int c = 8; c < NC; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
+#pragma unroll
+        for (int w = 4; w; w >>= 1)
+#pragma unroll
+          for (int c = 0; c < w; ++c) mx[c] = fmaxf(mx[c], mx[c + w]);
+        const float bm = mx[0];
+        // lazy max update: move the reference max only when it grows by > 2^8
+        const bool grow = bm > m + kRescaleThreshold / p.scale_log2 || (m == -INFINITY && bm > -INFINITY);
+        if (__any_sync(0xffffffffu, grow) && it > 0) {
+          // O holds blocks < it: wait for PV(it-1), then scale the rows that grow
+          mbar_wait(&pv_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
+          tc_fence_after();
+          const float f = grow ? fast_exp2((m - bm) * p.scale_log2) : 1.f;  // m = -inf -> 0
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 16) {
+            float ov[16];
+            tmem_ld16(tO + lane_off + c, ov);
+#pragma unroll
+            for (int x = 0; x < 16; ++x) ov[x] *= f;
+            tmem_st16(tO + lane_off + c, ov);
+          }
+          tmem_st_wait();
+        }
+        if (grow) {
+          l *= fast_exp2((m - bm) * p.scale_log2);
+          m = bm;
+        }
+        const float mb = (m == -INFINITY) ? 0.f : m * p.scale_log2;  // all scores -inf when m is
+        float bs[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
+        uint32_t packed[NC / 2];
+#pragma unroll
+        for (int c = 0; c < NC; c += 2) {
+          const float p0 = fast_exp2(fmaf(sv[c], p.scale_log2, -mb));
+          const float p1 = fast_exp2(fmaf(sv[c + 1], p.scale_log2, -mb));
+          bs[(c >> 1) & 3] += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
+        if (threadIdx.x == 128) probe(p, 7, it);
+        // P buffer it&1 is free once PV(it-2) completed
+        if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
+        if (threadIdx.x == 128) probe(p, 8, it);
+        // P row (64 keys, SW128): this lane's columns; dup: zeros in the other half
+        uint8_t* prow = sP + (it & 1) * S::kP + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 16-byte chunk c holds columns [8c, 8c + 8)
+          const int k = c & (NC / 8 - 1);
+          const bool mine = NC == 64 || (c >> 2) == (r >> 6);
+          const uint4 v = mine ? make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3])
+                               : make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        // a fast warp must not arrive for block it while block it-1's phase is still
+        // collecting arrivals (its arrival would complete that phase early)
+        mbar_arrive(&p_full[it & 1]);  // the P-buffer wait above ordered it after block it-2's phase
+        if (threadIdx.x == 128) probe(p, 1, it);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      // a fast warp must not arrive for block it while block it-1's phase is still
-      // collecting arrivals (its arrival would complete that phase early)
-      mbar_arrive(&p_full[it & 1]);  // the P-buffer wait above ordered it after block it-2's phase
-      if (threadIdx.x == 128) probe(p, 1, it);
-    }
+    };
+    if (dup) blocks(std::integral_constant<int, 32>{});
+    else blocks(std::integral_constant<int, BKV>{});
     if (nb > 0) {
       mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
       tc_fence_after();
       if (p.splits == 1) {
+        // dup: lane r + 64 holds query r's other half-keys partial; it parks (O, m, l) in the
+        // idle K/V stages and lane r merges (tcgen05.ld is warp-collective: lane conditions
+        // guard only the memory operations)
+        float w0 = 1.f, w1 = 0.f;
+        float* xo = reinterpret_cast<float*>(sKV);
+        float2* xml = reinterpret_cast<float2*>(sKV + 64 * (HD + 4) * 4);
+        if (dup) {
+          if (r >= 64) {
+#pragma unroll 1
+            for (int c = 0; c < HD; c += 16) {
+              float ov[16];
+              tmem_ld16(tO + lane_off + c, ov);
+#pragma unroll
+              for (int x = 0; x < 16; x += 4)
+                *reinterpret_cast<float4*>(xo + qi * (HD + 4) + c + x) = make_float4(ov[x], ov[x + 1], ov[x + 2], ov[x + 3]);
+            }
+            xml[qi] = make_float2(m, l);
+          }
+          named_bar(1, 128);
+          if (r < 64) {
+            const float2 o = xml[qi];
+            const float M = l > 0.f && o.y > 0.f ? fmaxf(m, o.x) : (l > 0.f ? m : o.x);
+            w0 = l > 0.f ? fast_exp2((m - M) * p.scale_log2) : 0.f;
+            w1 = o.y > 0.f ? fast_exp2((o.x - M) * p.scale_log2) : 0.f;
+            l = w0 * l + w1 * o.y;
+          }
+        }
         const float inv = 1.f / l;
         __nv_bfloat16* dst = p.out + (qrow0 + qi) * p.d + h * HD;
+        if (!dup || r < 64) {
 #pragma unroll 1
-        for (int c = 0; c < HD; c += 16) {
-          float ov[16];
-          tmem_ld16(tO + lane_off + c, ov);
-          if (qi < n_) {
-            uint4 w[2];
-            __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w);
+          for (int c = 0; c < HD; c += 16) {
+            float ov[16];
+            tmem_ld16(tO + lane_off + c, ov);
+            if (qi < n_) {
+              if (dup) {
 #pragma unroll
-            for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
-            *reinterpret_cast<uint4*>(dst + c) = w[0];
-            *reinterpret_cast<uint4*>(dst + c + 8) = w[1];
+                for (int y = 0; y < 16; ++y) ov[y] = w0 * ov[y] + w1 * xo[qi * (HD + 4) + c + y];
+              }
+              uint4 w[2];
+              __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w);
+#pragma unroll
+              for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
+              *reinterpret_cast<uint4*>(dst + c) = w[0];
+              *reinterpret_cast<uint4*>(dst + c + 8) = w[1];
+            }
           }
         }
       } else {
@@ -628,7 +681,9 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   p.counters = a.counters;
   if (splits > 8) splits = 8;
   p.splits = splits;
-  CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), BQ);
+  CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), 64);  // 64-row boxes
+  static const bool nodup = std::getenv("PCB_ATTN_NODUP") != nullptr;  // A/B switch
+  p.dup = batched && a.max_n <= 64 && splits == 1 && !nodup ? 1 : 0;
   static const bool hm_probe = std::getenv("PCB_ATTN_HM_PROBE") != nullptr;  // timing probe (values meaningless)
   p.kv_head_major = hm_probe ? 1 : 0;
   p.kv_rows = p.total;
