@@ -19,7 +19,7 @@ import paper_2311_04934_b200 as pcb  # noqa: E402
 L = pcb.lib()
 L.pcb_debug_chain_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_void_p]
 MAXL = 256
-times = np.zeros((MAXL, 8, 160, 12), np.uint64)
+times = np.zeros((MAXL, 8, 160, 16), np.uint64)
 phases = np.zeros(MAXL, np.int32)
 
 
@@ -112,6 +112,12 @@ for i in range(n):
                 row["s1_loop"] = np.median((ev[:, 9] - ev[:, 4])[ok9]) / 1e3
                 row["s1_copy"] = np.median((ev[:, 10] - ev[:, 9])[ok9]) / 1e3
                 row["s1_tail"] = np.median((ev[:, 5] - ev[:, 10])[ok9]) / 1e3
+                okc = ok9 & (ev[:, 15] > 0)
+                if okc.any():  # first two chunks: TMEM load / values + smem staging
+                    row["c0_ld"] = np.median((ev[:, 12] - ev[:, 4])[okc]) / 1e3
+                    row["c0_val"] = np.median((ev[:, 13] - ev[:, 12])[okc]) / 1e3
+                    row["c1_ld"] = np.median((ev[:, 14] - ev[:, 13])[okc]) / 1e3
+                    row["c1_val"] = np.median((ev[:, 15] - ev[:, 14])[okc]) / 1e3
             ok5 = (ev[:, 5] > 0) & (ev[:, 4] > 0)
             if ok5.any():
                 row["flagwait"] = np.median((ev[:, 5] - ev[:, 4])[ok5]) / 1e3
