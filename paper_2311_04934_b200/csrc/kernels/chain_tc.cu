@@ -106,6 +106,7 @@ struct ChainParams {
   unsigned long long* tl;    // timeline probe [phase][cta][4] (null: off)
   int pf_dist;               // weight tiles prefetched into L2 ahead of the ring (0: off)
   int warm;                  // dry epilogue pass while the weights stream (instruction cache)
+  int dsm;                   // launched in clusters of 4: split partials / attention splits meet in DSMEM
 };
 
 static_assert(sizeof(ChainParams) <= 32764, "chain kernel parameters exceed the 32 KB parameter space");
@@ -124,7 +125,14 @@ __device__ __forceinline__ void ctl(const ChainParams& p, int ph, int ev) {
 template <int BN, int STAGES>
 struct ChainSmem {
   static constexpr int kStage = kWTileC + BN * 128;
-  static constexpr int kBytes = STAGES * kStage + 1024 + 1024 + 1024 + 2 * 16 * 128 * 4;  // + LN-fold scratch
+  // cluster exchange buffer (BN <= 64, dsm launches): a split GEMM phase parks its fp32
+  // partial (float4 [BN / 4][128]) here, the attention phase its normalised O [64][132] +
+  // (m, l)[64];
+  // the S CTAs of a tile / head read each other's through DSMEM
+  static constexpr int kPbLd = 132;  // floats per parked row (pad 4: conflict-free v4 rows)
+  static constexpr int kPbAttn = 64 * kPbLd * 4 + 64 * 8, kPbGemm = 128 * BN * 4;
+  static constexpr int kPB = BN <= 64 ? (kPbAttn > kPbGemm ? kPbAttn : kPbGemm) : 0;
+  static constexpr int kBytes = STAGES * kStage + kPB + 1024 + 1024 + 1024 + 2 * 16 * 128 * 4;  // + LN-fold scratch
   static constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;
   // attention phase layout of the ring: Q (32 KB), two P buffers (32 KB), K/V stages of 32 KB
   static constexpr int kAttnFit = (STAGES * kStage - 65536) / 32768;
@@ -230,13 +238,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   using S = ChainSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  float* pb = reinterpret_cast<float*>(smem + STAGES * S::kStage);  // cluster exchange buffer (S::kPB bytes)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage + S::kPB);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   double* red = reinterpret_cast<double*>(acc_empty + 4);  // [4] LayerNorm partial sums
-  float2* lnst = reinterpret_cast<float2*>(smem + STAGES * S::kStage + 1024);  // [128] {mean, rstd}
+  float2* lnst = reinterpret_cast<float2*>(smem + STAGES * S::kStage + S::kPB + 1024);  // [128] {mean, rstd}
   float* colsum = reinterpret_cast<float*>(lnst + 128);  // [2][16 tokens][128 columns] h, h^2 of a chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -256,6 +265,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   uint64_t* a_pfull = a_sfull + 2;     // [2] (two: see attn_tc.cu, one p_full can deadlock)
   uint64_t* a_pvdone = a_pfull + 2;    // [2]
   uint64_t* a_done = a_pvdone + 2;     // this CTA's attention is off the ring (128 arrivals)
+  // exchange-buffer barriers (dsm): pb_ready completes when every CTA of this CTA's group
+  // has parked its data (each group member arrives once with count 4 / S, S = group size),
+  // pb_free when they have all finished reading this CTA's buffer
+  uint64_t* pb_ready = full + 100;
+  uint64_t* pb_free = full + 101;
+  const bool dsm = S::kPB > 0 && p.dsm;
   // a QKV phase with a per-request RoPE table stages each tile's {cos, sin} operands in TMEM
   // columns [256, 384) and [384, 512) while its weights stream (idle there: attention is
   // phase 0 only; GEMM accumulators use [0, 2 BN) with BN <= 128)
@@ -288,6 +303,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
       mbar_init(&a_pfull[1], 128);
       mbar_init(a_done, 128);
     }
+    if (dsm) {
+      mbar_init(pb_ready, 4);
+      mbar_init(pb_free, 4);
+    }
     fence_barrier_init();
   }
   if (warp == 2 && lane == 0)
@@ -296,6 +315,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   if (warp == 1) tmem_alloc(tmem_slot, tcols);
   tc_fence_before();
   __syncthreads();
+  if (dsm) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t aS0 = tmem + 256, aO = tmem + 384;  // attention: two score buffers, O
@@ -523,6 +543,21 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     float v[16];
     int seg = 0;
+    uint32_t pb_uses = 0;  // dsm: completed uses of this CTA's exchange buffer
+    // dsm helpers: the S CTAs [g0, g0 + S) of a group sit in one cluster of 4 (C % 4 == 0,
+    // S in {1, 2, 4}, groups aligned), so a member's cluster rank is its index & 3
+    // One remote arrive per (CTA, member): bar.sync orders the 128 epilogue threads' buffer
+    // writes / reads before thread u's cluster-scope release (128 remote arrivals per barrier,
+    // one per thread, serialised on the barrier word: +2 us per exchange).  The wait is one
+    // acquiring thread followed by bar.sync.
+    auto pb_signal = [&](uint64_t* bar, int g0, int S_) {
+      named_bar(1, 128);
+      if (et < S_) mbar_arrive_cluster(mapa_shared(smem_u32(bar), (g0 + et) & 3), 4 / S_);
+    };
+    auto pb_wait = [&](uint64_t* bar, uint32_t parity) {
+      if (et == 0) mbar_wait_cluster(bar, parity);
+      named_bar(1, 128);
+    };
     for (int ph = 0; ph < p.n_phases; ++ph) {
       const PhaseDev& P = p.ph[ph];
       if (ph == 0) {
@@ -668,6 +703,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         // (the K/V stages are idle once the last PV completed); a single split writes O
         const int nparts = P.aS;
         const bool out_lane = dup ? row < 64 : true;  // lanes that own a query's result
+        // dsm (n <= 64): the split partials meet in the cluster's exchange buffers -- one
+        // DSMEM round trip instead of global partials + release flags + L2 polls (~7 us of
+        // the phase tail under a saturated memory system)
+        const bool adsm = dsm && dup && nparts > 1 && c < P.items;
+        float2* pbml = reinterpret_cast<float2*>(pb + 64 * S::kPbLd);
         float* part = P.apart + (static_cast<int64_t>(c) * 128 + qi) * 128;
         float2* ml = reinterpret_cast<float2*>(P.apart + static_cast<int64_t>(P.items) * 128 * 128);
         if (nb > 0) {
@@ -721,6 +761,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
                 *reinterpret_cast<uint4*>(dst + x) = w2[0];
                 *reinterpret_cast<uint4*>(dst + x + 8) = w2[1];
+              } else if (adsm) {  // park O / l (fp32) in this CTA's exchange buffer
+                const float il = l > 0.f ? 1.f / l : 0.f;
+                float* pr = pb + qi * S::kPbLd + x;
+#pragma unroll
+                for (int y = 0; y < 16; y += 4)
+                  *reinterpret_cast<float4*>(pr + y) = make_float4(ov[y] * il, ov[y + 1] * il, ov[y + 2] * il, ov[y + 3] * il);
               } else {  // park the normalised O row in fp16 (O / l: |values| <= max |V|) for the merge
                 const float il = l > 0.f ? 1.f / l : 0.f;
                 uint32_t hw[8];
@@ -734,7 +780,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 __stcg(reinterpret_cast<uint4*>(ph + 8), make_uint4(hw[4], hw[5], hw[6], hw[7]));
               }
             }
-            if (nparts > 1 && qi < n_) __stcg(ml + static_cast<int64_t>(c) * 128 + qi, make_float2(m, l));
+            if (nparts > 1 && qi < n_) {
+              if (adsm) pbml[qi] = make_float2(m, l);
+              else __stcg(ml + static_cast<int64_t>(c) * 128 + qi, make_float2(m, l));
+            }
           }
         }
         tc_fence_before();
@@ -744,7 +793,56 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         // flag became visible ~2 us later (tools/chain_ab.py, per-CTA attention events)
         const bool merge = c < P.items && nparts > 1;
         if (!merge) mbar_arrive(a_done);
-        if (merge) {
+        if (adsm) {
+          // every epilogue thread releases its parked rows to the head's S CTAs, then the CTA
+          // merges queries {sp, sp + S, ...} reading all S buffers (split order: deterministic)
+          const int base = h * P.aS;
+          pb_signal(pb_ready, base, nparts);
+          mbar_arrive(a_done);
+          if (et == 0) ctl(p, ph, 8);
+          pb_wait(pb_ready, pb_uses & 1);
+          if (et == 0) ctl(p, ph, 5);
+          const int x0 = (et & 7) * 4;  // dims x0 + 32 y + [0, 4): 8 threads read 128 contiguous bytes
+          for (int64_t r2 = sp + static_cast<int64_t>(et >> 3) * P.aS; r2 < n_; r2 += 16 * P.aS) {
+            // every remote load issued before the first use (member indices past S re-read
+            // member 0 and get weight 0)
+            float ms[4], ls[4], f[4][16];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rk = (base + (u < nparts ? u : 0)) & 3;
+              const uint32_t a = mapa_shared(smem_u32(pbml + r2), rk);
+              asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(ms[u]), "=f"(ls[u]) : "r"(a) : "memory");
+              const uint32_t b = mapa_shared(smem_u32(pb + r2 * S::kPbLd + x0), rk);
+#pragma unroll
+              for (int y = 0; y < 4; ++y) ld_dsmem_v4(b + 128 * y, f[u] + 4 * y);
+            }
+            float M = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u < nparts && ls[u] > 0.f) M = fmaxf(M, ms[u]);
+            float den = 0.f, acc[16];
+#pragma unroll
+            for (int x = 0; x < 16; ++x) acc[x] = 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float wl = (u < nparts && ls[u] > 0.f) ? fast_exp2((ms[u] - M) * P.ascale) * ls[u] : 0.f;
+              den += wl;
+#pragma unroll
+              for (int x = 0; x < 16; ++x) acc[x] = fmaf(wl, f[u][x], acc[x]);
+            }
+            const float inv = 1.f / den;
+            __nv_bfloat16* dst = P.aout + r2 * P.a_d + h * 128 + x0;
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              const __nv_bfloat162 lo = __floats2bfloat162_rn(acc[4 * y] * inv, acc[4 * y + 1] * inv);
+              const __nv_bfloat162 hi = __floats2bfloat162_rn(acc[4 * y + 2] * inv, acc[4 * y + 3] * inv);
+              *reinterpret_cast<uint2*>(dst + 32 * y) =
+                  make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+            }
+          }
+          pb_signal(pb_free, base, nparts);
+          ++pb_uses;
+        } else if (merge) {
           // the S split CTAs of head h each merge queries {sp, sp + S, ...} of all S partials
           // in split order (deterministic):
           //   O = sum_s w_s O_s / sum_s w_s l_s,  w_s = 2^((m_s - M) scale),  M = max_s m_s
@@ -850,7 +948,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         // column sums of the new residual of one 16-token chunk -> stats_out[tile][m]
         // (transposed through smem: each thread parks its 16 values, then 8 threads per
         // token sum 16 columns each and combine with 3 shuffles)
-        auto stats_chunk = [&](int tile, int64_t m0, int64_t lim) {
+        auto stats_chunk = [&](int tile, int64_t m0, int64_t lim, bool nost = false) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             colsum[j * 128 + row] = v[j];
@@ -869,7 +967,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             a += __shfl_xor_sync(0xffffffffu, a, o);
             b += __shfl_xor_sync(0xffffffffu, b, o);
           }
-          if ((et & 7) == 0 && m0 + j < lim)
+          if ((et & 7) == 0 && m0 + j < lim && !nost)
             reinterpret_cast<float2*>(P.stats_out)[static_cast<int64_t>(tile) * P.stats_ld + m0 + j] = make_float2(a, b);
           named_bar(1, 128);
         };
@@ -1073,6 +1171,83 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             if (et == 0) ctl(p, ph, 5);
             continue;
           }
+          if (dsm) {
+            // split tile, cluster path: park the fp32 partial in this CTA's exchange buffer,
+            // release it to the tile's S CTAs (one cluster), then finish a 1/S slice of the
+            // token columns reading all S buffers through DSMEM (split order: deterministic).
+            // Pass 0 is a dry run while the weights stream (no waits, arrivals or stores): it
+            // only warms the instruction cache, as for the S = 1 epilogue.
+            // partial layout float4 [BN / 4][128 rows]: a warp's v4 access to one 4-token group
+            // of 32 rows is 512 contiguous bytes (DSMEM reads coalesce into whole lines; a
+            // row-per-thread layout made every 16-byte read its own remote transaction)
+            const int g0 = tile * P.S;
+            float4* pb4 = reinterpret_cast<float4*>(pb);
+            const int Mr = (Mc + 3) & ~3;
+            const int sw = ((Mr + P.S - 1) / P.S + 3) & ~3;
+            const int s0 = j * sw, s1 = min(Mr, s0 + sw);
+            const int64_t lim = min(static_cast<int64_t>(s1), M);
+            // (only where the item streams long enough to hide it: Wo's 256 KB items are done
+            // before a cold dry pass is, which then delayed the real one by ~5 us)
+#pragma unroll 1
+            for (int pass = (p.warm && P.kbs / P.S >= 32) ? 0 : 1; pass < 2; ++pass) {
+              const bool dry = pass == 0;
+              if (!dry) {
+                mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+                tc_fence_after();
+                if (et == 0) ctl(p, ph, 4);
+                if (pb_uses > 0) pb_wait(pb_free, (pb_uses - 1) & 1);  // peers done with the last use
+              }
+#pragma unroll 1
+              for (int cc = 0; cc < Mc; cc += 16) {
+                tmem_ld16(acc + cc, v);
+                if (!dry)
+#pragma unroll
+                  for (int x = 0; x < 16; x += 4) pb4[((cc + x) >> 2) * 128 + row] = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
+              }
+              if (!dry) {
+                tc_fence_before();
+                mbar_arrive(&acc_empty[buf]);
+                pb_signal(pb_ready, g0, P.S);
+              }
+              if (s0 < lim) epi_prefetch(e, n, P.N, s0, lim, cur);
+              if (!dry) {
+                pb_wait(pb_ready, pb_uses & 1);
+                if (et == 0) ctl(p, ph, 5);
+              }
+#pragma unroll 1
+              for (int m0 = s0; m0 < lim; m0 += 16) {
+                // all 16 DSMEM loads in flight at once (a member index past S re-reads
+                // member 0 and is not summed): a data-dependent loop bound serialised one
+                // remote round trip per member
+                float f[4][16];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const uint32_t a = mapa_shared(smem_u32(pb4 + (m0 >> 2) * 128 + row), (g0 + (u < P.S ? u : 0)) & 3);
+#pragma unroll
+                  for (int y = 0; y < 4; ++y) ld_dsmem_v4(a + y * 128 * 16, f[u] + 4 * y);
+                }
+#pragma unroll
+                for (int x = 0; x < 16; ++x) v[x] = f[0][x];
+#pragma unroll
+                for (int u = 1; u < 4; ++u)
+                  if (u < P.S)
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) v[x] += f[u][x];
+                if (et == 0 && m0 == s0 && !dry) ctl(p, ph, 9);
+                if (m0 + 16 < lim) epi_prefetch(e, n, P.N, m0 + 16, lim, nxt);
+                epi_chunk(e, n, P.N, m0, lim, v, cur, ln, dry);
+                if (et == 0 && m0 == s0 && !dry) ctl(p, ph, 10);
+                if (P.stats_out) stats_chunk(tile, m0, lim, dry);
+                if (et == 0 && m0 == s0 && !dry) ctl(p, ph, 11);
+                cur = nxt;
+              }
+              if (!dry) {
+                pb_signal(pb_free, g0, P.S);
+                ++pb_uses;
+              }
+            }
+            continue;
+          }
           mbar_wait(&acc_full[buf], (seg >> 1) & 1);
           tc_fence_after();
           if (et == 0) ctl(p, ph, 4);
@@ -1166,6 +1341,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
+  if (dsm) cluster_sync_all();  // no CTA leaves while a peer may still read its buffer
   if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
@@ -1211,7 +1387,35 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   ChainParams p;
   std::memset(&p, 0, sizeof(p));
   p.n_phases = n;
-  const int C = sms;
+  // Cluster launch (BN <= 64): 4-CTA clusters so the S CTAs of a split tile / attention head
+  // exchange partials through DSMEM.  Clusters of 4 with this kernel's footprint fit fewer
+  // than all SMs (132 of 148 on B200); every phase of the layer chain has <= 128 work items,
+  // so the grid is the co-resident cluster count x 4 (the grid barrier needs co-residency).
+  static const int dsm_grid = [&] {
+    const char* v = std::getenv("PCB_CHAIN_DSM");
+    if (Sm::kPB == 0 || (v && v[0] == '0')) return 0;
+    PCB_CUDA(cudaFuncSetAttribute(k_chain<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((sms / 4) * 4);
+    cfg.blockDim = dim3(kChainThreads);
+    cfg.dynamicSmemBytes = Sm::kBytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k_chain<BN, STAGES>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return std::min(nc, sms / 4) * 4;
+  }();
+  const bool dsm = dsm_grid >= 128;
+  const int C = dsm ? dsm_grid : sms;
+  p.dsm = dsm ? 1 : 0;
   for (int i = 0; i < n; ++i) {
     const ChainStep& st = steps[i];
     PhaseDev& d = p.ph[i];
@@ -1223,7 +1427,7 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.kbs = st.K / 64;
       d.units = static_cast<int64_t>(st.N / 128) * d.kbs;
       const int tiles = st.N / 128;
-      d.S = 2 * tiles > C ? 1 : std::min({4, C / tiles, d.kbs});
+      d.S = 2 * tiles > C ? 1 : std::min({4, C / tiles, d.kbs});  // dsm: a tile's splits share a cluster
       if (d.S == 3) d.S = 2;  // slices of 1/S of the columns: S in {1, 2, 4}
       d.items = tiles * d.S;
       d.w = static_cast<const uint8_t*>(st.w);
@@ -1249,7 +1453,8 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
         nblk = 0;
         for (int sgi = 0; sgi < st.a_nseg; ++sgi) nblk += (st.a_seg[sgi].rows + 63) / 64;
       }
-      d.aS = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({C / st.aH, nblk, 8})));  // <= 16 partials
+      d.aS = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({C / st.aH, nblk, dsm ? 4 : 8})));
+      if (dsm && d.aS == 3) d.aS = 2;  // a head's splits share one cluster of 4
       d.items = st.aH * d.aS;
       d.ascale = 1.4426950408889634f / sqrtf(128.f);
       d.apart = st.a_scratch;
@@ -1291,6 +1496,7 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   }
   p.ws = ws;
   p.ws_half = static_cast<int64_t>(C) * 128 * BN;
+  if (C > 160) throw std::runtime_error("chain: grid exceeds the timeline probe layout");
   if (static_cast<size_t>(2 * p.ws_half) * sizeof(float) > ws_bytes) throw std::runtime_error("chain workspace too small");
   p.flags = flags;
   p.epoch0 = g_chain_epoch.fetch_add(n) + 1;
@@ -1331,7 +1537,23 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   o.last = s;
   PdlClass pc(PDL_GEMM);
   static const bool coop = std::getenv("PCB_CHAIN_COOP") != nullptr;  // A/B: cooperative launch attribute
-  if (coop) {
+  if (dsm) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kChainThreads);
+    cfg.dynamicSmemBytes = Sm::kBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = (pdl_enabled() && ((pdl_mask() >> PDL_GEMM) & 1)) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_chain<BN, STAGES>, p));
+  } else if (coop) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kChainThreads);
@@ -1398,9 +1620,11 @@ void chain_tc(const ChainStep* steps, int n_steps, float* ws, size_t ws_bytes, i
       throw std::runtime_error("chain: unsupported attention phase");
     M = std::max<int64_t>(M, st.M);
   }
-  if (M <= 16) launch_chain<16, 10>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
-  else if (M <= 32) launch_chain<32, 10>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
-  else if (M <= 64) launch_chain<64, 8>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  // ring depth: what is left of 227 KB after the cluster exchange buffer (BN <= 64) and the
+  // barrier / LayerNorm scratch
+  if (M <= 16) launch_chain<16, 9>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else if (M <= 32) launch_chain<32, 8>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
+  else if (M <= 64) launch_chain<64, 7>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
   else launch_chain<128, 6>(steps, n_steps, ws, ws_bytes, flags, gbar, gbar_count, s, sms);
 }
 

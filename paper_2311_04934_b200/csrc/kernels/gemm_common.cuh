@@ -78,8 +78,9 @@ __device__ __forceinline__ float gelu_bf16path(float x) {
 // The epilogue warps are one per scheduler, so the per-element cost is latency, not
 // throughput: fields are read once into registers, full chunks take an unguarded,
 // fully unrolled path, and only a ragged last chunk is guarded.
+// nost: compute everything but store nothing (the chain's instruction-cache warm-up pass)
 __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int64_t m0, int64_t M, float* v,
-                                          const EpiPre& pre, const float2* lnst = nullptr) {
+                                          const EpiPre& pre, const float2* lnst = nullptr, bool nost = false) {
   const int kind = ep.kind;
   const int jn = M - m0 >= 16 ? 16 : static_cast<int>(M - m0);
   if (lnst) {  // folded LayerNorm: {mean, rstd} of token m0 + j
@@ -90,6 +91,7 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int6
       v[j] = st.y * fmaf(-st.x, ws, v[j]);
     }
   }
+  if (kind != EPI_RESID && nost) return;  // the warm-up pass only runs residual (split) phases
   if (kind == EPI_QKV) {
     const int d = ep.d;
     const int seg = n / d, c = n - seg * d;
@@ -129,14 +131,17 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& ep, int n, int N, int6
       for (int j = 0; j < 16; ++j) {
         v[j] = pre.a[j] + v[j];
         if (j < jn) {
-          dst[j * N] = v[j];
-          xo[j * N] = __float2bfloat16_rn(v[j]);
+          if (!nost) {
+            dst[j * N] = v[j];
+            xo[j * N] = __float2bfloat16_rn(v[j]);
+          }
         } else {
           v[j] = 0.f;
         }
       }
       return;
     }
+    if (nost) return;
     if (jn == 16) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) dst[j * N] = pre.a[j] + v[j];

@@ -87,7 +87,8 @@ for i in range(n):
     names = ["LN1", "QKV"] if npn == 2 else (["ATTN", "O", "W1", "W2", "QKV"] if npn == 5 else (names6 + ["?"] * 8)[:npn])
     for ph in range(npn):
         ev = t[ph]
-        done = ev[:, 2]
+        act = ev[:, 2] > 0  # CTAs of the grid (a cluster launch uses fewer than 148)
+        done = ev[act, 2]
         start_x = ev[:, 0]
         row = {}
         if ph > 0:
@@ -98,7 +99,7 @@ for i in range(n):
             mma_end = ev[:, 1]
             ok = (start_x > 0) & (mma_end > 0)
             row["stream"] = np.median((mma_end - start_x)[ok]) / 1e3
-            row["epi_tail"] = np.median((done - mma_end)[ok]) / 1e3
+            row["epi_tail"] = np.median((ev[:, 2] - mma_end)[ok]) / 1e3
             row["w_lead"] = np.median((start_x - ev[:, 3])[ok]) / 1e3  # >0: weights issued before barrier passed
         if (start_x > 0).any():
             okk = (ev[:, 6] > 0) & (ev[:, 7] > 0)
@@ -128,7 +129,8 @@ for i in range(n):
                     row["o_epi"] = np.median((ev[:, 10] - ev[:, 9])[ok8]) / 1e3
                     row["o_stats"] = np.median((ev[:, 11] - ev[:, 10])[ok8]) / 1e3
                     row["o_after"] = np.median((ev[:, 2] - ev[:, 11])[ok8]) / 1e3
-        row["phase_span"] = (done.max() - (t[ph - 1][:, 2].max() if ph > 0 else t[0][:, 2].min())) / 1e3
+        first_done = t[0][:, 2]
+        row["phase_span"] = (done.max() - (t[ph - 1][:, 2].max() if ph > 0 else first_done[first_done > 0].min())) / 1e3
         agg.setdefault((npn, names[ph]), []).append(row)
     first = t[0][:, 0]
     first = first[first > 0]
