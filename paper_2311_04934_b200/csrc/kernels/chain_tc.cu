@@ -171,6 +171,11 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// probe slot holding a raw value (cycle counts) instead of a timestamp
+__device__ __forceinline__ void ctl_val(const ChainParams& p, int ph, int ev, unsigned long long v) {
+  if (p.tl) p.tl[(static_cast<size_t>(ph) * 160 + blockIdx.x) * 16 + ev] = v;
+}
+
 // wait until every CTA has finished phases [0, ph)
 __device__ __forceinline__ void grid_wait(const ChainParams& p, int ph) {
   const unsigned long long target = p.gbar_base + static_cast<unsigned long long>(ph) * gridDim.x;
@@ -480,9 +485,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
         const uint32_t q_addr = smem_u32(aQ), p_addr = smem_u32(aPb);
         mbar_wait(a_qfull, 0);
+        long long kv_wait = 0, p_wait = 0;
         auto issue_qk = [&](int it) {
           const int s = it % AKV;
+          const long long t0 = p.tl ? clock64() : 0;
           mbar_wait(&a_kvfull[s], (it / AKV) & 1);
+          if (p.tl) kv_wait += clock64() - t0;
           tc_fence_after();
           const uint32_t k_addr = smem_u32(aKV + s * 32768);
 #pragma unroll
@@ -494,7 +502,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         issue_qk(0);
         for (int it = 0; it < nb; ++it) {
           if (it + 1 < nb) issue_qk(it + 1);
+          const long long t1 = p.tl ? clock64() : 0;
           mbar_wait(&a_pfull[it & 1], (it >> 1) & 1);
+          if (p.tl) p_wait += clock64() - t1;
           tc_fence_after();
           const uint32_t v_addr = smem_u32(aKV + (it % AKV) * 32768 + 16384);
           const uint32_t pb = p_addr + (it & 1) * 16384;
@@ -506,6 +516,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           umma_commit(&a_kvempty[it % AKV]);
         }
         ctl(p, 0, 1);
+        ctl_val(p, 0, 14, kv_wait);  // MMA thread: cycles waiting for K/V blocks, for P
+        ctl_val(p, 0, 15, p_wait);
       }
       constexpr uint32_t idesc = idesc_bf16(128, BN);
       int it = 0, seg = 0;
@@ -589,29 +601,49 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         const bool alibi = P.a_alibi != nullptr;
         const int32_t qpos = alibi && c < P.items && qi < n_ ? P.a_qpos[qi] : 0;
         const float slope_raw = alibi && c < P.items ? P.a_alibi[h] * 11.313708498984761f : 0.f;
+        long long sfull_wait = 0;
+        const long long tsm0 = p.tl ? clock64() : 0;
         auto blocks = [&](auto ncols) {
           constexpr int NC = decltype(ncols)::value;  // score columns per lane: 64, or 32 (dup)
-          const int c0 = NC == 32 ? (row >> 6) * 32 : 0;
-          for (int it = 0, sg = 0; it < nb; ++it) {
-            // lim: last visible key of this block, relative to the block's first key.
+          const int hi = NC == 32 ? (row >> 6) : 0;     // dup: which half of each block's keys
+          const int c0 = hi * 32;
+          const float ascale = P.ascale, thr = kRescaleThreshold / ascale;
+          // dup: this lane's P row is zero in the other half's 16-byte chunks for every block;
+          // those zeros are written once per P buffer here instead of every block
+          if (NC == 32 && live)
+#pragma unroll
+            for (int pb_ = 0; pb_ < 2; ++pb_)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                *reinterpret_cast<uint4*>(aPb + pb_ * 16384 + row * 128 + (((4 * (1 - hi) + k) ^ (row & 7)) << 4)) =
+                    make_uint4(0u, 0u, 0u, 0u);
+          // key-block visibility in 32-bit arithmetic (positions < 2^31, checked on the host):
+          // lim = last visible key of the block relative to this lane's first column
+          int sg = 0, seg_first = 0, seg_next = P.a_nseg ? P.a_first[1] : 0x7fffffff;
+          for (int it = 0; it < nb; ++it) {
             // contiguous: key j visible iff j <= P + qi; zero-copy: a prefix segment's rows
             // are all visible (its padding is not), the tail is visible up to tail_vis + qi
             const int b = b0 + it;
-            int64_t lim;
+            int lim;
             if (P.a_nseg) {
-              while (b >= P.a_first[sg + 1]) ++sg;
-              const int64_t local = static_cast<int64_t>(b - P.a_first[sg]) * 64;
-              lim = sg == P.a_nseg - 1 ? P.a_tail_vis + qi - local : P.a_rows[sg] - 1 - local;
+              while (b >= seg_next) {
+                ++sg;
+                seg_first = seg_next;
+                seg_next = P.a_first[sg + 1];
+              }
+              const int local = (b - seg_first) * 64;
+              lim = (sg == P.a_nseg - 1 ? P.a_tail_vis + qi : P.a_rows[sg] - 1) - local - c0;
             } else {
-              lim = P.aP + qi - static_cast<int64_t>(b) * 64;
+              lim = static_cast<int>(P.aP) + qi - b * 64 - c0;
             }
-            lim -= c0;  // relative to this lane's first column
             if (!live) {
               if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);
               mbar_arrive(&a_pfull[it & 1]);
               continue;
             }
+            const long long tw0 = p.tl ? clock64() : 0;
             mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
+            if (p.tl) sfull_wait += clock64() - tw0;
             tc_fence_after();
             float sv[NC];
             {
@@ -640,6 +672,24 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               for (int x = 0; x < NC; ++x)
                 if (x > lim) sv[x] = -INFINITY;
             }
+            // exponentials against the running max, computed alongside the block max (they do
+            // not wait for it); only when some lane's max grows past the lazy-rescale threshold
+            // (the first block, rarely later) are they recomputed against the new max
+            float bs[4];
+            uint32_t packed[NC / 2];
+            auto expo = [&](float mb) {
+#pragma unroll
+              for (int x = 0; x < 4; ++x) bs[x] = 0.f;
+#pragma unroll
+              for (int x = 0; x < NC; x += 2) {
+                const float p0 = fast_exp2(fmaf(sv[x], ascale, -mb));
+                const float p1 = fast_exp2(fmaf(sv[x + 1], ascale, -mb));
+                bs[(x >> 1) & 3] += p0 + p1;
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                packed[x >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+            };
+            expo(m == -INFINITY ? 0.f : m * ascale);
             float mx[8];
 #pragma unroll
             for (int x = 0; x < 8; ++x) mx[x] = sv[x];
@@ -650,48 +700,36 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 #pragma unroll
               for (int x = 0; x < w; ++x) mx[x] = fmaxf(mx[x], mx[x + w]);
             const float bm = mx[0];
-            const bool grow = bm > m + kRescaleThreshold / P.ascale || (m == -INFINITY && bm > -INFINITY);
-            if (__any_sync(0xffffffffu, grow) && it > 0) {
-              mbar_wait(&a_pvdone[(it - 1) & 1], ((it - 1) >> 1) & 1);
-              tc_fence_after();
-              const float f = grow ? fast_exp2((m - bm) * P.ascale) : 1.f;
+            const bool grow = bm > m + thr || (m == -INFINITY && bm > -INFINITY);
+            if (__any_sync(0xffffffffu, grow)) {
+              if (it > 0) {
+                mbar_wait(&a_pvdone[(it - 1) & 1], ((it - 1) >> 1) & 1);
+                tc_fence_after();
+                const float f = grow ? fast_exp2((m - bm) * ascale) : 1.f;
 #pragma unroll 1
-              for (int x = 0; x < 128; x += 16) {
-                float ov[16];
-                tmem_ld16(aO + lane_off + x, ov);
+                for (int x = 0; x < 128; x += 16) {
+                  float ov[16];
+                  tmem_ld16(aO + lane_off + x, ov);
 #pragma unroll
-                for (int y = 0; y < 16; ++y) ov[y] *= f;
-                tmem_st16(aO + lane_off + x, ov);
+                  for (int y = 0; y < 16; ++y) ov[y] *= f;
+                  tmem_st16(aO + lane_off + x, ov);
+                }
+                tmem_st_wait();
               }
-              tmem_st_wait();
-            }
-            if (grow) {
-              l *= fast_exp2((m - bm) * P.ascale);
-              m = bm;
-            }
-            const float mb = (m == -INFINITY) ? 0.f : m * P.ascale;
-            float bs[4] = {0.f, 0.f, 0.f, 0.f};
-            uint32_t packed[NC / 2];
-#pragma unroll
-            for (int x = 0; x < NC; x += 2) {
-              const float p0 = fast_exp2(fmaf(sv[x], P.ascale, -mb));
-              const float p1 = fast_exp2(fmaf(sv[x + 1], P.ascale, -mb));
-              bs[(x >> 1) & 3] += p0 + p1;
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-              packed[x >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+              if (grow) {
+                l *= fast_exp2((m - bm) * ascale);
+                m = bm;
+              }
+              expo(m == -INFINITY ? 0.f : m * ascale);
             }
             l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
             if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);  // P buffer free
-            // P row (64 keys, SW128): this lane's columns, zeros in the other half (dup)
+            // P row (64 keys, SW128): this lane's 16-byte chunks (dup: half of them)
             uint8_t* prow = aPb + (it & 1) * 16384 + row * 128;
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {  // 16-byte chunk x holds columns [8x, 8x + 8)
-              const int k = x & (NC / 8 - 1);
-              const bool mine = NC == 64 || (x >> 2) == (row >> 6);
-              const uint4 v4 = mine ? make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3])
-                                    : make_uint4(0u, 0u, 0u, 0u);
-              *reinterpret_cast<uint4*>(prow + ((x ^ (row & 7)) << 4)) = v4;
-            }
+            for (int k = 0; k < NC / 8; ++k)  // chunk x = 4 hi + k holds columns [8x, 8x + 8)
+              *reinterpret_cast<uint4*>(prow + (((4 * hi + k) ^ (row & 7)) << 4)) =
+                  make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc_fence_before();
             mbar_arrive(&a_pfull[it & 1]);  // ordered after block it-2's phase by the P-buffer wait
@@ -699,6 +737,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         };
         if (dup) blocks(std::integral_constant<int, 32>{});
         else blocks(std::integral_constant<int, 64>{});
+        if (et == 0) {  // softmax loop: total cycles, cycles waiting for S
+          ctl_val(p, ph, 12, p.tl ? clock64() - tsm0 : 0);
+          ctl_val(p, ph, 13, sfull_wait);
+        }
         // one partial per (query, split): the dup halves combine first through shared memory
         // (the K/V stages are idle once the last PV completed); a single split writes O
         const int nparts = P.aS;

@@ -137,6 +137,18 @@ for i in range(n):
     if prev_end is not None and len(first):
         agg.setdefault(("gap", "attention+launch"), []).append({"gap": (first.min() - prev_end) / 1e3})
     prev_end = t[npn - 1][:, 2].max()
+# attention-phase cycle accounting (raw clock64 counts in slots 12-15 of phase 0)
+cyc = []
+for i in range(n):
+    if int(phases[i]) == 5:
+        ev = times[i, 0, :148].astype(np.int64)
+        ok = ev[:, 12] > 0
+        if ok.any():
+            cyc.append([np.median(ev[ok, k]) for k in (12, 13, 14, 15)])
+if cyc:
+    c = np.median(np.array(cyc), axis=0)
+    print(f"ATTN cycles (median CTA, median chain): softmax loop {c[0]:.0f}, of which waiting for S {c[1]:.0f}; "
+          f"MMA waiting for K/V {c[2]:.0f}, for P {c[3]:.0f}")
 print("per phase (median over chains), us")
 for key, rows in agg.items():
     keys = sorted({k for r_ in rows for k in r_})
