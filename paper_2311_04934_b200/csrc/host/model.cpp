@@ -799,6 +799,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
   aa.alibi = alibi ? w_->alibi : nullptr;
   aa.kv_pos = alibi ? W.kvpos : nullptr;
   aa.counters = W.counters + 8192;  // [0, #SMs) are the GEMM's stream-K flags
+  aa.pair = attn_pair;
   const bool tc_attn = dtype_ == BF16 && !force_simt && !force_simt_attn && kern::attention_tc_supported(aa);
   int64_t nq = n;
   if (!tc_attn) {

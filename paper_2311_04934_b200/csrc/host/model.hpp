@@ -163,6 +163,7 @@ class Model {
   bool force_simt = false;       // testing: route bf16 GEMM/attention through SIMT kernels
   bool force_simt_gemm = false;  // testing: SIMT GEMM only
   bool force_simt_attn = false;  // testing: SIMT attention only
+  int attn_pair = 1;             // paired-tile prefill attention: 0 off, 1 when it fills the GPU, 2 always
   bool use_chain = true;         // few-token GEMM/LN segments as one persistent chain kernel (PCB_CHAIN=0: off)
   bool ln_fold = true;           // chain: LayerNorm folded into the neighbouring GEMMs (PCB_LN_FOLD=0: off)
   bool chain_attn = true;        // chain: a single request's attention as the chain's first phase (PCB_CHAIN_ATTN=0: off)

@@ -758,6 +758,20 @@ bool attention_tc_supported(const AttnArgs& a) {
 }
 
 void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s) {
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  static const bool pair_off = [] {  // A/B switch: the single-tile kernel for long prefills too
+    const char* v = std::getenv("PCB_ATTN_PAIR");
+    return v && v[0] == '0';
+  }();
+  if (!pair_off && attention_prefill_supported(a, sms)) {
+    attention_prefill(a, s);
+    return;
+  }
   if (a.alibi) {
     if (a.hd == 128) launch_attn<128, true>(a, scratch, scratch_bytes, s);
     else launch_attn<64, true>(a, scratch, scratch_bytes, s);

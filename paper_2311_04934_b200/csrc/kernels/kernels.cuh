@@ -208,6 +208,7 @@ struct AttnArgs {
   const void* maps = nullptr;
   int layer = 0;
   int64_t max_blocks = 0;  // longest request's key blocks (with per-segment padding)
+  int pair = 1;  // paired-tile prefill kernel: 0 off, 1 when pairs x heads fill the SMs, 2 whenever it applies
 };
 constexpr int kAttnMaxSeg = 16;
 // 3-D bf16 TMA map {cols, rows, planes} (plane stride in bytes), box {64, box_rows, 1}, SW128
@@ -217,6 +218,9 @@ void attention_simt(int dtype, const AttnArgs& a, float* scratch, cudaStream_t s
 size_t attention_simt_scratch(const AttnArgs& a);
 bool attention_tc_supported(const AttnArgs& a);
 void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s);
+// causal prefill over long query ranges (hd 128): two 128-query tiles per CTA (attn_prefill.cu)
+bool attention_prefill_supported(const AttnArgs& a, int sms);
+void attention_prefill(const AttnArgs& a, cudaStream_t s);
 int attn_tl_dump(unsigned long long* out, int max_ctas);  // debug: last launch's per-CTA phases (PCB_ATTN_TL)
 
 // ---- KV assembly: batched contiguous copies (one descriptor per segment) ----

@@ -37,6 +37,29 @@ def test_tc_path_vs_simt_7b_shape(m7):
         assert all(same_greedy_token(a, b) for a, b in zip(x2, y2))
 
 
+@pytest.mark.parametrize("n,P", [(129, 0), (256, 0), (300, 0), (640, 0), (1000, 0), (300, 700), (520, 64)])
+def test_paired_prefill_attention(m7, n, P):
+    """attn_prefill.cu (two 128-query tiles per CTA, P in TMEM, 128-key blocks) against the
+    single-tile kernel and the exact SIMT attention: ragged pairs (a lone tile A), a past that is
+    not a multiple of the key block, every row's logits."""
+    rng = np.random.default_rng(n * 7 + P)
+    t = rng.integers(0, 259, P + n)
+    p = np.arange(P + n)
+    out = {}
+    for name, opts in (("pair", {"attn_pair": 2}), ("single", {"attn_pair": 0}), ("simt", {"force_simt_attn": 1})):
+        for k, v in opts.items():
+            m7.set_option(k, v)
+        past = m7.forward(t[:P], p[:P])[1] if P else None
+        logits, kv = m7.forward(t[P:], p[P:], past=past)
+        out[name] = (logits, kv.layer(1, 0), kv.layer(1, 1))
+        m7.set_option("attn_pair", 1)
+        m7.set_option("force_simt_attn", 0)
+    for other in ("single", "simt"):
+        for x, y in zip(out["pair"], out[other]):
+            assert rel(x, y) <= BF16_REL, (other, rel(x, y))
+    assert all(same_greedy_token(a, b) for a, b in zip(out["pair"][0], out["simt"][0]))
+
+
 @pytest.mark.parametrize("M", [1, 7, 16, 33, 64, 100, 128, 200, 256, 300])
 def test_gemm_token_counts(m7, M):
     rng = np.random.default_rng(M)

@@ -223,12 +223,17 @@ def test_w7b_prefill_matches_reference(w7b, w7b_gold):
     ragged 64-row tail and causal tcgen05 attention; logits and layer-1 K/V rows."""
     m, _, _, _ = w7b
     toks = pc.w7b_prefill_tokens()
-    logits, kv = m.forward(toks, list(range(len(toks))))
-    check_bf16(logits[0], w7b_gold["prefill_row0"], "w7b prefill row0")
-    check_bf16(logits[-1], w7b_gold["prefill_last"], "w7b prefill last")
-    rows = w7b_gold["prefill_kv_rows"]
-    assert rel(kv.layer(1, 0)[rows], w7b_gold["prefill_k1"]) <= BF16_REL
-    assert rel(kv.layer(1, 1)[rows], w7b_gold["prefill_v1"]) <= BF16_REL
+    # attn_pair 0: single-tile k_attn_tc; 2: the paired-tile prefill kernel (attn_prefill.cu,
+    # used at full-prefill sizes; forced here at 320 rows: one full pair + a lone 64-row tile)
+    for pair in (0, 2):
+        m.set_option("attn_pair", pair)
+        logits, kv = m.forward(toks, list(range(len(toks))))
+        check_bf16(logits[0], w7b_gold["prefill_row0"], f"w7b prefill row0 pair={pair}")
+        check_bf16(logits[-1], w7b_gold["prefill_last"], f"w7b prefill last pair={pair}")
+        rows = w7b_gold["prefill_kv_rows"]
+        assert rel(kv.layer(1, 0)[rows], w7b_gold["prefill_k1"]) <= BF16_REL
+        assert rel(kv.layer(1, 1)[rows], w7b_gold["prefill_v1"]) <= BF16_REL
+    m.set_option("attn_pair", 1)
 
 
 # ---------------------------------------------------------------------------
