@@ -134,9 +134,12 @@ struct ChainSmem {
   static constexpr int kPB = BN <= 64 ? (kPbAttn > kPbGemm ? kPbAttn : kPbGemm) : 0;
   static constexpr int kBytes = STAGES * kStage + kPB + 1024 + 1024 + 1024 + 2 * 16 * 128 * 4;  // + LN-fold scratch
   static constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;
-  // attention phase layout of the ring: Q (32 KB), two P buffers (32 KB), K/V stages of 32 KB
-  static constexpr int kAttnFit = (STAGES * kStage - 65536) / 32768;
-  static constexpr int kAttnKV = kAttnFit > 4 ? 4 : kAttnFit;  // 2 stages: +4.7 us per layer
+  // attention phase: Q (32 KB) in the cluster exchange buffer when there is one (it is only
+  // needed there after the last QK^T), P in TMEM, and the ring re-carved as K/V stages of 32 KB
+  // (the phase is bound by K/V arrival: 4 -> 5 stages)
+  static constexpr bool kQInPb = kPB >= 32768;
+  static constexpr int kAttnFit = (STAGES * kStage - (kQInPb ? 0 : 32768)) / 32768;
+  static constexpr int kAttnKV = kAttnFit > 6 ? 6 : kAttnFit;
   static_assert(kAttnKV >= 2, "attention phase needs two K/V stages in the ring");
 };
 
@@ -150,6 +153,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const float* v) {
       "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
       "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16u(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -260,13 +271,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   // columns [256, 512), clear of the GEMM accumulators
   const bool has_attn = p.ph[0].kind == CHAIN_ATTN;
   constexpr int AKV = S::kAttnKV;
-  uint8_t* aQ = smem;
-  uint8_t* aPb = smem + 32768;
-  uint8_t* aKV = smem + 65536;
+  uint8_t* aQ = S::kQInPb ? reinterpret_cast<uint8_t*>(pb) : smem;
+  uint8_t* aKV = S::kQInPb ? smem : smem + 32768;
   uint64_t* a_qfull = full + 64;
   uint64_t* a_kvfull = a_qfull + 1;    // [AKV]
-  uint64_t* a_kvempty = a_kvfull + 4;  // [AKV]
-  uint64_t* a_sfull = a_kvempty + 4;   // [2]
+  uint64_t* a_kvempty = a_kvfull + 8;  // [AKV]
+  uint64_t* a_sfull = a_kvempty + 8;   // [2]
   uint64_t* a_pfull = a_sfull + 2;     // [2] (two: see attn_tc.cu, one p_full can deadlock)
   uint64_t* a_pvdone = a_pfull + 2;    // [2]
   uint64_t* a_done = a_pvdone + 2;     // this CTA's attention is off the ring (128 arrivals)
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         attn_range(p.ph[0], h, sp, b0, nb);
         constexpr uint32_t idS = idesc_bf16(128, 64);
         constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
-        const uint32_t q_addr = smem_u32(aQ), p_addr = smem_u32(aPb);
+        const uint32_t q_addr = smem_u32(aQ);
         mbar_wait(a_qfull, 0);
         long long kv_wait = 0, p_wait = 0;
         auto issue_qk = [&](int it) {
@@ -507,11 +517,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           if (p.tl) p_wait += clock64() - t1;
           tc_fence_after();
           const uint32_t v_addr = smem_u32(aKV + (it % AKV) * 32768 + 16384);
-          const uint32_t pb = p_addr + (it & 1) * 16384;
+          // P(it) is the A operand straight from TMEM: packed bf16 over the first 32 columns of
+          // its score buffer (S(it + 2) reuses the buffer; it is issued after this PV)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(aO, sw128_kmajor_desc(pb + k * 32), sw128_mnmajor_desc(v_addr + k * 2048, 8192, 1024), idO,
-                      (it > 0 || k > 0) ? 1u : 0u);
+            umma_bf16_ts(aO, aS0 + (it & 1) * 64 + k * 8, sw128_mnmajor_desc(v_addr + k * 2048, 8192, 1024), idO,
+                         (it > 0 || k > 0) ? 1u : 0u);
           umma_commit(&a_pvdone[it & 1]);
           umma_commit(&a_kvempty[it % AKV]);
         }
@@ -608,15 +619,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           const int hi = NC == 32 ? (row >> 6) : 0;     // dup: which half of each block's keys
           const int c0 = hi * 32;
           const float ascale = P.ascale, thr = kRescaleThreshold / ascale;
-          // dup: this lane's P row is zero in the other half's 16-byte chunks for every block;
-          // those zeros are written once per P buffer here instead of every block
-          if (NC == 32 && live)
-#pragma unroll
-            for (int pb_ = 0; pb_ < 2; ++pb_)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                *reinterpret_cast<uint4*>(aPb + pb_ * 16384 + row * 128 + (((4 * (1 - hi) + k) ^ (row & 7)) << 4)) =
-                    make_uint4(0u, 0u, 0u, 0u);
           // key-block visibility in 32-bit arithmetic (positions < 2^31, checked on the host):
           // lim = last visible key of the block relative to this lane's first column
           int sg = 0, seg_first = 0, seg_next = P.a_nseg ? P.a_first[1] : 0x7fffffff;
@@ -637,7 +639,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               lim = static_cast<int>(P.aP) + qi - b * 64 - c0;
             }
             if (!live) {
-              if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);
+              // S(it) was issued after p_full(it - 2) completed: arriving after it keeps this
+              // warp's arrival out of block it - 2's phase of the same barrier
+              mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
               mbar_arrive(&a_pfull[it & 1]);
               continue;
             }
@@ -723,16 +727,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               expo(m == -INFINITY ? 0.f : m * ascale);
             }
             l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
-            if (it > 1) mbar_wait(&a_pvdone[it & 1], ((it - 2) >> 1) & 1);  // P buffer free
-            // P row (64 keys, SW128): this lane's 16-byte chunks (dup: half of them)
-            uint8_t* prow = aPb + (it & 1) * 16384 + row * 128;
-#pragma unroll
-            for (int k = 0; k < NC / 8; ++k)  // chunk x = 4 hi + k holds columns [8x, 8x + 8)
-              *reinterpret_cast<uint4*>(prow + (((4 * hi + k) ^ (row & 7)) << 4)) =
-                  make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3]);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            // P row into TMEM over the first 32 columns of the score buffer (64 bf16 keys; dup:
+            // this lane's half of the keys, zeros in the other half)
+            {
+              const uint32_t pa = aS0 + (it & 1) * 64 + lane_off;
+              if constexpr (NC == 64) {
+                tmem_st16u(pa, packed);
+                tmem_st16u(pa + 16, packed + 16);
+              } else {
+                const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                tmem_st16u(pa + 16 * hi, packed);
+                tmem_st16u(pa + 16 * (1 - hi), z);
+              }
+              tmem_st_wait();
+            }
             tc_fence_before();
-            mbar_arrive(&a_pfull[it & 1]);  // ordered after block it-2's phase by the P-buffer wait
+            mbar_arrive(&a_pfull[it & 1]);  // ordered after block it-2's phase: S(it) needed p_full(it-2)
           }
         };
         if (dup) blocks(std::integral_constant<int, 32>{});
@@ -1234,6 +1244,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             for (int pass = (p.warm && P.kbs / P.S >= 32) ? 0 : 1; pass < 2; ++pass) {
               const bool dry = pass == 0;
               if (!dry) {
+                // the residual slice (written a phase or a launch ago: an HBM / loaded-L2 round
+                // trip of ~2 us) is read while the accumulator is still being filled
+                if (s0 < lim) epi_prefetch(e, n, P.N, s0, lim, cur);
                 mbar_wait(&acc_full[buf], (seg >> 1) & 1);
                 tc_fence_after();
                 if (et == 0) ctl(p, ph, 4);
@@ -1251,7 +1264,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 mbar_arrive(&acc_empty[buf]);
                 pb_signal(pb_ready, g0, P.S);
               }
-              if (s0 < lim) epi_prefetch(e, n, P.N, s0, lim, cur);
+              if (dry && s0 < lim) epi_prefetch(e, n, P.N, s0, lim, cur);
               if (!dry) {
                 pb_wait(pb_ready, pb_uses & 1);
                 if (et == 0) ctl(p, ph, 5);
