@@ -210,6 +210,7 @@ int pcb_model_set_option(pcb_model* m, const char* key, int64_t v) {
     else if (std::strcmp(key, "chain_attn") == 0) m->m->chain_attn = v != 0;
     else if (std::strcmp(key, "zero_copy") == 0) m->m->zero_copy = v != 0;
     else if (std::strcmp(key, "attn_pair") == 0) m->m->attn_pair = v;
+    else if (std::strcmp(key, "chain_group") == 0) m->m->chain_group = v;
     else throw Error(ErrorCode::InvalidConfig, std::string("unknown option ") + key);
   });
 }

@@ -1060,12 +1060,22 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
                            kern::chain_attn_supported(n, P, H, hd);
     if (!kv_prefix_.empty() && (!fuse_attn || P < kv_prefix_rows_))
       throw Error(ErrorCode::ShapeMismatch, "zero-copy prefix set for a forward that cannot read it in place");
-    kern::ChainStep steps[8];
-    steps[0] = ln(W.h, n);
-    steps[1] = mm(W.x, w_->wqkv[0], n, 3 * d, d, qkv_epi(0));
-    chain(steps, 2);
+    // Layers per launch: with the attention as a chain phase and no per-layer event gating it
+    // (slow-tier uploads), one launch spans up to chain_group layers -- no launch gap, prologue
+    // or cold attention start between them; otherwise one launch per layer.
+    const int group = fuse_attn && layer_ev.empty() ? std::max(1, chain_group) : 1;
+    kern::ChainStep steps[kern::kChainMaxPhases];
+    int k = 0, in_launch = 0;
+    auto flush = [&] {
+      if (k) chain(steps, k);
+      k = 0;
+      in_launch = 0;
+    };
+    steps[k++] = ln(W.h, n);
+    steps[k++] = mm(W.x, w_->wqkv[0], n, 3 * d, d, qkv_epi(0));
+    if (group == 1) flush();
     for (int l = 0; l < c.n_layers; ++l) {
-      int k = 0;
+      if (in_launch == group || k + 8 > kern::kChainMaxPhases) flush();
       if (fuse_attn) {
         if (l < static_cast<int>(layer_ev.size())) CK(cudaStreamWaitEvent(s, layer_ev[l], 0));
         kern::ChainStep st;
@@ -1095,6 +1105,7 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
         }
         steps[k++] = st;
       } else {
+        flush();
         attention(l);
       }
       if (ln_fold && d % 128 == 0) {
@@ -1141,8 +1152,10 @@ void Model::run_impl(const BatchItem* items, int B, const uint8_t* mask, const i
           steps[k++] = mm(W.x, w_->unembed, logit_rows, c.vocab_size, d, ef);
         }
       }
-      chain(steps, k);
+      ++in_launch;
+      if (group == 1) flush();
     }
+    flush();
   } else {
     for (int l = 0; l < c.n_layers; ++l) {
       prof_begin();

@@ -166,6 +166,7 @@ class Model {
   int attn_pair = 1;             // paired-tile prefill attention: 0 off, 1 when it fills the GPU, 2 always
   bool use_chain = true;         // few-token GEMM/LN segments as one persistent chain kernel (PCB_CHAIN=0: off)
   bool ln_fold = true;           // chain: LayerNorm folded into the neighbouring GEMMs (PCB_LN_FOLD=0: off)
+  int chain_group = 9;           // chain: layers per launch when the attention is a chain phase (1: per layer)
   bool chain_attn = true;        // chain: a single request's attention as the chain's first phase (PCB_CHAIN_ATTN=0: off)
   bool zero_copy = true;         // serve: cached modules read in place by the attention, no assembly copy (PCB_ZERO_COPY=0: off)
   int64_t launches = 0;          // kernels launched by run() (bench evidence)

@@ -52,7 +52,8 @@ CUtensorMap tmap_bf16_3d(const void* ptr, uint64_t cols, uint64_t rows, uint64_t
 
 namespace {
 
-constexpr int kMaxPhases = 8;
+constexpr int kMaxPhases = kChainMaxPhases;  // [LN1, QKV] + 9 layers x [ATTN, O, W1, W2, QKV] + unembed
+constexpr int kMaxAttn = 9;     // attention phases per launch
 constexpr int kChainThreads = 224;  // 7 warps
 constexpr int kWTileC = 128 * 64 * 2;
 
@@ -83,6 +84,7 @@ struct PhaseDev {
   // [a_row0[s], a_row0[s] + a_rows[s]) of its source (tensor map tkv[s], plane 2 layer + w);
   // the last segment is the request's own rows (first a_tail_vis visible to all queries)
   int a_nseg, a_layer, a_tail_vis;
+  int a_map;  // index of the phase's K / V maps (contiguous cache)
   const float* a_alibi;   // ALiBi slopes [aH] (null: off); key positions by key block, query positions
   const int32_t* a_kpos;
   const int32_t* a_qpos;
@@ -93,7 +95,8 @@ struct PhaseDev {
 
 struct ChainParams {
   CUtensorMap tm[kMaxPhases];  // activation maps of the GEMM phases
-  CUtensorMap tma[3];          // attention phase: Q [n][d], K and V planes [P + n][d]
+  CUtensorMap tma[1];          // attention phases: Q [n][d] (one buffer for every layer)
+  CUtensorMap tak[kMaxAttn], tav[kMaxAttn];  // attention phase a_map: K and V planes [P + n][d]
   CUtensorMap tkv[ChainStep::kMaxSeg];  // attention phase, zero-copy: {d, cap, planes} per KV source
   PhaseDev ph[kMaxPhases];
   int n_phases;
@@ -104,7 +107,6 @@ struct ChainParams {
   unsigned long long* gbar;  // grid barrier arrival counter (monotonic)
   unsigned long long gbar_base;
   unsigned long long* tl;    // timeline probe [phase][cta][4] (null: off)
-  int pf_dist;               // weight tiles prefetched into L2 ahead of the ring (0: off)
   int warm;                  // dry epilogue pass while the weights stream (instruction cache)
   int dsm;                   // launched in clusters of 4: split partials / attention splits meet in DSMEM
 };
@@ -269,17 +271,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   // attention phase (first phase only): the ring's shared memory is re-carved as Q, P and
   // K/V stages; its barriers sit 512 bytes into the barrier block; S and O live in TMEM
   // columns [256, 512), clear of the GEMM accumulators
-  const bool has_attn = p.ph[0].kind == CHAIN_ATTN;
+  // attention phases: any position (a launch spans several layers); each takes the ring for
+  // its K/V stages and needs the previous phase's outputs (Q, the new K/V rows)
+  bool has_attn = false;
+  for (int ph = 0; ph < p.n_phases; ++ph) has_attn |= p.ph[ph].kind == CHAIN_ATTN;
   constexpr int AKV = S::kAttnKV;
   uint8_t* aQ = S::kQInPb ? reinterpret_cast<uint8_t*>(pb) : smem;
   uint8_t* aKV = S::kQInPb ? smem : smem + 32768;
   uint64_t* a_qfull = full + 64;
   uint64_t* a_kvfull = a_qfull + 1;    // [AKV]
   uint64_t* a_kvempty = a_kvfull + 8;  // [AKV]
-  uint64_t* a_sfull = a_kvempty + 8;   // [2]
-  uint64_t* a_pfull = a_sfull + 2;     // [2] (two: see attn_tc.cu, one p_full can deadlock)
-  uint64_t* a_pvdone = a_pfull + 2;    // [2]
-  uint64_t* a_done = a_pvdone + 2;     // this CTA's attention is off the ring (128 arrivals)
+  // three score buffers: S(it + 2) is issued right after PV(it), so S(it + 1) is ready when the
+  // softmax of block it ends (with two, S(it + 1) waited for PV(it - 1): ~500 cycles per block)
+  uint64_t* a_sfull = a_kvempty + 8;   // [3] block it -> buffer it % 3, phase (it / 3) & 1
+  uint64_t* a_pfull = a_sfull + 3;     // [3] (one per buffer: a single p_full can deadlock, attn_tc.cu)
+  uint64_t* a_pvdone = a_pfull + 3;    // [3]
+  uint64_t* a_done = a_pvdone + 3;     // this CTA's attention is off the ring (128 arrivals)
   // exchange-buffer barriers (dsm): pb_ready completes when every CTA of this CTA's group
   // has parked its data (each group member arrives once with count 4 / S, S = group size),
   // pb_free when they have all finished reading this CTA's buffer
@@ -310,12 +317,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         mbar_init(&a_kvfull[s], 1);
         mbar_init(&a_kvempty[s], 1);
       }
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < 3; ++b) {
         mbar_init(&a_sfull[b], 1);
         mbar_init(&a_pvdone[b], 1);
+        mbar_init(&a_pfull[b], 128);
       }
-      mbar_init(&a_pfull[0], 128);
-      mbar_init(&a_pfull[1], 128);
       mbar_init(a_done, 128);
     }
     if (dsm) {
@@ -333,7 +339,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   if (dsm) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t aS0 = tmem + 256, aO = tmem + 384;  // attention: two score buffers, O
+  // attention: three 64-column score buffers at [192, 384), O at [384, 512) (the GEMM
+  // accumulators [0, 2 BN) are only written by MMAs issued after the last PV)
+  const uint32_t aS0 = tmem + 192, aO = tmem + 384;
 
   // attention item of this CTA: head h, key split sp -> key blocks [b0, b0 + nb) of 64
   auto attn_range = [&](const PhaseDev& A, int& h, int& sp, int& b0, int& nb) {
@@ -358,96 +366,79 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   if (warp == 0) {
     // ---- W producer: never waits for a phase boundary ----
     if (elect_one()) {
-      if (has_attn) {
-        // attention loads first (Q once, then the K/V blocks of this CTA's split); the
-        // weight stream resumes once this CTA's attention no longer uses the ring
-        const PhaseDev& A = p.ph[0];
-        if (c < A.items) {
-          int h, sp, b0, nb;
-          attn_range(A, h, sp, b0, nb);
-          tma_prefetch(&p.tma[0]);
-          if (A.a_nseg) {
-            for (int sgi = 0; sgi < A.a_nseg; ++sgi) tma_prefetch(&p.tkv[sgi]);
-          } else {
-            tma_prefetch(&p.tma[1]);
-            tma_prefetch(&p.tma[2]);
-          }
-          pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
-          mbar_expect_tx(a_qfull, 32768);
-          for (int a = 0; a < 2; ++a)  // 64-row boxes: rows [0, 64) twice (dup) or [0, 128)
-            for (int hh = 0; hh < 2; ++hh)
-              tma_load_2d(aQ + a * 16384 + hh * 8192, &p.tma[0], a_qfull, h * 128 + a * 64, A.adup ? 0 : 64 * hh);
-          for (int it = 0, sg = 0; it < nb; ++it) {
-            const int s = it % AKV;
-            mbar_wait(&a_kvempty[s], ((it / AKV) & 1) ^ 1);
-            uint8_t* st = aKV + s * 32768;
-            const int b = b0 + it;
-            mbar_expect_tx(&a_kvfull[s], A.a_alibi ? 32768 + 256 : 32768);
-            if (A.a_alibi)  // the block's 64 key positions into the (idle) LN-fold scratch
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                      smem_u32(reinterpret_cast<int32_t*>(colsum) + s * 64)),
-                  "l"(A.a_kpos + static_cast<int64_t>(b) * 64), "r"(256), "r"(smem_u32(&a_kvfull[s]))
-                  : "memory");
-            if (A.a_nseg) {
-              while (b >= A.a_first[sg + 1]) ++sg;
-              const int row = A.a_row0[sg] + (b - A.a_first[sg]) * 64;
-              for (int a = 0; a < 2; ++a) {
-                tma_load_3d(st + a * 8192, &p.tkv[sg], &a_kvfull[s], h * 128 + a * 64, row, 2 * A.a_layer);
-                tma_load_3d(st + 16384 + a * 8192, &p.tkv[sg], &a_kvfull[s], h * 128 + a * 64, row, 2 * A.a_layer + 1);
-              }
-            } else {
-              for (int a = 0; a < 2; ++a) {
-                tma_load_2d(st + a * 8192, &p.tma[1], &a_kvfull[s], h * 128 + a * 64, b * 64);
-                tma_load_2d(st + 16384 + a * 8192, &p.tma[2], &a_kvfull[s], h * 128 + a * 64, b * 64);
-              }
-            }
-          }
-        }
-        mbar_wait(a_done, 0);
-        ctl(p, 0, 3);
-      }
       const uint64_t pol_w = policy_evict_first();
-      // optional L2 prefetch of this CTA's weight tiles pf_dist tiles ahead of the issue point
-      // (keeps HBM busy through phase tails, when the ring is full and waits on the barrier)
-      struct Cursor {
-        int ph = -1, i = 0, kb = 0, kb1 = 0, tile = 0;
-      } pf;
-      auto pf_next = [&](Cursor& u) -> bool {  // advance to the next weight tile of this CTA
-        while (true) {
-          if (u.ph >= 0 && ++u.kb < u.kb1) return true;
-          if (u.ph >= 0) u.i += C;
-          while (u.ph < p.n_phases && (u.ph < 0 || p.ph[u.ph].kind != CHAIN_GEMM || u.i >= p.ph[u.ph].items)) {
-            ++u.ph;
-            u.i = c;
-            if (u.ph >= p.n_phases) return false;
-          }
-          int kb0;
-          item_kb(p.ph[u.ph], u.i, u.tile, kb0, u.kb1);
-          u.kb = kb0 - 1;
-        }
-      };
-      int pf_left = p.pf_dist;
-      bool pf_ok = pf_left > 0;
-      auto pf_issue = [&]() {
-        if (!pf_ok) return;
-        if (!(pf_ok = pf_next(pf))) return;
-        const PhaseDev& Q = p.ph[pf.ph];
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Q.w + (static_cast<int64_t>(pf.tile) * Q.kbs + pf.kb) * kWTileC),
-                     "r"(kWTileC)
-                     : "memory");
-      };
-      while (pf_left-- > 0) pf_issue();  // the window: pf_dist tiles ahead
-      int it = 0;
+      int it = 0, ab = 0, an = 0;  // weight stages issued; attention blocks / phases so far
       for (int ph = 0; ph < p.n_phases; ++ph) {
         const PhaseDev& P = p.ph[ph];
+        if (P.kind == CHAIN_ATTN) {
+          // attention loads (Q once, then the K/V blocks of this CTA's split) through the ring;
+          // the weight stream resumes once this CTA's softmax no longer uses it
+          if (c < P.items) {
+            int h, sp, b0, nb;
+            attn_range(P, h, sp, b0, nb);
+            const CUtensorMap* tk = &p.tak[P.a_map];
+            const CUtensorMap* tv = &p.tav[P.a_map];
+            tma_prefetch(&p.tma[0]);
+            if (P.a_nseg) {
+              for (int sgi = 0; sgi < P.a_nseg; ++sgi) tma_prefetch(&p.tkv[sgi]);
+            } else {
+              tma_prefetch(tk);
+              tma_prefetch(tv);
+            }
+            if (ph == 0) {
+              pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
+            } else {
+              // every weight stage issued so far has been consumed (the K/V stages overwrite
+              // the ring), then the grid barrier that publishes the QKV phase before
+              for (int k = 0; k < STAGES; ++k) mbar_wait(&empty[(it + k) % STAGES], (((it + k) / STAGES) & 1) ^ 1);
+              grid_wait(p, ph);
+              fence_proxy_async_global();
+            }
+            mbar_expect_tx(a_qfull, 32768);
+            for (int a = 0; a < 2; ++a)  // 64-row boxes: rows [0, 64) twice (dup) or [0, 128)
+              for (int hh = 0; hh < 2; ++hh)
+                tma_load_2d(aQ + a * 16384 + hh * 8192, &p.tma[0], a_qfull, h * 128 + a * 64, P.adup ? 0 : 64 * hh);
+            for (int j = 0, sg = 0; j < nb; ++j) {
+              const int g = ab + j;  // block sequence over the launch's attention phases
+              const int s = g % AKV;
+              mbar_wait(&a_kvempty[s], ((g / AKV) & 1) ^ 1);
+              uint8_t* st = aKV + s * 32768;
+              const int b = b0 + j;
+              mbar_expect_tx(&a_kvfull[s], P.a_alibi ? 32768 + 256 : 32768);
+              if (P.a_alibi)  // the block's 64 key positions into the (idle) LN-fold scratch
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(reinterpret_cast<int32_t*>(colsum) + s * 64)),
+                    "l"(P.a_kpos + static_cast<int64_t>(b) * 64), "r"(256), "r"(smem_u32(&a_kvfull[s]))
+                    : "memory");
+              if (P.a_nseg) {
+                while (b >= P.a_first[sg + 1]) ++sg;
+                const int row = P.a_row0[sg] + (b - P.a_first[sg]) * 64;
+                for (int a = 0; a < 2; ++a) {
+                  tma_load_3d(st + a * 8192, &p.tkv[sg], &a_kvfull[s], h * 128 + a * 64, row, 2 * P.a_layer);
+                  tma_load_3d(st + 16384 + a * 8192, &p.tkv[sg], &a_kvfull[s], h * 128 + a * 64, row,
+                              2 * P.a_layer + 1);
+                }
+              } else {
+                for (int a = 0; a < 2; ++a) {
+                  tma_load_2d(st + a * 8192, tk, &a_kvfull[s], h * 128 + a * 64, b * 64);
+                  tma_load_2d(st + 16384 + a * 8192, tv, &a_kvfull[s], h * 128 + a * 64, b * 64);
+                }
+              }
+            }
+            ab += nb;
+            mbar_wait(a_done, an & 1);
+          }
+          ++an;
+          ctl(p, ph, 3);
+          continue;
+        }
         if (P.kind != CHAIN_GEMM) continue;
         for (int i = c; i < P.items; i += C) {
           int tile, kb0, kb1;
           item_kb(P, i, tile, kb0, kb1);
           for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const int s = it % STAGES;
-            pf_issue();
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
             mbar_expect_tx(&full[s], S::kStage);
             // packed tiles of one 128-row block are contiguous along K
@@ -486,54 +477,61 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   } else if (warp == 1) {
     // ---- MMA issuer: one accumulator per item ----
     if (elect_one()) {
-      if (has_attn && c < p.ph[0].items) {
-        // S_j = Q K_j^T (M=128, N=64, K=128) into one of two score buffers while the
-        // softmax of block j-1 runs; O += P_j V_j (V MN-major) accumulated in TMEM
+      // attention phase: S_j = Q K_j^T (M=128, N=64, K=128) into one of three score buffers,
+      // O += P_j V_j (P from TMEM, V MN-major) accumulated in TMEM
+      int ab = 0, aw = 0;  // attention blocks / phases with work so far (barrier phases)
+      auto attn_mma = [&](const PhaseDev& A, int ph) {
         int h, sp, b0, nb;
-        attn_range(p.ph[0], h, sp, b0, nb);
+        attn_range(A, h, sp, b0, nb);
         constexpr uint32_t idS = idesc_bf16(128, 64);
         constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
         const uint32_t q_addr = smem_u32(aQ);
-        mbar_wait(a_qfull, 0);
+        mbar_wait(a_qfull, aw & 1);
+        ++aw;
         long long kv_wait = 0, p_wait = 0;
-        auto issue_qk = [&](int it) {
-          const int s = it % AKV;
+        auto issue_qk = [&](int j) {
+          const int g = ab + j, s = g % AKV;
           const long long t0 = p.tl ? clock64() : 0;
-          mbar_wait(&a_kvfull[s], (it / AKV) & 1);
+          mbar_wait(&a_kvfull[s], (g / AKV) & 1);
           if (p.tl) kv_wait += clock64() - t0;
           tc_fence_after();
           const uint32_t k_addr = smem_u32(aKV + s * 32768);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            umma_bf16(aS0 + (it & 1) * 64, sw128_kmajor_desc(q_addr + (k >> 2) * 16384 + (k & 3) * 32),
+            umma_bf16(aS0 + (g % 3) * 64, sw128_kmajor_desc(q_addr + (k >> 2) * 16384 + (k & 3) * 32),
                       sw128_kmajor_desc(k_addr + (k >> 2) * 8192 + (k & 3) * 32), idS, k > 0 ? 1u : 0u);
-          umma_commit(&a_sfull[it & 1]);
+          umma_commit(&a_sfull[g % 3]);
         };
         issue_qk(0);
-        for (int it = 0; it < nb; ++it) {
-          if (it + 1 < nb) issue_qk(it + 1);
+        if (nb > 1) issue_qk(1);
+        for (int j = 0; j < nb; ++j) {
+          const int g = ab + j;
           const long long t1 = p.tl ? clock64() : 0;
-          mbar_wait(&a_pfull[it & 1], (it >> 1) & 1);
+          mbar_wait(&a_pfull[g % 3], (g / 3) & 1);
           if (p.tl) p_wait += clock64() - t1;
           tc_fence_after();
-          const uint32_t v_addr = smem_u32(aKV + (it % AKV) * 32768 + 16384);
-          // P(it) is the A operand straight from TMEM: packed bf16 over the first 32 columns of
-          // its score buffer (S(it + 2) reuses the buffer; it is issued after this PV)
+          const uint32_t v_addr = smem_u32(aKV + (g % AKV) * 32768 + 16384);
+          // P(j) is the A operand straight from TMEM: packed bf16 over the first 32 columns of
+          // its score buffer (S(j + 3) reuses the buffer; it is issued after this PV)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16_ts(aO, aS0 + (it & 1) * 64 + k * 8, sw128_mnmajor_desc(v_addr + k * 2048, 8192, 1024), idO,
-                         (it > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&a_pvdone[it & 1]);
-          umma_commit(&a_kvempty[it % AKV]);
+            umma_bf16_ts(aO, aS0 + (g % 3) * 64 + k * 8, sw128_mnmajor_desc(v_addr + k * 2048, 8192, 1024), idO,
+                         (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&a_pvdone[g % 3]);
+          umma_commit(&a_kvempty[g % AKV]);
+          // S(j + 2) into the buffer of P(j - 1), whose PV was issued an iteration ago
+          if (j + 2 < nb) issue_qk(j + 2);
         }
-        ctl(p, 0, 1);
-        ctl_val(p, 0, 14, kv_wait);  // MMA thread: cycles waiting for K/V blocks, for P
-        ctl_val(p, 0, 15, p_wait);
-      }
+        ab += nb;
+        ctl(p, ph, 1);
+        ctl_val(p, ph, 14, kv_wait);  // MMA thread: cycles waiting for K/V blocks, for P
+        ctl_val(p, ph, 15, p_wait);
+      };
       constexpr uint32_t idesc = idesc_bf16(128, BN);
       int it = 0, seg = 0;
       for (int ph = 0; ph < p.n_phases; ++ph) {
         const PhaseDev& P = p.ph[ph];
+        if (P.kind == CHAIN_ATTN && c < P.items) attn_mma(P, ph);
         if (P.kind != CHAIN_GEMM) continue;
         for (int i = c; i < P.items; i += C, ++seg) {
           int tile, kb0, kb1;
@@ -566,6 +564,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     float v[16];
     int seg = 0;
+    int ab = 0;            // attention blocks so far (buffer / barrier phases)
     uint32_t pb_uses = 0;  // dsm: completed uses of this CTA's exchange buffer
     // dsm helpers: the S CTAs [g0, g0 + S) of a group sit in one cluster of 4 (C % 4 == 0,
     // S in {1, 2, 4}, groups aligned), so a member's cluster rank is its index & 3
@@ -626,6 +625,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             // contiguous: key j visible iff j <= P + qi; zero-copy: a prefix segment's rows
             // are all visible (its padding is not), the tail is visible up to tail_vis + qi
             const int b = b0 + it;
+            const int g = ab + it;  // block sequence over the launch's attention phases
             int lim;
             if (P.a_nseg) {
               while (b >= seg_next) {
@@ -640,28 +640,28 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             }
             if (!live) {
               // S(it) was issued after p_full(it - 2) completed: arriving after it keeps this
-              // warp's arrival out of block it - 2's phase of the same barrier
-              mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
-              mbar_arrive(&a_pfull[it & 1]);
+              // warp's arrival out of block it - 3's phase of the same barrier
+              mbar_wait(&a_sfull[g % 3], (g / 3) & 1);
+              mbar_arrive(&a_pfull[g % 3]);
               continue;
             }
             const long long tw0 = p.tl ? clock64() : 0;
-            mbar_wait(&a_sfull[it & 1], (it >> 1) & 1);
+            mbar_wait(&a_sfull[g % 3], (g / 3) & 1);
             if (p.tl) sfull_wait += clock64() - tw0;
             tc_fence_after();
             float sv[NC];
             {
               uint32_t raw[NC];
 #pragma unroll
-              for (int x = 0; x < NC; x += 16) tmem_ld16_nowait(aS0 + (it & 1) * 64 + lane_off + c0 + x, raw + x);
+              for (int x = 0; x < NC; x += 16) tmem_ld16_nowait(aS0 + (g % 3) * 64 + lane_off + c0 + x, raw + x);
               tmem_wait_ld();
 #pragma unroll
               for (int x = 0; x < NC; ++x) sv[x] = __uint_as_float(raw[x]);
             }
             if (alibi) {
-              mbar_wait(&a_kvfull[it % AKV], (it / AKV) & 1);  // the positions' bulk copy (complete)
+              mbar_wait(&a_kvfull[g % AKV], (g / AKV) & 1);  // the positions' bulk copy (complete)
               const int4* kp = reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(colsum) +
-                                                             (it % AKV) * 64 + c0);
+                                                             (g % AKV) * 64 + c0);
 #pragma unroll
               for (int x = 0; x < NC; x += 4) {
                 const int4 k4 = kp[x >> 2];
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             const bool grow = bm > m + thr || (m == -INFINITY && bm > -INFINITY);
             if (__any_sync(0xffffffffu, grow)) {
               if (it > 0) {
-                mbar_wait(&a_pvdone[(it - 1) & 1], ((it - 1) >> 1) & 1);
+                mbar_wait(&a_pvdone[(g - 1) % 3], ((g - 1) / 3) & 1);
                 tc_fence_after();
                 const float f = grow ? fast_exp2((m - bm) * ascale) : 1.f;
 #pragma unroll 1
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             // P row into TMEM over the first 32 columns of the score buffer (64 bf16 keys; dup:
             // this lane's half of the keys, zeros in the other half)
             {
-              const uint32_t pa = aS0 + (it & 1) * 64 + lane_off;
+              const uint32_t pa = aS0 + (g % 3) * 64 + lane_off;
               if constexpr (NC == 64) {
                 tmem_st16u(pa, packed);
                 tmem_st16u(pa + 16, packed + 16);
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               tmem_st_wait();
             }
             tc_fence_before();
-            mbar_arrive(&a_pfull[it & 1]);  // ordered after block it-2's phase: S(it) needed p_full(it-2)
+            mbar_arrive(&a_pfull[g % 3]);  // after block it-3's phase: S(it) needed p_full(it-2)
           }
         };
         if (dup) blocks(std::integral_constant<int, 32>{});
@@ -763,8 +763,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         float* part = P.apart + (static_cast<int64_t>(c) * 128 + qi) * 128;
         float2* ml = reinterpret_cast<float2*>(P.apart + static_cast<int64_t>(P.items) * 128 * 128);
         if (nb > 0) {
-          mbar_wait(&a_pvdone[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+          mbar_wait(&a_pvdone[(ab + nb - 1) % 3], ((ab + nb - 1) / 3) & 1);
           tc_fence_after();
+          ab += nb;
           constexpr int kXld = 132;  // padded fp32 row
           float* xo = reinterpret_cast<float*>(aKV);
           float2* xml = reinterpret_cast<float2*>(aKV + 64 * kXld * 4);
@@ -1403,7 +1404,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 std::atomic<int> g_chain_epoch{0};
 
 
-constexpr int kProbeMax = 256;
+constexpr int kProbeMax = 64;
 unsigned long long* g_ctl = nullptr;
 int g_ctl_n = 0;
 int g_ctl_ph[kProbeMax];
@@ -1471,6 +1472,8 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   const bool dsm = dsm_grid >= 128;
   const int C = dsm ? dsm_grid : sms;
   p.dsm = dsm ? 1 : 0;
+  int n_attn = 0;
+  const ChainStep* attn0 = nullptr;
   for (int i = 0; i < n; ++i) {
     const ChainStep& st = steps[i];
     PhaseDev& d = p.ph[i];
@@ -1495,7 +1498,14 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
       d.ln_dim = st.ln_dim;
       p.tm[i] = tmap_bf16_2d(st.x, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.K), BN);
     } else if (st.kind == CHAIN_ATTN) {
-      if (i != 0) throw std::runtime_error("chain: attention must be the first phase");
+      // every attention phase of a launch serves the same request (one Q buffer, one segment
+      // table); a contiguous cache has K / V maps per layer
+      if (n_attn == kMaxAttn) throw std::runtime_error("chain: too many attention phases");
+      if (n_attn > 0 && (st.aq != attn0->aq || st.M != attn0->M || st.a_d != attn0->a_d || st.aP != attn0->aP ||
+                         st.a_nseg != attn0->a_nseg || st.aH != attn0->aH))
+        throw std::runtime_error("chain: attention phases of one launch must serve one request");
+      if (n_attn == 0) attn0 = &st;
+      d.a_map = n_attn++;
       d.aP = st.aP;
       d.aH = st.aH;
       d.a_d = st.a_d;
@@ -1518,7 +1528,7 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
         throw std::runtime_error("chain: attention scratch too small");
       static const bool nodup = std::getenv("PCB_CHAIN_ATTN_NODUP") != nullptr;  // A/B switch
       d.adup = st.M <= 64 && !nodup;
-      p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 64);
+      if (d.a_map == 0) p.tma[0] = tmap_bf16_2d(st.aq, static_cast<uint64_t>(st.M), static_cast<uint64_t>(st.a_d), 64);
       d.a_nseg = st.a_nseg;
       if (st.a_nseg) {
         if (st.a_nseg > ChainStep::kMaxSeg) throw std::runtime_error("chain: too many KV segments");
@@ -1531,8 +1541,12 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
           if (g.rows <= 0 || g.row0 + g.rows > g.cap) throw std::runtime_error("chain: bad KV segment");
           // rows end at the segment's last valid row: the rest of a 64-row block is TMA
           // zero fill, never stale memory (a masked key has P = 0, but 0 * NaN in PV is NaN)
-          p.tkv[sgi] = tmap_bf16_3d(g.base, static_cast<uint64_t>(st.a_d), static_cast<uint64_t>(g.row0 + g.rows),
-                                    static_cast<uint64_t>(st.a_planes), g.plane_bytes, 64);
+          const ChainStep::KVSeg& g0 = attn0->a_seg[sgi];
+          if (g.base != g0.base || g.row0 != g0.row0 || g.rows != g0.rows)
+            throw std::runtime_error("chain: attention phases of one launch must share the KV segments");
+          if (d.a_map == 0)
+            p.tkv[sgi] = tmap_bf16_3d(g.base, static_cast<uint64_t>(st.a_d), static_cast<uint64_t>(g.row0 + g.rows),
+                                      static_cast<uint64_t>(st.a_planes), g.plane_bytes, 64);
           d.a_row0[sgi] = static_cast<int>(g.row0);
           d.a_rows[sgi] = static_cast<int>(g.rows);
           d.a_first[sgi + 1] = d.a_first[sgi] + static_cast<int>((g.rows + 63) / 64);
@@ -1540,8 +1554,8 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
         }
         if (keys != st.aP + st.M) throw std::runtime_error("chain: KV segments do not cover the keys");
       } else {
-        p.tma[1] = tmap_bf16_2d(st.ak, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
-        p.tma[2] = tmap_bf16_2d(st.av, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
+        p.tak[d.a_map] = tmap_bf16_2d(st.ak, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
+        p.tav[d.a_map] = tmap_bf16_2d(st.av, static_cast<uint64_t>(st.aP + st.M), static_cast<uint64_t>(st.a_d), 64);
       }
     } else {
       d.ln_src = st.ln_src;
@@ -1558,11 +1572,8 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   p.gbar = gbar;
   p.gbar_base = gbar_count;
   p.tl = chain_probe_slot(n);
-  static const int pf_dist = [] {  // L2 prefetch window (measured slower; off unless asked)
-    const char* v = std::getenv("PCB_CHAIN_L2PF");
-    return v ? std::atoi(v) : 0;
-  }();
-  p.pf_dist = pf_dist;
+  if (p.tl)  // phase kinds for the timeline tools, in a slot no CTA writes (CTA 159, event 15)
+    for (int i = 0; i < n; ++i) p.tl[(static_cast<size_t>(i) * 160 + 159) * 16 + 15] = 1 + p.ph[i].kind;
   static const int warm = [] {  // A/B switch: PCB_CHAIN_WARM=0 turns the dry epilogue pass off
     const char* v = std::getenv("PCB_CHAIN_WARM");
     return v ? std::atoi(v) : 1;
@@ -1671,7 +1682,7 @@ void chain_tc(const ChainStep* steps, int n_steps, float* ws, size_t ws_bytes, i
     if (st.kind == CHAIN_GEMM && !chain_tc_supported(st.M, st.N, st.K))
       throw std::runtime_error("chain: unsupported GEMM shape");
     if (st.kind == CHAIN_LN && !chain_ln_supported(st.ln_d)) throw std::runtime_error("chain: unsupported LN width");
-    if (st.kind == CHAIN_ATTN && (i != 0 || !chain_attn_supported(st.M, st.aP, st.aH, st.a_d / std::max(1, st.aH))))
+    if (st.kind == CHAIN_ATTN && !chain_attn_supported(st.M, st.aP, st.aH, st.a_d / std::max(1, st.aH)))
       throw std::runtime_error("chain: unsupported attention phase");
     M = std::max<int64_t>(M, st.M);
   }

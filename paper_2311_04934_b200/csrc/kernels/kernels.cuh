@@ -114,6 +114,7 @@ void gemm_tc(const void* A, const void* W_packed, int64_t M, int N, int K, const
 // One launch runs the phases in order with a grid barrier between them; the packed
 // weights of later phases stream in while earlier phases finish (chain_tc.cu).
 enum ChainKind : int { CHAIN_GEMM = 0, CHAIN_LN = 1, CHAIN_ATTN = 2 };
+constexpr int kChainMaxPhases = 48;  // phases per chain launch
 struct ChainStep {
   int kind = CHAIN_GEMM;
   int64_t M = 0;             // rows (tokens)
@@ -130,7 +131,7 @@ struct ChainStep {
   float* stats_out = nullptr;
   const float* stats_in = nullptr;
   int stats_tiles = 0, stats_ld = 0, stats_row0 = 0, ln_dim = 0;
-  // attention phase (CHAIN_ATTN; only as the first phase of a chain): M = n <= 128 new rows
+  // attention phase (CHAIN_ATTN; one request per launch, any position): M = n <= 128 new rows
   // of one request, causal against P cached rows; q / out [n][a_d], k / v the layer's cache
   // planes [P + n][a_d]; a_H heads of 128; a_scratch holds the split partials
   const void* aq = nullptr;

@@ -18,8 +18,9 @@ import paper_2311_04934_b200 as pcb  # noqa: E402
 
 L = pcb.lib()
 L.pcb_debug_chain_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_void_p]
-MAXL = 256
-times = np.zeros((MAXL, 8, 160, 16), np.uint64)
+MAXL = 64
+KMAX = 48  # kern::kChainMaxPhases
+times = np.zeros((MAXL, KMAX, 160, 16), np.uint64)
 phases = np.zeros(MAXL, np.int32)
 
 
@@ -84,7 +85,18 @@ prev_end = None
 for i in range(n):
     npn = int(phases[i])
     t = times[i, :npn, :148].astype(np.int64)  # [ph][cta][ev]
-    names = ["LN1", "QKV"] if npn == 2 else (["ATTN", "O", "W1", "W2", "QKV"] if npn == 5 else (names6 + ["?"] * 8)[:npn])
+    kinds = times[i, :npn, 159, 15].astype(np.int64) - 1  # 0 GEMM, 1 LN, 2 ATTN
+    names, after = [], None
+    for kd in kinds:
+        if kd == 1:
+            names.append("LN1")
+            after = 3
+        elif kd == 2:
+            names.append("ATTN")
+            after = 0
+        else:
+            names.append(["O", "W1", "W2", "QKV"][after] if after is not None and after < 4 else "GEMM")
+            after = (after + 1) if after is not None else None
     for ph in range(npn):
         ev = t[ph]
         act = ev[:, 2] > 0  # CTAs of the grid (a cluster launch uses fewer than 148)
@@ -131,7 +143,7 @@ for i in range(n):
                     row["o_after"] = np.median((ev[:, 2] - ev[:, 11])[ok8]) / 1e3
         first_done = t[0][:, 2]
         row["phase_span"] = (done.max() - (t[ph - 1][:, 2].max() if ph > 0 else first_done[first_done > 0].min())) / 1e3
-        agg.setdefault((npn, names[ph]), []).append(row)
+        agg.setdefault(names[ph], []).append(row)
     first = t[0][:, 0]
     first = first[first > 0]
     if prev_end is not None and len(first):
@@ -163,11 +175,12 @@ for key, rows in agg.items():
 if os.environ.get("TL_ATTN", "1") != "0":
     rows = []
     for i in range(n):
-        if int(phases[i]) != 5:
-            continue
-        ev = times[i, 0, :128].astype(np.int64)
-        t0 = ev[:, 0][ev[:, 0] > 0].min()
-        rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 4, 8, 5, 2)])
+        for ph in range(int(phases[i])):
+            if times[i, ph, 159, 15] != 3:
+                continue
+            ev = times[i, ph, :128].astype(np.int64)
+            t0 = ev[:, 0][ev[:, 0] > 0].min()
+            rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 4, 8, 5, 2)])
     if rows:
         a = np.array(rows)  # [chain][event][cta]
         print("ATTN per-CTA events (median over chains of the percentile), us: start / last PV / a_done / released / flags / done")

@@ -4,7 +4,8 @@
   PCB_LIB_PATH=ablib/base/libpcb200.so python tools/ttft_ab.py base
   python tools/ttft_ab.py new
 Prints one line: label, median / min TTFT (ms) and device ms per request over N requests
-of the configs[1] workload (7B shape, 4096 cached + 64 uncached).
+of the configs[1] workload (7B shape, 4096 cached + 64 uncached).  AB_OPTS=k=v,... sets model
+options (e.g. AB_OPTS=chain_group=1).
 """
 import os
 import statistics
@@ -24,6 +25,9 @@ s = pcb.Schema.parse(schema_text)
 st = pcb.ModuleStore(m)
 st.encode_schema(s)
 parsed = [pcb.Prompt.parse(p) for p in prompts]
+for kv in filter(None, os.environ.get("AB_OPTS", "").split(",")):  # model options, e.g. chain_group=1
+    k, v = kv.split("=")
+    m.set_option(k, int(v))
 for i in range(5):
     pcb.serve(st, s, parsed[i % 4], max_new_tokens=1)
 tt, dev = [], []
