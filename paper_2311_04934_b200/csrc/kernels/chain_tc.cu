@@ -385,20 +385,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               tma_prefetch(tk);
               tma_prefetch(tv);
             }
-            if (ph == 0) {
-              pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
-            } else {
-              // every weight stage issued so far has been consumed (the K/V stages overwrite
-              // the ring), then the grid barrier that publishes the QKV phase before
-              for (int k = 0; k < STAGES; ++k) mbar_wait(&empty[(it + k) % STAGES], (((it + k) / STAGES) & 1) ^ 1);
-              grid_wait(p, ph);
-              fence_proxy_async_global();
-            }
-            mbar_expect_tx(a_qfull, 32768);
-            for (int a = 0; a < 2; ++a)  // 64-row boxes: rows [0, 64) twice (dup) or [0, 128)
-              for (int hh = 0; hh < 2; ++hh)
-                tma_load_2d(aQ + a * 16384 + hh * 8192, &p.tma[0], a_qfull, h * 128 + a * 64, P.adup ? 0 : 64 * hh);
-            for (int j = 0, sg = 0; j < nb; ++j) {
+            auto load_kv = [&](int j, int& sg) {
               const int g = ab + j;  // block sequence over the launch's attention phases
               const int s = g % AKV;
               mbar_wait(&a_kvempty[s], ((g / AKV) & 1) ^ 1);
@@ -425,7 +412,29 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                   tma_load_2d(st + 16384 + a * 8192, tv, &a_kvfull[s], h * 128 + a * 64, b * 64);
                 }
               }
+            };
+            if (ph > 0)  // the K/V stages overwrite the ring: every weight stage issued so far consumed
+              for (int k = 0; k < STAGES; ++k) mbar_wait(&empty[(it + k) % STAGES], (((it + k) / STAGES) & 1) ^ 1);
+            // Blocks whose keys the phase before does not write -- cached-module segments read in
+            // place, or cache rows below P -- are loaded before waiting for it (no ALiBi: its key
+            // positions go through the LN scratch the phase before may still use)
+            int pre = 0, sg = 0;
+            if (!P.a_alibi) {
+              const int indep = P.a_nseg ? P.a_first[P.a_nseg - 1] : static_cast<int>(P.aP / 64);
+              pre = max(0, min(min(indep - b0, nb), AKV));
             }
+            for (int j = 0; j < pre; ++j) load_kv(j, sg);
+            if (ph == 0) {
+              pdl_wait();  // Q and the new K/V rows come from the previous chain's QKV phase
+            } else {
+              grid_wait(p, ph);  // ... or from this launch's QKV phase
+              fence_proxy_async_global();
+            }
+            mbar_expect_tx(a_qfull, 32768);
+            for (int a = 0; a < 2; ++a)  // 64-row boxes: rows [0, 64) twice (dup) or [0, 128)
+              for (int hh = 0; hh < 2; ++hh)
+                tma_load_2d(aQ + a * 16384 + hh * 8192, &p.tma[0], a_qfull, h * 128 + a * 64, P.adup ? 0 : 64 * hh);
+            for (int j = pre; j < nb; ++j) load_kv(j, sg);
             ab += nb;
             mbar_wait(a_done, an & 1);
           }
