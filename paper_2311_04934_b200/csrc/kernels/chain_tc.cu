@@ -771,13 +771,24 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         float2* pbml = reinterpret_cast<float2*>(pb + 64 * S::kPbLd);
         float* part = P.apart + (static_cast<int64_t>(c) * 128 + qi) * 128;
         float2* ml = reinterpret_cast<float2*>(P.apart + static_cast<int64_t>(P.items) * 128 * 128);
+        // a_done hands the ring to the W producer (the next phase's weights).  It is free once
+        // the last PV completed -- the dup halves combine in the exchange buffer (Q, parked
+        // there, is dead) -- except on the global-partials path, where a split CTA publishes
+        // its partial first (with the weight prefetch in flight its flag became visible ~2 us
+        // later, tools/chain_ab.py per-CTA attention events)
+        const bool merge = c < P.items && nparts > 1;
+        const bool early = (!merge || adsm) && (S::kPB > 0 || !dup);
         if (nb > 0) {
           mbar_wait(&a_pvdone[(ab + nb - 1) % 3], ((ab + nb - 1) / 3) & 1);
           tc_fence_after();
           ab += nb;
-          constexpr int kXld = 132;  // padded fp32 row
-          float* xo = reinterpret_cast<float*>(aKV);
-          float2* xml = reinterpret_cast<float2*>(aKV + 64 * kXld * 4);
+        }
+        if (early) mbar_arrive(a_done);
+        if (nb > 0) {
+          constexpr int kXld = 132;  // padded fp32 row (= S::kPbLd: a lane reads its dup partner's
+                                     // row, then parks its own result over it, in order)
+          float* xo = S::kPB > 0 ? pb : reinterpret_cast<float*>(aKV);
+          float2* xml = reinterpret_cast<float2*>(xo + 64 * kXld);
           float w0 = 1.f, w1 = 0.f;
           // tcgen05.ld is warp-collective: lane conditions only guard the memory operations
           if (dup) {
@@ -850,17 +861,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         }
         tc_fence_before();
         if (et == 0) ctl(p, ph, 4);
-        // a_done releases the W producer onto the ring (the next phase's weights).  A split
-        // CTA publishes its partial first: with the weight prefetch already in flight its
-        // flag became visible ~2 us later (tools/chain_ab.py, per-CTA attention events)
-        const bool merge = c < P.items && nparts > 1;
-        if (!merge) mbar_arrive(a_done);
+        if (!early && !merge) mbar_arrive(a_done);
         if (adsm) {
           // every epilogue thread releases its parked rows to the head's S CTAs, then the CTA
           // merges queries {sp, sp + S, ...} reading all S buffers (split order: deterministic)
           const int base = h * P.aS;
           pb_signal(pb_ready, base, nparts);
-          mbar_arrive(a_done);
+          if (!early) mbar_arrive(a_done);
           if (et == 0) ctl(p, ph, 8);
           pb_wait(pb_ready, pb_uses & 1);
           if (et == 0) ctl(p, ph, 5);
