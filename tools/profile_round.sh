@@ -13,15 +13,15 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_r
 # launch list of one full-depth cached request (after warm-up requests)
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $OUT/launches.csv python tools/prof_step.py > $OUT/launches.log 2>&1
-# full captures of the top kernels of the measured cached request (2 layers keep the replay
-# short).  Launch order: precompute (per-GEMM k_gemm_sk, 2 prefill attention), warm-up request
-# (3 chains -- attention is the first phase of the per-layer chains -- 1 assembly), measured
-# request -> skip counts below (the attention capture is the precompute's prefill kernel).
+# full captures of the top kernels (2 layers keep the replay short).  Launch order: the
+# module precompute (4096-token prefill: per-GEMM k_gemm_2sm, one k_attn_prefill per layer),
+# the warm-up request, then the measured request -- at 2 layers each request is ONE chain launch
+# ([LN1, QKV0, ATTN0, O, W1, W2, QKV1, ATTN1, O, W1, W2, unembed]); skip counts below.
 cap() {  # kernel-regex skip count
   PROF_LAYERS=2 PROF_WARM=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 \
     -o $OUT/full_$1 python tools/prof_step.py > $OUT/full_$1.log 2>&1
 }
-cap k_chain 3 3
-cap k_attn_tc 0 1
+cap k_chain 1 1
+cap k_attn_prefill 0 1
 PROF_ZC=0 cap k_assemble 1 1  # single requests read modules in place; the copy path is measured with it off
 ls -la $OUT

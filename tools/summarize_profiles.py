@@ -39,13 +39,14 @@ def ncu_metrics(rep, want):
     rows = list(csv.reader(out.splitlines()))
     if len(rows) < 3:
         return []
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
         d = {}
         for w in want:
             if w in hdr:
-                d[w] = r[hdr.index(w)]
+                u = units[hdr.index(w)]
+                d[w] = r[hdr.index(w)] + (f" {u}" if u and u not in ("%",) else "")
         res.append(d)
     return res
 
@@ -99,12 +100,12 @@ def main(tag):
             "lts__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
             "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active"]
-    for kern in ("k_chain", "k_gemm_sk", "k_attn_tc", "k_assemble"):
+    for kern in ("k_chain", "k_gemm_sk", "k_attn_tc", "k_attn_prefill", "k_assemble"):
         rep = os.path.join(src, f"full_{kern}.ncu-rep")
         if not os.path.exists(rep):
             continue
         ms = ncu_metrics(rep, want)
-        lines += ["", f"## ncu --set full: {kern} ({len(ms)} launches of the measured request)", ""]
+        lines += ["", f"## ncu --set full: {kern} ({len(ms)} launch(es) captured)", ""]
         if ms:
             cols = [c for c in want if c in ms[0] and c != "Kernel Name"]
             lines.append("| " + " | ".join(cols) + " |")
