@@ -127,10 +127,15 @@ def test_hd128_corpus_matches_reference(parity, host_golden):
 # ---------------------------------------------------------------------------
 # configs[2] shape: 3 modules, 16,384 cached rows + 128 uncached
 # ---------------------------------------------------------------------------
-def test_long_context_matches_reference(parity):
+@pytest.mark.parametrize("pair", [1, 2])
+def test_long_context_matches_reference(parity, pair):
+    """pair 2: the module precompute runs the paired-tile prefill attention (attn_prefill.cu;
+    at this width -- 2 heads -- it would not fill the GPU, so auto mode picks the single-tile
+    kernel)."""
     g = parity["long"]
     schema_text, prompt_text = pc.long_workload()
     m = pcb.Model(pc.H128_LONG, dtype=pcb.BF16)
+    m.set_option("attn_pair", pair)
     schema = pcb.Schema.parse(schema_text)
     store = pcb.ModuleStore(m)
     assert store.encode_schema(schema) == 3
@@ -146,8 +151,8 @@ def test_long_context_matches_reference(parity):
         r = pcb.serve(store, schema, prompt_text, 4)
         assert r.cache_report["cached_token_count"] == 16384
         assert r.cache_report["uncached_token_count"] == 128
-        check_bf16(r.first_token_logits, f32(g["logits"]), f"long zc={zc}")
-        record_sequence(r.output_tokens, g["tokens"], f"long zc={zc}")
+        check_bf16(r.first_token_logits, f32(g["logits"]), f"long pair={pair} zc={zc}")
+        record_sequence(r.output_tokens, g["tokens"], f"long pair={pair} zc={zc}")
     m.set_option("zero_copy", 1)
 
 
