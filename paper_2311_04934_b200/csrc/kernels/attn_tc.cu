@@ -4,16 +4,17 @@
 //
 //   warp 0     TMA: Q tile once, then K/V blocks of 64 keys (ring as deep as smem allows)
 //   warp 1     TMEM alloc + MMA issue: S_j = Q K_j^T (M=128, N=64, K=hd) into one of
-//              two TMEM score buffers, O += P_j V_j (M=128, N=hd, K=64; V is an
-//              MN-major operand) accumulated in TMEM across all blocks
+//              three TMEM score buffers, O += P_j V_j (M=128, N=hd, K=64; P is the A
+//              operand straight from TMEM, V an MN-major smem operand) accumulated in TMEM
 //   warps 2-5  softmax: one thread per query row (TMEM lane); online max/sum in
-//              fp32, P_j -> swizzled smem (bf16)
-// Pipelining: QK^T of block j+1 runs while the softmax of block j executes (two
-// score buffers).  The running max is rescaled lazily: O (in TMEM) is corrected
-// only when a row's max grows by more than 2^8, so the common step never touches O.
-// Suffix prefill (few queries, long cache) splits the key range across CTAs so all
-// SMs stream the KV; a combine kernel merges the (O, m, l) partials in split order
-// (deterministic).  Prefill (P = 0) tiles queries and skips blocks above the diagonal.
+//              fp32, P_j (bf16) written back over the first 32 columns of S_j
+// Pipelining: S(j+2) is issued right after PV(j), so the scores of block j+1 are ready
+// when the softmax of block j ends.  The running max is rescaled lazily: O (in TMEM) is
+// corrected only when a row's max grows by more than 2^8, so the common step never touches O.
+// Suffix prefill (few queries, long cache) splits the key range across the CTAs of a
+// cluster and merges the (O, m, l) partials through DSMEM in split order (deterministic).
+// Prefill (P = 0) tiles queries and skips blocks above the diagonal; long prefills use the
+// paired-tile kernel (attn_prefill.cu).
 #include <cuda.h>
 
 #include "common.cuh"
@@ -40,14 +41,15 @@ struct AttnSmem {
   static constexpr int kQ = BQ * HD * 2;
   static constexpr int kKV = BKV * HD * 2;
   static constexpr int kStage = 2 * kKV;  // K + V
-  static constexpr int kP = BQ * BKV * 2;  // one P buffer (two are used)
   static constexpr int kPos = AL ? BKV * 4 : 0;  // ALiBi: the stage's key positions (int32)
-  // as many K/V stages as fit next to Q and the two P buffers (a stage is held from its
-  // TMA load through the PV MMA, so depth is what keeps HBM busy on long caches)
-  static constexpr int kStagesFit = (kSmemMax - kQ - 2 * kP - 2048) / (kStage + kPos);
+  // as many K/V stages as fit next to Q (a stage is held from its TMA load through the PV
+  // MMA, so depth is what keeps HBM busy on long caches); P lives in TMEM
+  static constexpr int kStagesFit = (kSmemMax - kQ - 2048) / (kStage + kPos);
   static constexpr int kStages = kStagesFit > PCB_ATTN_STAGES ? PCB_ATTN_STAGES : kStagesFit;
-  static constexpr int kBytes = kQ + kStages * (kStage + kPos) + 2 * kP + 1024 + 1024;
-  static constexpr uint32_t kTmemCols = 2 * BKV + HD <= 256 ? 256 : 512;
+  static constexpr int kBytes = kQ + kStages * (kStage + kPos) + 1024 + 1024;
+  // three 64-column score buffers (P written back over the first 32 columns of its buffer)
+  // and O: 3 BKV + HD columns
+  static constexpr uint32_t kTmemCols = 3 * BKV + HD <= 256 ? 256 : 512;
 };
 
 struct AttnParams {
@@ -112,6 +114,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const float* v) {
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16u(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) = +0
   float y;
@@ -131,20 +141,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + S::kQ;
-  uint8_t* sP = sKV + KV_STAGES * S::kStage;
-  int32_t* sPos = reinterpret_cast<int32_t*>(sP + 2 * S::kP);  // [KV_STAGES][BKV] (ALiBi)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * S::kP + KV_STAGES * S::kPos);
+  int32_t* sPos = reinterpret_cast<int32_t*>(sKV + KV_STAGES * S::kStage);  // [KV_STAGES][BKV] (ALiBi)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + KV_STAGES * S::kStage + KV_STAGES * S::kPos);
   uint64_t* q_full = bar;
   uint64_t* kv_full = bar + 1;                // [KV_STAGES]
   uint64_t* kv_empty = kv_full + KV_STAGES;   // [KV_STAGES]
-  uint64_t* s_full = kv_empty + KV_STAGES;    // [2] score buffer b holds blocks it with it&1 == b
-  // [2] P(it) of blocks it with it&1 == b in smem.  Two barriers, not one: with a single
-  // p_full the softmax could complete the phase of block it+1 (S(it+1) is already issued and
-  // its P buffer free) before the MMA thread observed block it's phase -- two completions
-  // restore the parity the MMA waits on and it sleeps forever (seen in the chain version)
-  uint64_t* p_full = s_full + 2;
-  uint64_t* pv_done = p_full + 2;             // [2] PV of blocks it with it&1 == b completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  // Score buffer b (of 3) holds blocks it with it % 3 == b; P(it) is written back over the first
+  // 32 columns of S(it) and read from TMEM by the PV MMA.  S(it + 2) is issued right after
+  // PV(it), so S(it + 1) is ready when the softmax of block it ends.  One p_full per buffer:
+  // with a single barrier the softmax could complete block it+1's phase before the MMA thread
+  // observed block it's, and two completions restore the parity it waits on (a hang seen in
+  // the chain version).
+  uint64_t* s_full = kv_empty + KV_STAGES;  // [3] S(it) in TMEM, phase (it / 3) & 1
+  uint64_t* p_full = s_full + 3;            // [3] P(it) in TMEM (128 arrivals)
+  uint64_t* pv_done = p_full + 3;           // [3] PV(it) completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tlm(p, 0);  // entry
@@ -192,12 +203,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
-    mbar_init(&p_full[0], 128);
-    mbar_init(&p_full[1], 128);
-    mbar_init(&pv_done[0], 1);
-    mbar_init(&pv_done[1], 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&pv_done[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, S::kTmemCols);
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 2 * BKV;  // S buffers at columns [0, 64) and [64, 128)
+  const uint32_t tO = tmem + 3 * BKV;  // S buffers at columns [0, 64), [64, 128), [128, 192)
   // No early trigger: a GEMM / chain launched programmatically after this kernel was
   // seen to deadlock with it (the dependent's CTAs resident and waiting in
   // griddepcontrol.wait while the attention grid never completed -- tools/pdl_bisect2.sh,
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (elect_one() && nb > 0) {
       constexpr uint32_t idS = idesc_bf16(BQ, BKV);
       constexpr uint32_t idO = idesc_bf16(BQ, HD, false, true);  // V is MN-major
-      const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
+      const uint32_t q_addr = smem_u32(sQ);
       mbar_wait(q_full, 0);
       auto issue_qk = [&](int it) {
         const int s = it % KV_STAGES;
@@ -277,32 +287,32 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         probe(p, 5, it);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sKV + s * S::kStage);
-        const uint32_t tS = tmem + (it & 1) * BKV;
+        const uint32_t tS = tmem + (it % 3) * BKV;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const int a = k >> 2, kk = k & 3;
           umma_bf16(tS, sw128_kmajor_desc(q_addr + a * (BQ * 128) + kk * 32),
                     sw128_kmajor_desc(k_addr + a * (BKV * 128) + kk * 32), idS, k > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[it & 1]);
+        umma_commit(&s_full[it % 3]);
       };
       issue_qk(0);
+      if (nb > 1) issue_qk(1);
       for (int it = 0; it < nb; ++it) {
-        // S(it+1) goes to the other buffer; its previous content S(it-1) was consumed
-        // before p_full(it-1), which the previous iteration waited for.
-        if (it + 1 < nb) issue_qk(it + 1);
-        mbar_wait(&p_full[it & 1], (it >> 1) & 1);  // P(it) in smem (and any O correction done)
+        mbar_wait(&p_full[it % 3], (it / 3) & 1);  // P(it) in TMEM (and any O correction done)
         probe(p, 2, it);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sKV + (it % KV_STAGES) * S::kStage + S::kKV);
-        const uint32_t pb = p_addr + (it & 1) * S::kP;
+        const uint32_t pt = tmem + (it % 3) * BKV;  // P(it): A operand from TMEM
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16(tO, sw128_kmajor_desc(pb + k * 32), sw128_mnmajor_desc(v_addr + k * 2048, BKV * 128, 1024),
-                    idO, (it > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&pv_done[it & 1]);
+          umma_bf16_ts(tO, pt + k * 8, sw128_mnmajor_desc(v_addr + k * 2048, BKV * 128, 1024), idO,
+                       (it > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&pv_done[it % 3]);
         umma_commit(&kv_empty[it % KV_STAGES]);
         probe(p, 3, it);
+        // S(it + 2) into the buffer of P(it - 1), whose PV was issued an iteration ago
+        if (it + 2 < nb) issue_qk(it + 2);
       }
       tlm(p, 3);  // last PV issued
     }
@@ -341,19 +351,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         j0 += c0;  // first key of this lane's columns
         if (!live) {
-          // p_full[it&1]'s previous phase (block it-2) completed before PV(it-2) was issued
-          if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
-          mbar_arrive(&p_full[it & 1]);
+          // S(it) was issued after p_full(it - 2) completed: arriving after it keeps this warp
+          // out of block it - 3's phase of the same barrier
+          mbar_wait(&s_full[it % 3], (it / 3) & 1);
+          mbar_arrive(&p_full[it % 3]);
           continue;
         }
-        mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+        mbar_wait(&s_full[it % 3], (it / 3) & 1);
         if (threadIdx.x == 128) probe(p, 0, it);
         tc_fence_after();
         float sv[NC];
         {
           uint32_t raw[NC];
 #pragma unroll
-          for (int c = 0; c < NC; c += 16) tmem_ld16_nowait(tmem + (it & 1) * BKV + lane_off + c0 + c, raw + c);
+          for (int c = 0; c < NC; c += 16) tmem_ld16_nowait(tmem + (it % 3) * BKV + lane_off + c0 + c, raw + c);
           tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < NC; ++c) sv[c] = __uint_as_float(raw[c]);
@@ -394,7 +405,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const bool grow = bm > m + kRescaleThreshold / p.scale_log2 || (m == -INFINITY && bm > -INFINITY);
         if (__any_sync(0xffffffffu, grow) && it > 0) {
           // O holds blocks < it: wait for PV(it-1), then scale the rows that grow
-          mbar_wait(&pv_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
+          mbar_wait(&pv_done[(it - 1) % 3], ((it - 1) / 3) & 1);
           tc_fence_after();
           const float f = grow ? fast_exp2((m - bm) * p.scale_log2) : 1.f;  // m = -inf -> 0
 #pragma unroll 1
@@ -424,31 +435,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         l += (bs[0] + bs[1]) + (bs[2] + bs[3]);
         if (threadIdx.x == 128) probe(p, 7, it);
-        // P buffer it&1 is free once PV(it-2) completed
-        if (it > 1) mbar_wait(&pv_done[it & 1], ((it - 2) >> 1) & 1);
-        if (threadIdx.x == 128) probe(p, 8, it);
-        // P row (64 keys, SW128): this lane's columns; dup: zeros in the other half
-        uint8_t* prow = sP + (it & 1) * S::kP + r * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {  // 16-byte chunk c holds columns [8c, 8c + 8)
-          const int k = c & (NC / 8 - 1);
-          const bool mine = NC == 64 || (c >> 2) == (r >> 6);
-          const uint4 v = mine ? make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3])
-                               : make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = v;
+        // P row (64 keys) into TMEM over the first 32 columns of its score buffer; dup: this
+        // lane's half of the keys, zeros in the other half
+        {
+          const uint32_t pa = tmem + (it % 3) * BKV + lane_off;
+          if constexpr (NC == 64) {
+            tmem_st16u(pa, packed);
+            tmem_st16u(pa + 16, packed + 16);
+          } else {
+            const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            tmem_st16u(pa + 16 * (r >> 6), packed);
+            tmem_st16u(pa + 16 * (1 - (r >> 6)), z);
+          }
+          tmem_st_wait();
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (threadIdx.x == 128) probe(p, 8, it);
         tc_fence_before();
-        // a fast warp must not arrive for block it while block it-1's phase is still
-        // collecting arrivals (its arrival would complete that phase early)
-        mbar_arrive(&p_full[it & 1]);  // the P-buffer wait above ordered it after block it-2's phase
+        mbar_arrive(&p_full[it % 3]);  // after block it-3's phase: S(it) needed p_full(it-2)
         if (threadIdx.x == 128) probe(p, 1, it);
       }
     };
     if (dup) blocks(std::integral_constant<int, 32>{});
     else blocks(std::integral_constant<int, BKV>{});
     if (nb > 0) {
-      mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+      mbar_wait(&pv_done[(nb - 1) % 3], ((nb - 1) / 3) & 1);
       tc_fence_after();
       if (p.splits == 1) {
         // dup: lane r + 64 holds query r's other half-keys partial; it parks (O, m, l) in the
