@@ -96,8 +96,11 @@ void pcb_model_destroy(pcb_model* m);
 /* Options (value 0/1 unless noted): "profile" (per-kernel-class CUDA-event timing),
  * "force_simt" / "force_simt_gemm" / "force_simt_attn" (testing: SIMT kernels only),
  * "chain" (few-token forwards as persistent chain kernels), "ln_fold" (LayerNorm folded into
- * the chain's GEMMs), "chain_attn" (a single request's attention as the chain's first phase),
- * "zero_copy" (serve / serve_batch read cached modules in place instead of the concat_kv copy).
+ * the chain's GEMMs), "chain_attn" (a single request's attention as a chain phase),
+ * "chain_group" (layers per chain launch when the attention is a chain phase, default 9;
+ * 1 = one launch per layer), "zero_copy" (serve / serve_batch read cached modules in place
+ * instead of the concat_kv copy), "attn_pair" (paired-tile prefill attention: 0 off, 1 when
+ * it fills the GPU (default), 2 whenever it applies).
  * Returns PCB_ERR_INVALID_CONFIG for an unknown key. */
 int pcb_model_set_option(pcb_model* m, const char* key, int64_t value);
 int pcb_model_weight_checksum(pcb_model* m, const char* tensor, uint64_t* out);
