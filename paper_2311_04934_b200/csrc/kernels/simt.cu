@@ -230,10 +230,17 @@ __global__ void __launch_bounds__(kLnThreads) k_layernorm(const float* h, int d,
   for (int u = 0; u < kLnVec; ++u) {
     const int i = threadIdx.x + u * kLnThreads;
     if (i < nv) {
-      st_f(orow, 4 * i + 0, static_cast<float>((x[u].x - mean) * inv));
-      st_f(orow, 4 * i + 1, static_cast<float>((x[u].y - mean) * inv));
-      st_f(orow, 4 * i + 2, static_cast<float>((x[u].z - mean) * inv));
-      st_f(orow, 4 * i + 3, static_cast<float>((x[u].w - mean) * inv));
+      const float a = static_cast<float>((x[u].x - mean) * inv), b = static_cast<float>((x[u].y - mean) * inv);
+      const float c = static_cast<float>((x[u].z - mean) * inv), e = static_cast<float>((x[u].w - mean) * inv);
+      if constexpr (std::is_same_v<T, float>) {  // one 16-byte store per 4 elements
+        reinterpret_cast<float4*>(orow)[i] = make_float4(a, b, c, e);
+      } else {  // bf16: one 8-byte store (2-byte stores left the kernel at ~2.2 TB/s)
+        __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, e);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(orow)[i] = pk;
+      }
     }
   }
 }
