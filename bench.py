@@ -432,13 +432,17 @@ def run_c5(a) -> None:
     tokens (64 x 1024 = 172 GB of KV + 130 GB of weights: more than one GPU's HBM), head-sharded over
     all ranks (tensor parallel, NCCL all-reduce after Wo and W2); one request = 4 modules (4096 cached
     rows) + 64 uncached tokens served by all ranks together (strong scaling)."""
-    D = Dist()
+    # --share-device: every rank on GPU 0 (the head-sharded path as separate processes on a
+    # one-GPU box; peer-memory transport, gloo for the timing plumbing)
+    D = Dist(backend="gloo" if a.share_device else "nccl")
+    if a.share_device:
+        D.local = 0
     import paper_2311_04934_b200 as pcb
 
     n_mod = a.c5_modules
     cfg = dict(n_layers=a.c5_layers, n_heads=64, head_dim=128, hidden=8192, vocab_size=32000, pos_encoding="rope",
                max_position=n_mod * 1024 + 256, bytes_per_element=2, seed=42)
-    if D.world > 1 and a.tp_transport == "peer":  # CUDA-IPC peer memory, one-shot collectives
+    if D.world > 1 and (a.tp_transport == "peer" or a.share_device):  # CUDA-IPC peer memory, one-shot collectives
         peer = pcb.peer_group(D.dist, device=D.local, cap_floats=1024 * cfg["hidden"])
         model = pcb.Model(cfg, dtype=pcb.BF16, peer=peer)
     else:
@@ -462,6 +466,7 @@ def run_c5(a) -> None:
         r = pcb.serve(store, schema, parsed[i % len(parsed)], max_new_tokens=1)
         ttfts.append(r.timings["ttft_us"] / 1e3)
     region_ms = D.max(model.timer_stop())
+    ttft_ms = D.max(statistics.mean(ttfts))  # every rank joins the reduction
     if D.rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": a.steps / (region_ms / 1e3), "unit": "requests/s", "n_gpus": D.world,
@@ -471,9 +476,10 @@ def run_c5(a) -> None:
                     "seeded PCG32 streams, sharded by rank)",
             "config": {"workload": f"configs[4]: Llama-2-70B shape ({a.c5_layers} layers), {n_mod} x 1024-token "
                                    "module store head-sharded, 4 modules (4096 cached) + 64 uncached per request",
-                       "parallelism": f"tp{D.world}", "tp_transport": a.tp_transport if D.world > 1 else None,
+                       "parallelism": f"tp{D.world}", "tp_transport": ("peer" if a.share_device else a.tp_transport)
+                       if D.world > 1 else None, "ranks_share_one_gpu": bool(a.share_device),
                        "cached_tokens": 4096, "uncached_tokens": 64},
-            "ttft_ms": D.max(statistics.mean(ttfts)), "precompute_s": precompute_s,
+            "ttft_ms": ttft_ms, "precompute_s": precompute_s,
             "store_gb_per_gpu": n_mod * 1024 * 2 * a.c5_layers * 8192 * 2 / D.world / 1e9}), flush=True)
     D.close()
 
@@ -781,6 +787,7 @@ def main():
     ap.add_argument("--c5-layers", type=int, default=80)
     ap.add_argument("--c5-modules", type=int, default=64)
     ap.add_argument("--tp-transport", default="nccl", choices=["nccl", "peer"])
+    ap.add_argument("--share-device", action="store_true", help="c5: all ranks on GPU 0 (peer transport)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--skip-batch", action="store_true")
