@@ -60,8 +60,6 @@ struct AttnParams {
   __nv_bfloat16* out;
   float* part_o;   // [H][splits][BQ][HD]
   float* part_ml;  // [H][splits][BQ][2]
-  int kv_head_major;
-  int64_t kv_rows;  // rows per head plane (head-major layout)
   int* counters;    // [H] split arrival counters (zero between launches)
   // batched requests (one launch for a micro-batch): blockIdx.x = request, per request
   // {first q row, n, P}; K/V come from a 3-D tensor map {d, rows, request}
@@ -249,8 +247,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               : "memory");
         // head-interleaved cache [rows][H*hd]: x = h*hd + a*64, y = key row;
         // head-major cache [H][rows][hd]:     x = a*64,        y = h*rows + key row
-        const int kx = p.kv_head_major ? 0 : h * HD;
-        const int ky = p.kv_head_major ? static_cast<int>(h * p.kv_rows + j0) : j0;
+        const int kx = h * HD, ky = j0;
         if (p.segs) {
           const int b = static_cast<int>(b0) + it;
           while (b >= seg_first[sg + 1]) ++sg;
@@ -694,9 +691,6 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
   CUtensorMap tq = tmap_bf16_2d(a.q, static_cast<uint64_t>(a.n), static_cast<uint64_t>(a.d), 64);  // 64-row boxes
   static const bool nodup = std::getenv("PCB_ATTN_NODUP") != nullptr;  // A/B switch
   p.dup = batched && a.max_n <= 64 && splits == 1 && !nodup ? 1 : 0;
-  static const bool hm_probe = std::getenv("PCB_ATTN_HM_PROBE") != nullptr;  // timing probe (values meaningless)
-  p.kv_head_major = hm_probe ? 1 : 0;
-  p.kv_rows = p.total;
   static const bool tl_on = std::getenv("PCB_ATTN_TL") != nullptr;
   if (tl_on) {  // per-CTA phase timeline of the LAST launch (attn_tl_dump)
     if (!g_tlbuf) PCB_CUDA(cudaMalloc(&g_tlbuf, 8192 * 8 * sizeof(unsigned long long)));
@@ -725,10 +719,8 @@ void launch_attn(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaSt
     tk = tmap_bf16_3d(a.k, a.d, a.kv_cap, a.n_req, a.req_stride, BKV);
     tv = tmap_bf16_3d(a.v, a.d, a.kv_cap, a.n_req, a.req_stride, BKV);
   } else {
-    tk = p.kv_head_major ? tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
-                         : tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
-    tv = p.kv_head_major ? tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total) * a.H, static_cast<uint64_t>(HD), BKV)
-                         : tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+    tk = tmap_bf16_2d(a.k, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
+    tv = tmap_bf16_2d(a.v, static_cast<uint64_t>(p.total), static_cast<uint64_t>(a.d), BKV);
   }
   dim3 grid(q_tiles, a.H, splits);
   PdlClass pc(PDL_ATTN);

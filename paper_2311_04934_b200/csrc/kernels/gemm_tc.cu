@@ -115,7 +115,6 @@ struct SkArgs {
   int epoch;
   float* ws;  // [gridDim.x][128][BN] partial tiles
   int* flags; // [gridDim.x] epoch flags
-  const uint8_t* x_bulk_probe = nullptr;
   unsigned long long* tl = nullptr;  // timeline probe: [cta][4] globaltimer ns (PCB_GEMM_PROBE)
 };
 
@@ -203,11 +202,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         bulk_load(st, w_src(g), kWTile, &full[s], pol_w);
         int kx, my;
         x_coords(g, kx, my);
-        if (a.x_bulk_probe)  // timing probe: activation tile as one bulk copy (values meaningless)
-          bulk_load(st + kWTile, a.x_bulk_probe + (static_cast<int64_t>(kx) / 64 * a.m_tiles + my / BN) * (BN * 128),
-                    BN * 128, &full[s], pol_x);
-        else
-          tma_load_2d_hint(st + kWTile, &tmX, &full[s], kx, my, pol_x);
+        tma_load_2d_hint(st + kWTile, &tmX, &full[s], kx, my, pol_x);
       }
     }
   } else if (warp == 1) {
@@ -392,7 +387,6 @@ static void launch_sk(const void* A, const void* Wp, int64_t M, int N, int K, co
   a.ws = ws;
   a.flags = flags;
   a.epoch = ++g_sk_epoch;
-  if (std::getenv("PCB_GEMM_XBULK_PROBE")) a.x_bulk_probe = static_cast<const uint8_t*>(A);
   int C = static_cast<int>(std::min<int64_t>(sms, a.units));
   static const int ctas_env = [] {  // tuning override (environment read once)
     const char* v = std::getenv("PCB_GEMM_CTAS");
