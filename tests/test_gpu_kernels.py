@@ -127,16 +127,21 @@ def test_chain_and_ln_fold_full_depth():
     store.encode_schema(schema)
     prompt = '<prompt schema="deep"><doc/>' + ("Summarise the document above briefly " * 2)[:64] + '</prompt>'
     out = {}
+    # chain_group: layers per chain launch (default 9: 4 launches for 32 layers; 1: one per layer;
+    # 4: 8 launches) -- the same phases in the same order, so bit-identical logits
     for name, opts in (("fold", {"chain": 1, "ln_fold": 1}), ("ln", {"chain": 1, "ln_fold": 0}),
-                       ("kernels", {"chain": 0})):
+                       ("kernels", {"chain": 0}), ("group1", {"chain": 1, "ln_fold": 1, "chain_group": 1}),
+                       ("group4", {"chain": 1, "ln_fold": 1, "chain_group": 4})):
         for k, v in opts.items():
             m.set_option(k, v)
         out[name] = pcb.serve(store, schema, prompt, 1).first_token_logits
+        m.set_option("chain_group", 9)
     m.set_option("chain", 1)
     m.set_option("ln_fold", 1)
     for other in ("ln", "kernels"):
         assert rel(out["fold"], out[other]) <= BF16_REL
         assert same_greedy_token(out["fold"], out[other])
+    assert np.array_equal(out["fold"], out["group1"]) and np.array_equal(out["fold"], out["group4"])
 
 
 @pytest.mark.parametrize("doc_len,suffix", [(4096, 64), (700, 128), (37, 1), (0, 40), (130, 120)])
