@@ -774,6 +774,14 @@ void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaS
     attention_prefill(a, s);
     return;
   }
+  static const bool batch_off = [] {  // A/B switch: PCB_ATTN_BATCH=0 keeps one CTA per (request, head)
+    const char* v = std::getenv("PCB_ATTN_BATCH");
+    return v && v[0] == '0';
+  }();
+  if (!batch_off && attention_batch_supported(a)) {
+    attention_batch(a, s);
+    return;
+  }
   if (a.alibi) {
     if (a.hd == 128) launch_attn<128, true>(a, scratch, scratch_bytes, s);
     else launch_attn<64, true>(a, scratch, scratch_bytes, s);

@@ -221,6 +221,9 @@ bool attention_tc_supported(const AttnArgs& a);
 void attention_tc(const AttnArgs& a, float* scratch, size_t scratch_bytes, cudaStream_t s);
 // causal prefill over long query ranges (hd 128): two 128-query tiles per CTA (attn_prefill.cu)
 bool attention_prefill_supported(const AttnArgs& a, int sms);
+// micro-batched suffix attention (<= 64 rows per request, hd 128): persistent over (request, head)
+bool attention_batch_supported(const AttnArgs& a);
+void attention_batch(const AttnArgs& a, cudaStream_t s);
 void attention_prefill(const AttnArgs& a, cudaStream_t s);
 int attn_tl_dump(unsigned long long* out, int max_ctas);  // debug: last launch's per-CTA phases (PCB_ATTN_TL)
 
