@@ -1,14 +1,17 @@
 // Persistent chain of weight-streaming GEMM and LayerNorm phases for the few-token
-// (suffix prefill / decode) regime, one launch per transformer-layer segment:
+// (suffix prefill / decode) regime.  A launch runs the phases of up to 9 transformer layers:
 //
-//   [attention_l, O_l (+resid), LN2_l, W1_l (+GELU), W2_l (+resid), LN1_{l+1}, QKV_{l+1} (+RoPE, K/V -> cache)]
+//   [LN1_0, QKV_0] then per layer [attention_l, O_l (+resid), W1_l (+GELU), W2_l (+resid), QKV_{l+1}]
 //
-// (reference Model::run, model.cpp:376-436).  The attention phase (one request, hd 128)
-// runs the attn_tc.cu pipeline on the ring's shared memory -- TMA Q and K/V blocks, QK^T
-// and PV on tcgen05 with S / O in TMEM, online softmax on the epilogue warps -- over
-// (head, key split) items, and merges the split partials through global memory; each
-// CTA hands the ring back to the weight stream as soon as its own item is done.  (As a
-// separate kernel it cost a launch, a prologue and the next chain's cold start per layer.)
+// with LayerNorm folded into the neighbouring GEMMs (LN phases when the fold is off; the
+// last layer ends with the unembedding), reference Model::run, model.cpp:376-436.  An
+// attention phase (one request, hd 128) runs the attn_tc.cu pipeline on the ring's shared
+// memory -- TMA Q and K/V blocks, QK^T and PV on tcgen05 with S, P and O in TMEM, online
+// softmax on the epilogue warps -- over (head, key split) items whose partials merge through
+// the cluster's DSMEM; each CTA hands the ring back to the weight stream as soon as its own
+// item is done, and the cached modules' K/V blocks load before the grid barrier that
+// publishes the phase's Q.  (As a separate kernel, and with one launch per layer, each layer
+// paid a launch, a prologue and a cold start.)
 // At 64 tokens every GEMM is HBM-bound on its weights, and as separate
 // launches each one paid a ramp (launch, prologue, first weight bytes) and a drain
 // (stream-K fix-up, epilogue, the slowest CTA) during which HBM idles: the measured
