@@ -17,7 +17,7 @@ def pytest_configure(config):
 
 def pytest_terminal_summary(terminalreporter, exitstatus, config):
     """Greedy-token parity accounting (report how many cases used the tie exemption)."""
-    from tests.util import GREEDY, SEQ
+    from tests.util import GREEDY, RELS, SEQ
 
     if not GREEDY["checked"] and not SEQ["checked"]:
         return
@@ -32,6 +32,10 @@ def pytest_terminal_summary(terminalreporter, exitstatus, config):
                       f"{len(SEQ['diverged'])}")
         for e in SEQ["diverged"][:20]:
             tr.write_line(f"  {e}")
+    if RELS:
+        tr.write_line("bf16 logits rel-err vs the reference at Llama-2-7B width (bar 2e-2):")
+        for k, v in RELS.items():
+            tr.write_line(f"  {k}: {v:.2e}")
 
 
 def _ensure_built():

@@ -93,6 +93,31 @@ def job_w7b_request(i, alibi=False):
                                                    "row0": logits[0], "last": logits[-1]}
 
 
+def job_w7b_full(_):
+    """configs[1]'s model at full depth (32 layers): Model::forward of request 0's 64 suffix
+    tokens over doc0 + doc1 (4096 synthetic cached rows).  ~30 GB of host memory and ~10 min
+    of one core: run alone (`python tests/golden/make_golden_parity.py full`)."""
+    m = RefModel(pc.W7B_FULL)
+    res = Ref.resolve(pc.W7B_SCHEMA, pc.W7B_PROMPTS[0])
+    toks = [t for u in res["uncached"] for t in u["seg"]["tokens"]]
+    pos = [q for u in res["uncached"] for q in u["seg"]["positions"]]
+    ks, vs, ps = [], [], []
+    for name in res["cached_imports"]:
+        k, v, p = pc.w7b_full_module_kv(int(name[3:]))
+        ks.append(k)
+        vs.append(v)
+        ps.append(p)
+    k = np.concatenate(ks, axis=1)
+    del ks
+    v = np.concatenate(vs, axis=1)
+    del vs
+    past = ref_kv(k, v, np.concatenate(ps))
+    del k, v
+    logits, _ = m.forward(toks, pos, past=past)
+    return "full0", {"tokens": np.array(toks, np.int32), "positions": np.array(pos, np.int64),
+                     "row0": logits[0], "last": logits[-1]}
+
+
 def job_w7b_alibi(i):
     return job_w7b_request(i, alibi=True)
 
@@ -123,6 +148,7 @@ JOBS = {
     "long": [(job_long, 0)], "h128": [(job_h128, 0)], "c1": [(job_c1, 0)],
     # ALiBi on the tensor-core paths: head-dim-128 corpus, 7B-width suffixes
     "h128_alibi": [(job_h128, 1)], "alibi_requests": [(job_w7b_alibi, i) for i in (0, 1)],
+    "full": [(job_w7b_full, 0)],
 }
 
 
@@ -140,7 +166,7 @@ def main(groups):
     with open(jpath, "w") as f:
         json.dump(parity, f, separators=(",", ":"))
     flat = dict(np.load(npath)) if os.path.exists(npath) else {}
-    for key in [k for k in results if "req" in k or k == "prefill"]:
+    for key in [k for k in results if "req" in k or k in ("prefill", "full0")]:
         for name, arr in results[key].items():
             flat[f"{key}_{name}"] = arr
     np.savez(npath, **flat)
@@ -148,4 +174,4 @@ def main(groups):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or list(JOBS))
+    main(sys.argv[1:] or [g for g in JOBS if g != "full"])

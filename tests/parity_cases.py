@@ -80,5 +80,20 @@ def w7b_module_kv(i: int):
     return k, v, pos
 
 
+# the benchmarked depth: Llama-2-7B shape at all 32 layers (configs[1]'s model), one request of
+# 4096 cached rows (doc0 + doc1, synthetic bf16-exact K/V) + 64 uncached tokens
+W7B_FULL = dict(W7B, n_layers=32)
+
+
+def w7b_full_module_kv(i: int):
+    """Synthetic K/V [32][rows][hidden] of module doc{i} for the full-depth case."""
+    L, d = W7B_FULL["n_layers"], W7B_FULL["hidden"]
+    g = np.random.default_rng(20251117 + i)
+    k = bf16_round(g.uniform(-4.0, 4.0, (L, W7B_MOD_ROWS, d)).astype(np.float32))
+    v = bf16_round(g.uniform(-1.0, 1.0, (L, W7B_MOD_ROWS, d)).astype(np.float32))
+    pos = np.arange(i * W7B_MOD_ROWS, (i + 1) * W7B_MOD_ROWS, dtype=np.int64)
+    return k, v, pos
+
+
 def w7b_prefill_tokens():
     return [ord(c) for c in synthetic_text(W7B_PREFILL, 4242)]

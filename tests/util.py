@@ -11,6 +11,9 @@ BF16_REL = 2e-2  # north star: bf16 path logits rel-err <= 2e-2 (max |a-b| / max
 GREEDY = {"checked": 0, "identical": 0, "exempt": []}
 # bf16 multi-token sequences that diverged from the reference after an identical first token
 SEQ = {"checked": 0, "diverged": []}
+# logits rel-err of the reference comparisons at the benchmarked shapes (label -> rel), printed
+# in the terminal summary
+RELS = {}
 
 
 def rel(a, b) -> float:
