@@ -247,6 +247,10 @@ def test_w7b_full_depth_matches_reference(w7b_gold):
         check_bf16(r.first_token_logits, w7b_gold["full0_last"], f"w7b full depth {variant}")
         m.set_option("zero_copy", 1)
         m.set_option("chain_group", 9)
+    # request 0 inside a 4-request micro-batch (configs[3]'s path at full depth: CTA-pair GEMMs
+    # at M = 256, the persistent batched attention reading the modules in place)
+    res = pcb.serve_batch(store, schema, pc.W7B_PROMPTS, micro_batch=4)
+    check_bf16(res[0].first_token_logits, w7b_gold["full0_last"], "w7b full depth micro-batch req0")
 
 
 def test_w7b_prefill_matches_reference(w7b, w7b_gold):
