@@ -163,10 +163,17 @@ __global__ void k_embed(const int32_t* tok, const int32_t* pos, const float* tab
   pdl_wait();
   int64_t i = blockIdx.x;
   const float* e = table + static_cast<int64_t>(tok[i]) * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float v = e[j];
-    if (abs_table) v = __fadd_rn(v, abs_table[static_cast<int64_t>(pos[i]) * d + j]);
-    h[i * d + j] = v;
+  if (!abs_table && (d & 3) == 0) {  // 16-byte copies of the embedding row
+    const float4* e4 = reinterpret_cast<const float4*>(e);
+    float4* h4 = reinterpret_cast<float4*>(h + i * d);
+#pragma unroll 4
+    for (int j = threadIdx.x; j < (d >> 2); j += blockDim.x) h4[j] = e4[j];
+  } else {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      float v = e[j];
+      if (abs_table) v = __fadd_rn(v, abs_table[static_cast<int64_t>(pos[i]) * d + j]);
+      h[i * d + j] = v;
+    }
   }
   if (rope_tab) {
     const int64_t p = static_cast<int64_t>(pos[i]) * half;
@@ -320,12 +327,26 @@ __global__ void k_argmax(const float* logits, int V, int32_t* out) {
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    float v = row[i];
+  auto take = [&](float v, int i) {
     if (v > best || (v == best && i < bi)) {
       best = v;
       bi = i;
     }
+  };
+  if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    // 16-byte loads, all of a thread's loads in flight before the compares
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int n4 = V >> 2;
+#pragma unroll 8
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+      const float4 v = r4[i];
+      take(v.x, 4 * i);
+      take(v.y, 4 * i + 1);
+      take(v.z, 4 * i + 2);
+      take(v.w, 4 * i + 3);
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) take(row[i], i);
   }
   for (int o = 16; o; o >>= 1) {
     float ov = __shfl_xor_sync(0xffffffffu, best, o);
