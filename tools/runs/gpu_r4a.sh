@@ -1,0 +1,8 @@
+#!/bin/bash
+# round-2 final evidence: smoke, -m gpu, bench + reference arm + launch list + ncu captures, chain timeline
+OUT=gpurun_out/r4a
+mkdir -p $OUT
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo rc=$? >> $OUT/smoke.log
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/pytest.log 2>&1; echo rc=$? >> $OUT/pytest.log
+bash tools/profile_round.sh r4a
+AB_VARIANTS=zero-copy timeout 300 python tools/chain_ab.py 2 > $OUT/chain_tl.txt 2>&1
