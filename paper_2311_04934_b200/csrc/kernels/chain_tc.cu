@@ -1088,7 +1088,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           // 8 16-byte stores per thread instead of 64 scattered 2-byte ones
           const bool tstore = P.S == 1 && (e.kind == EPI_QKV || e.kind == EPI_GELU) && Mc <= 64 && !P.stats_out;
           __nv_bfloat16* T = reinterpret_cast<__nv_bfloat16*>(colsum);  // [64 tokens][128 rows]
-          if (tstore && (e.kind == EPI_GELU || !e.rope || rope_stage)) {
+          // the lean path stages <= 64 tokens at a time in T: 65-128 tokens (configs[2]'s 128-token
+          // suffix) take two rounds
+          const bool tlean = P.S == 1 && (e.kind == EPI_QKV || e.kind == EPI_GELU) && Mc <= 128 && !P.stats_out &&
+                             (e.kind == EPI_GELU || !e.rope || rope_stage);
+          if (tlean) {
             // Lean path: every per-row choice (GELU / RoPE / LN fold, the RoPE sign of an odd
             // column) is made once, outside the element loops, so the 16-token chunk is
             // straight-line code.  One epilogue warp per scheduler has no latency hiding: the
@@ -1127,7 +1131,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                 if (et == 0) ctl(p, ph, 4);
               }
 #pragma unroll 1
-              for (int cc = 0; cc < Mc; cc += 16) {
+              for (int h0 = 0; h0 < Mc; h0 += 64) {  // rounds of <= 64 tokens through T
+                const int hn = Mc - h0 < 64 ? Mc - h0 : 64;
+#pragma unroll 1
+              for (int cc = h0; cc < h0 + hn; cc += 16) {
                 uint32_t ra[16], rc[16], rs[16];
                 tmem_ld16_nowait(acc + cc, ra);
                 if (rot) {
@@ -1157,24 +1164,26 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                   }
                 }
 #pragma unroll
-                for (int j = 0; j < 16; ++j) T[(cc + j) * 128 + row] = __float2bfloat16_rn(x[j]);
+                for (int j = 0; j < 16; ++j) T[(cc - h0 + j) * 128 + row] = __float2bfloat16_rn(x[j]);
                 if (et == 0 && !dry && cc < 32) ctl(p, ph, 13 + 2 * (cc >> 4));
               }
-              if (!dry) {
+              if (!dry && h0 + hn >= Mc) {  // the accumulator is fully read
                 tc_fence_before();
                 mbar_arrive(&acc_empty[buf]);
                 if (et == 0) ctl(p, ph, 9);
               }
               named_bar(1, 128);
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {  // Mc * 16 <= 1024 16-byte pieces, 128 threads
+              for (int u = 0; u < 8; ++u) {  // hn * 16 <= 1024 16-byte pieces, 128 threads
                 const int i = et + u * 128;
-                if (i < Mc * 16) {
+                if (i < hn * 16) {
                   const int m = i >> 4, q16 = i & 15;
                   const uint4 val = *reinterpret_cast<const uint4*>(T + m * 128 + q16 * 8);
-                  __nv_bfloat16* dst = off ? base + off[m] + q16 * 8 : base + m * ld + q16 * 8;
+                  __nv_bfloat16* dst = off ? base + off[h0 + m] + q16 * 8 : base + (h0 + m) * ld + q16 * 8;
                   if (!dry) *reinterpret_cast<uint4*>(dst) = val;
                 }
+              }
+              if (h0 + hn < Mc) named_bar(1, 128);  // T is reused by the next round
               }
               if (et == 0 && !dry) ctl(p, ph, 10);
               named_bar(1, 128);  // T is reused by this CTA's next item

@@ -44,8 +44,9 @@ if os.environ.get("AB_VARIANTS"):
 
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 layers = int(os.environ.get("PROF_LAYERS", "32"))
-cfg = dict(bench.CFG_7B, n_layers=layers)
-schema_text, prompts = bench.workload(4096, 64, 1)
+cfg = dict(bench.CFG_7B, n_layers=layers, max_position=32768)
+schema_text, prompts = bench.workload(int(os.environ.get("AB_CACHED", "4096")), int(os.environ.get("AB_UNC", "64")),
+                                     int(os.environ.get("AB_MODS", "1")))  # configs[2]: 16384 128 3
 m = pcb.Model(cfg, dtype=pcb.BF16)
 s = pcb.Schema.parse(schema_text)
 st = pcb.ModuleStore(m)

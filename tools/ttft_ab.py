@@ -19,7 +19,8 @@ import paper_2311_04934_b200 as pcb  # noqa: E402
 label = sys.argv[1] if len(sys.argv) > 1 else "run"
 n_req = int(os.environ.get("AB_N", "40"))
 layers = int(os.environ.get("AB_LAYERS", "32"))
-schema_text, prompts = bench.workload(4096, 64, 1)
+schema_text, prompts = bench.workload(int(os.environ.get("AB_CACHED", "4096")), int(os.environ.get("AB_UNC", "64")),
+                                     int(os.environ.get("AB_MODS", "1")))  # configs[2]: 16384 128 3
 m = pcb.Model(dict(bench.CFG_7B, n_layers=layers), dtype=pcb.BF16)
 s = pcb.Schema.parse(schema_text)
 st = pcb.ModuleStore(m)
