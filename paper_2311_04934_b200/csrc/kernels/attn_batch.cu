@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_attn_batch(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, BatchParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ symbol (not an integer round trip) keeps the
+  // shared address space visible to the compiler: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + kQ;
   float* sX = reinterpret_cast<float*>(sKV + kStages * kStage);  // merge chunk [64][17]

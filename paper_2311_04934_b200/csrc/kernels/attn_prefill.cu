@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_attn_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, PrefillParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ symbol (not an integer round trip) keeps the
+  // shared address space visible to the compiler: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                 // [2 tiles][32 KB]
   uint8_t* sKV = smem + 2 * kQBytes;  // [kSlots][32 KB]: K_0, V_0, K_1, V_1, ... (across units)
   uint64_t* q_full = reinterpret_cast<uint64_t*>(sKV + kSlots * kSlotBytes);  // Q tiles of a unit landed

@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   constexpr int kRedRow = HD + 4;  // padded fp32 row of a parked partial O
   static_assert(BQ * (kRedRow + 2) * 4 <= KV_STAGES * S::kStage, "split merge buffer must fit the K/V stages");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ symbol (not an integer round trip) keeps the
+  // shared address space visible to the compiler: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + S::kQ;
   int32_t* sPos = reinterpret_cast<int32_t*>(sKV + KV_STAGES * S::kStage);  // [KV_STAGES][BKV] (ALiBi)

@@ -258,7 +258,9 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constant__ ChainParams p) {
   using S = ChainSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ symbol (not an integer round trip) keeps the
+  // shared address space visible to the compiler: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   float* pb = reinterpret_cast<float*>(smem + STAGES * S::kStage);  // cluster exchange buffer (S::kPB bytes)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage + S::kPB);
   uint64_t* empty = full + STAGES;
@@ -632,24 +634,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           const float ascale = P.ascale, thr = kRescaleThreshold / ascale;
           // key-block visibility in 32-bit arithmetic (positions < 2^31, checked on the host):
           // lim = last visible key of the block relative to this lane's first column
-          int sg = 0, seg_first = 0, seg_next = P.a_nseg ? P.a_first[1] : 0x7fffffff;
+          //     = vis - 64 b, vis re-derived only when the block enters a new segment
+          // contiguous: key j visible iff j <= P + qi; zero-copy: a prefix segment's rows are
+          // all visible (its padding is not), the tail is visible up to tail_vis + qi
+          int sg = -1, seg_next = P.a_nseg ? 0 : 0x7fffffff;
+          int vis = static_cast<int>(P.aP) + qi - c0;
           for (int it = 0; it < nb; ++it) {
-            // contiguous: key j visible iff j <= P + qi; zero-copy: a prefix segment's rows
-            // are all visible (its padding is not), the tail is visible up to tail_vis + qi
             const int b = b0 + it;
             const int g = ab + it;  // block sequence over the launch's attention phases
-            int lim;
-            if (P.a_nseg) {
-              while (b >= seg_next) {
-                ++sg;
-                seg_first = seg_next;
-                seg_next = P.a_first[sg + 1];
-              }
-              const int local = (b - seg_first) * 64;
-              lim = (sg == P.a_nseg - 1 ? P.a_tail_vis + qi : P.a_rows[sg] - 1) - local - c0;
-            } else {
-              lim = static_cast<int>(P.aP) + qi - b * 64 - c0;
+            if (b >= seg_next) {
+              do ++sg;
+              while (b >= P.a_first[sg + 1]);
+              const int seg_first = P.a_first[sg];
+              seg_next = P.a_first[sg + 1];
+              vis = (sg == P.a_nseg - 1 ? P.a_tail_vis + qi : P.a_rows[sg] - 1) + seg_first * 64 - c0;
             }
+            const int lim = vis - b * 64;
             if (!live) {
               // S(it) was issued after p_full(it - 2) completed: arriving after it keeps this
               // warp's arrival out of block it - 3's phase of the same barrier
@@ -787,6 +787,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           ab += nb;
         }
         if (early) mbar_arrive(a_done);
+        long long tpk0 = 0, tld = 0;
         if (nb > 0) {
           constexpr int kXld = 132;  // padded fp32 row (= S::kPbLd: a lane reads its dup partner's
                                      // row, then parks its own result over it, in order)
@@ -797,14 +798,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           if (dup) {
             if (row >= 64) {
 #pragma unroll 1
-              for (int x = 0; x < 128; x += 16) {
-                float ov[16];
-                tmem_ld16(aO + lane_off + x, ov);
+              for (int x = 0; x < 128; x += 32) {
+                uint32_t ov[32];
+                tmem_ld16_nowait(aO + lane_off + x, ov);
+                tmem_ld16_nowait(aO + lane_off + x + 16, ov + 16);
+                tmem_wait_ld();
                 if (qi < n_)
 #pragma unroll
-                  for (int y = 0; y < 16; y += 4)
+                  for (int y = 0; y < 32; y += 4)
                     *reinterpret_cast<float4*>(xo + qi * kXld + x + y) =
-                        make_float4(ov[y], ov[y + 1], ov[y + 2], ov[y + 3]);
+                        make_float4(__uint_as_float(ov[y]), __uint_as_float(ov[y + 1]), __uint_as_float(ov[y + 2]),
+                                    __uint_as_float(ov[y + 3]));
               }
               if (qi < n_) xml[qi] = make_float2(m, l);
             }
@@ -818,42 +822,65 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               m = M;
             }
           }
+          if (et == 32) ctl(p, ph, 9);  // a result lane (warp quadrant 0): dup halves combined
+          tpk0 = p.tl ? clock64() : 0;
           if (out_lane) {
             const float inv = nparts == 1 ? 1.f / l : 1.f;
             __nv_bfloat16* dst = P.aout + qi * P.a_d + h * 128;
+            // two 16-column TMEM loads in flight per wait
 #pragma unroll 1
-            for (int x = 0; x < 128; x += 16) {
-              float ov[16];
-              tmem_ld16(aO + lane_off + x, ov);
-              if (qi >= n_) continue;
-              if (dup) {
+            for (int x2 = 0; x2 < 128; x2 += 32) {
+              float ov2[32];
+              {
+                uint32_t raw[32];
+                if (p.tl && x2 == 32) tld = clock64() - tpk0;  // first iteration (cold code)
+                tmem_ld16_nowait(aO + lane_off + x2, raw);
+                tmem_ld16_nowait(aO + lane_off + x2 + 16, raw + 16);
+                tmem_wait_ld();
 #pragma unroll
-                for (int y = 0; y < 16; ++y) ov[y] = w0 * ov[y] + w1 * xo[qi * kXld + x + y];
+                for (int y = 0; y < 32; ++y) ov2[y] = __uint_as_float(raw[y]);
               }
-              if (nparts == 1) {
-                uint4 w2[2];
-                __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w2);
+              if (qi >= n_) continue;
 #pragma unroll
-                for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
-                *reinterpret_cast<uint4*>(dst + x) = w2[0];
-                *reinterpret_cast<uint4*>(dst + x + 8) = w2[1];
-              } else if (adsm) {  // park O / l (fp32) in this CTA's exchange buffer
-                const float il = l > 0.f ? 1.f / l : 0.f;
-                float* pr = pb + qi * S::kPbLd + x;
+              for (int hx = 0; hx < 2; ++hx) {
+                const int x = x2 + 16 * hx;
+                float* ov = ov2 + 16 * hx;
+                if (dup) {
 #pragma unroll
-                for (int y = 0; y < 16; y += 4)
-                  *reinterpret_cast<float4*>(pr + y) = make_float4(ov[y] * il, ov[y + 1] * il, ov[y + 2] * il, ov[y + 3] * il);
-              } else {  // park the normalised O row in fp16 (O / l: |values| <= max |V|) for the merge
-                const float il = l > 0.f ? 1.f / l : 0.f;
-                uint32_t hw[8];
-#pragma unroll
-                for (int y = 0; y < 8; ++y) {
-                  const __half2 t = __floats2half2_rn(ov[2 * y] * il, ov[2 * y + 1] * il);
-                  hw[y] = *reinterpret_cast<const uint32_t*>(&t);
+                  for (int y = 0; y < 16; y += 4) {
+                    const float4 o4 = *reinterpret_cast<const float4*>(xo + qi * kXld + x + y);
+                    ov[y] = w0 * ov[y] + w1 * o4.x;
+                    ov[y + 1] = w0 * ov[y + 1] + w1 * o4.y;
+                    ov[y + 2] = w0 * ov[y + 2] + w1 * o4.z;
+                    ov[y + 3] = w0 * ov[y + 3] + w1 * o4.w;
+                  }
                 }
-                __half* ph = reinterpret_cast<__half*>(part) + x;  // row stride stays 128 floats
-                __stcg(reinterpret_cast<uint4*>(ph), make_uint4(hw[0], hw[1], hw[2], hw[3]));
-                __stcg(reinterpret_cast<uint4*>(ph + 8), make_uint4(hw[4], hw[5], hw[6], hw[7]));
+                if (nparts == 1) {
+                  uint4 w2[2];
+                  __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(w2);
+#pragma unroll
+                  for (int y = 0; y < 8; ++y) b[y] = __floats2bfloat162_rn(ov[2 * y] * inv, ov[2 * y + 1] * inv);
+                  *reinterpret_cast<uint4*>(dst + x) = w2[0];
+                  *reinterpret_cast<uint4*>(dst + x + 8) = w2[1];
+                } else if (adsm) {  // park O / l (fp32) in this CTA's exchange buffer
+                  const float il = l > 0.f ? 1.f / l : 0.f;
+                  float* pr = pb + qi * S::kPbLd + x;
+#pragma unroll
+                  for (int y = 0; y < 16; y += 4)
+                    *reinterpret_cast<float4*>(pr + y) =
+                        make_float4(ov[y] * il, ov[y + 1] * il, ov[y + 2] * il, ov[y + 3] * il);
+                } else {  // park the normalised O row in fp16 (O / l: |values| <= max |V|) for the merge
+                  const float il = l > 0.f ? 1.f / l : 0.f;
+                  uint32_t hw[8];
+#pragma unroll
+                  for (int y = 0; y < 8; ++y) {
+                    const __half2 t = __floats2half2_rn(ov[2 * y] * il, ov[2 * y + 1] * il);
+                    hw[y] = *reinterpret_cast<const uint32_t*>(&t);
+                  }
+                  __half* ph = reinterpret_cast<__half*>(part) + x;  // row stride stays 128 floats
+                  __stcg(reinterpret_cast<uint4*>(ph), make_uint4(hw[0], hw[1], hw[2], hw[3]));
+                  __stcg(reinterpret_cast<uint4*>(ph + 8), make_uint4(hw[4], hw[5], hw[6], hw[7]));
+                }
               }
             }
             if (nparts > 1 && qi < n_) {
@@ -861,6 +888,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               else __stcg(ml + static_cast<int64_t>(c) * 128 + qi, make_float2(m, l));
             }
           }
+        }
+        if (et == 32) {
+          ctl(p, ph, 10);
+          ctl_val(p, ph, 6, p.tl ? clock64() - tpk0 : 0);  // cycles of the output / park loop
+          ctl_val(p, ph, 7, tld);
         }
         tc_fence_before();
         if (et == 0) ctl(p, ph, 4);
@@ -874,6 +906,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
           if (et == 0) ctl(p, ph, 8);
           pb_wait(pb_ready, pb_uses & 1);
           if (et == 0) ctl(p, ph, 5);
+          const long long tmg0 = p.tl ? clock64() : 0;
           const int x0 = (et & 7) * 4;  // dims x0 + 32 y + [0, 4): 8 threads read 128 contiguous bytes
           for (int64_t r2 = sp + static_cast<int64_t>(et >> 3) * P.aS; r2 < n_; r2 += 16 * P.aS) {
             // every remote load issued before the first use (member indices past S re-read
@@ -911,6 +944,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
               *reinterpret_cast<uint2*>(dst + 32 * y) =
                   make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
             }
+          }
+          if (et == 0) {
+            ctl(p, ph, 11);
+            (void)tmg0;
           }
           pb_signal(pb_free, base, nparts);
           ++pb_uses;

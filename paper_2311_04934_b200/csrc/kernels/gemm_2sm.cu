@@ -121,7 +121,9 @@ struct Args2 {
 __global__ void __launch_bounds__(k2Threads, 1)
     k_gemm_2sm(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, Args2 a, Epilogue e) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ symbol (not an integer round trip) keeps the
+  // shared address space visible to the compiler: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * kStage2);
   uint64_t* empty = full + k2Stages;
   uint64_t* acc_full = empty + k2Stages;  // [2]

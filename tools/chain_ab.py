@@ -153,15 +153,17 @@ for i in range(n):
 # attention-phase cycle accounting (raw clock64 counts in slots 12-15 of phase 0)
 cyc = []
 for i in range(n):
-    if int(phases[i]) == 5:
-        ev = times[i, 0, :148].astype(np.int64)
+    for ph in range(int(phases[i])):
+        if times[i, ph, 159, 15] != 3:  # attention phases only
+            continue
+        ev = times[i, ph, :128].astype(np.int64)
         ok = ev[:, 12] > 0
         if ok.any():
-            cyc.append([np.median(ev[ok, k]) for k in (12, 13, 14, 15)])
+            cyc.append([np.median(ev[ok, k]) for k in (12, 13, 14, 15, 6, 7)])
 if cyc:
     c = np.median(np.array(cyc), axis=0)
     print(f"ATTN cycles (median CTA, median chain): softmax loop {c[0]:.0f}, of which waiting for S {c[1]:.0f}; "
-          f"MMA waiting for K/V {c[2]:.0f}, for P {c[3]:.0f}")
+          f"MMA waiting for K/V {c[2]:.0f}, for P {c[3]:.0f}; output/park loop {c[4]:.0f}, split merge {c[5]:.0f}")
 print("per phase (median over chains), us")
 for key, rows in agg.items():
     keys = sorted({k for r_ in rows for k in r_})
@@ -181,12 +183,12 @@ if os.environ.get("TL_ATTN", "1") != "0":
                 continue
             ev = times[i, ph, :128].astype(np.int64)
             t0 = ev[:, 0][ev[:, 0] > 0].min()
-            rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 4, 8, 5, 2)])
+            rows.append([(ev[:, k] - t0) / 1e3 for k in (0, 1, 9, 10, 4, 8, 5, 11, 2)])
     if rows:
         a = np.array(rows)  # [chain][event][cta]
-        print("ATTN per-CTA events (median over chains of the percentile), us: start / last PV / a_done / released / flags / done")
+        print("ATTN per-CTA events (median over chains of the percentile), us: start / last PV / dup merged / parked / a_done / released / flags / merged / done")
         for q in (0, 50, 90, 100):
-            print(f"  p{q:3d}  " + "  ".join(f"{np.median(np.percentile(a[:, k, :], q, axis=1)):6.1f}" for k in range(6)))
+            print(f"  p{q:3d}  " + "  ".join(f"{np.median(np.percentile(a[:, k, :], q, axis=1)):6.1f}" for k in range(9)))
         # is the straggler split a fixed one (last split holds the diagonal block)?
         lastpv = np.median(a[:, 1, :], axis=0).reshape(-1, 4)
         print("  last PV by split (median over heads):", np.round(np.median(lastpv, axis=0), 1))

@@ -1,9 +1,9 @@
 // K/V streaming bandwidth of the chain's attention phase access pattern, without the math.
-// 128 CTAs = 32 heads x 4 key splits, each streaming its keys' K and V in 64-row blocks
-// through a ring of STAGES x 32 KB:
-//   rowmajor   K/V [rows][4096] bf16, per block two 64x64 TMA boxes of K and two of V
-//              (64 rows x 256 B of the head's slice, rows 8 KB apart) -- the store's layout
-//   headmajor  K/V [32 heads][rows][128]: a block is 16 KB contiguous per tensor, one bulk copy
+// One persistent launch streams L layers' K/V ([L * rows][4096] bf16, the store's row-major
+// layout: per 64-key block two 64x64 TMA boxes of K and two of V, 64 rows x 256 B of a head's
+// slice, rows 8 KB apart) through a ring of STAGES x 32 KB per CTA.  The (head, block) space
+// of a layer is cut into equal contiguous ranges over the grid (128 CTAs = 32 heads x 4 splits,
+// as the chain's attention phase; 148 = every SM).  No barrier between layers: an upper bound.
 // Build: nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/probe/kvstream tools/probe/kvstream.cu -lcuda
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -44,15 +44,15 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
                : "memory");
 }
 
-template <int STAGES, bool HM>
+template <int STAGES>
 __global__ void __launch_bounds__(64, 1) kstream(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
-                                                const __nv_bfloat16* K, const __nv_bfloat16* V, int rows, int splits) {
+                                                int rows, int layers) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * 32768);
   uint64_t* empty = full + STAGES;
-  const int h = blockIdx.x / splits, sp = blockIdx.x % splits;
-  const int nblk = (rows + 63) / 64;
-  const int b0 = nblk * sp / splits, nb = nblk * (sp + 1) / splits - b0;
+  const int nblk = (rows + 63) / 64, T = 32 * nblk, C = gridDim.x;
+  const int u0 = static_cast<int>(static_cast<long long>(T) * blockIdx.x / C);
+  const int u1 = static_cast<int>(static_cast<long long>(T) * (blockIdx.x + 1) / C);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       bar_init(&full[s], 1);
@@ -61,22 +61,18 @@ __global__ void __launch_bounds__(64, 1) kstream(const __grid_constant__ CUtenso
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const int nb = (u1 - u0) * layers;
   if (threadIdx.x == 0) {
     for (int it = 0; it < nb; ++it) {
       const int s = it % STAGES;
       wait(&empty[s], ((it / STAGES) & 1) ^ 1);
       expect_tx(&full[s], 32768);
       uint8_t* st = sm + s * 32768;
-      const int b = b0 + it;
-      if (HM) {
-        const size_t off = (static_cast<size_t>(h) * rows + static_cast<size_t>(b) * 64) * 128;
-        bulk(st, K + off, 16384, &full[s]);
-        bulk(st + 16384, V + off, 16384, &full[s]);
-      } else {
-        for (int a = 0; a < 2; ++a) {
-          tma2d(st + a * 8192, &tk, &full[s], h * 128 + a * 64, b * 64);
-          tma2d(st + 16384 + a * 8192, &tv, &full[s], h * 128 + a * 64, b * 64);
-        }
+      const int l = it / (u1 - u0), u = u0 + it % (u1 - u0);
+      const int h = u / nblk, b = u % nblk;
+      for (int a = 0; a < 2; ++a) {
+        tma2d(st + a * 8192, &tk, &full[s], h * 128 + a * 64, l * rows + b * 64);
+        tma2d(st + 16384 + a * 8192, &tv, &full[s], h * 128 + a * 64, l * rows + b * 64);
       }
     }
   } else if (threadIdx.x == 32) {
@@ -92,71 +88,53 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <int ST, bool HM>
-float run(const std::vector<CUtensorMap>& tk, const std::vector<CUtensorMap>& tv, const std::vector<const __nv_bfloat16*>& K,
-          const std::vector<const __nv_bfloat16*>& V, int rows, int splits) {
+template <int ST>
+float run(const CUtensorMap& tk, const CUtensorMap& tv, int rows, int layers, int ctas) {
   const int smem = ST * 32768 + 1024;
-  cudaFuncSetAttribute(kstream<ST, HM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(kstream<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int L = static_cast<int>(K.size());
-  for (int l = 0; l < L; ++l) kstream<ST, HM><<<32 * splits, 64, smem>>>(tk[l], tv[l], K[l], V[l], rows, splits);
+  kstream<ST><<<ctas, 64, smem>>>(tk, tv, rows, layers);
   cudaEventRecord(e0);
-  const int reps = 4;
-  for (int r = 0; r < reps; ++r)  // a different layer every launch: the working set (12 x 68 MB) exceeds L2
-    for (int l = 0; l < L; ++l) kstream<ST, HM><<<32 * splits, 64, smem>>>(tk[l], tv[l], K[l], V[l], rows, splits);
+  kstream<ST><<<ctas, 64, smem>>>(tk, tv, rows, layers);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  return ms * 1000.f / (reps * L);
+  return ms * 1000.f / layers;
 }
 
 int main() {
-  const int rows = 4160, d = 4096;
-  // 12 K/V layer pairs (> L2) cycled so every launch reads from HBM
-  const int L = 12;
-  const size_t n = static_cast<size_t>(rows) * d;
-  __nv_bfloat16* buf;
-  cudaMalloc(&buf, 2 * L * n * sizeof(__nv_bfloat16));
-  cudaMemset(buf, 0, 2 * L * n * sizeof(__nv_bfloat16));
+  const int d = 4096;
   EncodeFn enc = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
-  auto mk = [&](const void* p) {
-    CUtensorMap m;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
-    cuuint32_t box[2] = {64, 64}, es[2] = {1, 1};
-    enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
-        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return m;
-  };
-  const double bytes = 2.0 * n * 2;
-  std::vector<CUtensorMap> tk, tv;
-  std::vector<const __nv_bfloat16*> Ks, Vs;
-  for (int l = 0; l < L; ++l) {
-    Ks.push_back(buf + 2 * l * n);
-    Vs.push_back(buf + 2 * l * n + n);
-    tk.push_back(mk(Ks.back()));
-    tv.push_back(mk(Vs.back()));
-  }
-  for (int splits : {4, 8}) {
-    for (int layout = 0; layout < 2; ++layout) {
-      for (int st : {3, 4, 6}) {
-        float us;
-        if (layout == 0)
-          us = st == 3 ? run<3, false>(tk, tv, Ks, Vs, rows, splits)
-                       : st == 4 ? run<4, false>(tk, tv, Ks, Vs, rows, splits) : run<6, false>(tk, tv, Ks, Vs, rows, splits);
-        else
-          us = st == 3 ? run<3, true>(tk, tv, Ks, Vs, rows, splits)
-                       : st == 4 ? run<4, true>(tk, tv, Ks, Vs, rows, splits) : run<6, true>(tk, tv, Ks, Vs, rows, splits);
-        printf("splits %d %-9s stages %d: %7.1f us  %6.0f GB/s\n", splits, layout ? "headmajor" : "rowmajor", st, us,
-               bytes / us / 1e3);
+  for (int rows : {4160, 16512}) {
+    const int layers = rows == 4160 ? 32 : 8;  // 2.2 GB of K/V per launch (> L2)
+    const size_t n = static_cast<size_t>(rows) * layers * d;
+    __nv_bfloat16* buf;
+    cudaMalloc(&buf, 2 * n * sizeof(__nv_bfloat16));
+    cudaMemset(buf, 0, 2 * n * sizeof(__nv_bfloat16));
+    auto mk = [&](const void* p) {
+      CUtensorMap m;
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows) * layers};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
+      cuuint32_t box[2] = {64, 64}, es[2] = {1, 1};
+      enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      return m;
+    };
+    const CUtensorMap tk = mk(buf), tv = mk(buf + n);
+    const double bytes = 2.0 * rows * d * 2;  // per layer
+    for (int ctas : {128, 132, 148})
+      for (int st : {4, 5, 6}) {
+        const float us = st == 4 ? run<4>(tk, tv, rows, layers, ctas)
+                                 : st == 5 ? run<5>(tk, tv, rows, layers, ctas) : run<6>(tk, tv, rows, layers, ctas);
+        printf("rows %5d ctas %3d stages %d: %7.2f us/layer  %6.0f GB/s\n", rows, ctas, st, us, bytes / us / 1e3);
       }
-    }
+    cudaFree(buf);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
