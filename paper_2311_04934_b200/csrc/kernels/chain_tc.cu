@@ -198,8 +198,10 @@ __device__ __forceinline__ void grid_wait(const ChainParams& p, int ph) {
   for (uint32_t spins = 0; ld_relaxed_u64(p.gbar) < target;) {
     __nanosleep(32);
     if (++spins == (1u << 24)) {
+#ifdef PCB_TIMEOUT_PRINTF
       printf("[pcb] chain grid barrier timeout: block %d thread %d phase %d/%d counter %llu target %llu\n", blockIdx.x,
              threadIdx.x, ph, p.n_phases, ld_acquire_u64(p.gbar), target);
+#endif
       __trap();
     }
   }

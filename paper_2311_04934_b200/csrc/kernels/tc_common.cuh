@@ -30,12 +30,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Watchdog: a wait that has not completed after ~2^26 suspended try_wait rounds
-// (seconds) reports where it is stuck and traps, so a pipeline bug surfaces as a
-// CUDA error instead of a hung device.
-static __device__ __noinline__ void wait_timeout(const char* what, const void* addr, uint32_t parity) {
+// Watchdog: a wait that has not completed after ~2^26 suspended try_wait rounds (seconds)
+// traps, so a pipeline bug surfaces as a CUDA error instead of a hung device.  Inlined,
+// not a call: a call anywhere in a kernel makes ptxas ignore setmaxnreg's per-role register
+// budgets (k_chain's epilogue fell from 256 to the producers' 88 registers), and without the
+// printf the trap path stays a few instructions per wait site (instruction-cache footprint).
+// Build with -DPCB_TIMEOUT_PRINTF for a message naming the barrier.
+static __device__ __forceinline__ void wait_timeout(const char* what, const void* addr, uint32_t parity) {
+#ifdef PCB_TIMEOUT_PRINTF
   printf("[pcb] %s timeout: block (%d,%d,%d) thread %d addr %p parity %u\n", what, blockIdx.x, blockIdx.y, blockIdx.z,
          threadIdx.x, addr, parity);
+#else
+  (void)what;
+  (void)addr;
+  (void)parity;
+#endif
   __trap();
 }
 
