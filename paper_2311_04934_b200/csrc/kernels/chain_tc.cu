@@ -275,6 +275,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x, c = blockIdx.x;
+  // launch probes (slot of phase kMaxPhases - 1): 0 entry, 1 prologue done, 2 epilogue past
+  // the PDL wait, 3 exit
+  if (threadIdx.x == 0) ctl(p, kMaxPhases - 1, 0);
   // attention phase (first phase only): the ring's shared memory is re-carved as Q, P and
   // K/V stages; its barriers sit 512 bytes into the barrier block; S and O live in TMEM
   // columns [256, 512), clear of the GEMM accumulators
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   __syncthreads();
   if (dsm) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   tc_fence_after();
+  if (threadIdx.x == 0) ctl(p, kMaxPhases - 1, 1);
   const uint32_t tmem = *tmem_slot;
   // attention: three 64-column score buffers at [192, 384), O at [384, 512) (the GEMM
   // accumulators [0, 2 BN) are only written by MMAs issued after the last PV)
@@ -600,6 +604,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
       const PhaseDev& P = p.ph[ph];
       if (ph == 0) {
         pdl_wait();
+        if (et == 0) ctl(p, kMaxPhases - 1, 2);
       } else {
         if (et == 0) grid_wait(p, ph);
         named_bar(1, 128);
@@ -1466,6 +1471,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   __syncthreads();
   if (dsm) cluster_sync_all();  // no CTA leaves while a peer may still read its buffer
   if (warp == 1) tmem_dealloc(tmem, tcols);
+  if (threadIdx.x == 0) ctl(p, kMaxPhases - 1, 3);
 }
 
 std::atomic<int> g_chain_epoch{0};
@@ -1475,6 +1481,17 @@ constexpr int kProbeMax = 64;
 unsigned long long* g_ctl = nullptr;
 int g_ctl_n = 0;
 int g_ctl_ph[kProbeMax];
+// the probe buffer is made resident on the device before kernels write it: a first GPU touch
+// of a host-resident managed page faults (tens of us inside the timed chain per 64 KB page)
+void probe_to_device() {
+  int dev = 0;
+  PCB_CUDA(cudaGetDevice(&dev));
+  cudaMemLocation loc{};
+  loc.type = cudaMemLocationTypeDevice;
+  loc.id = dev;
+  PCB_CUDA(cudaMemPrefetchAsync(g_ctl, sizeof(unsigned long long) * kMaxPhases * 160 * 16 * kProbeMax, loc, 0, 0));
+  PCB_CUDA(cudaDeviceSynchronize());
+}
 unsigned long long* chain_probe_slot(int n_phases) {
   static const bool on = std::getenv("PCB_CHAIN_PROBE") != nullptr;
   if (!on || g_ctl_n >= kProbeMax) return nullptr;
@@ -1482,6 +1499,7 @@ unsigned long long* chain_probe_slot(int n_phases) {
   if (!g_ctl) {
     PCB_CUDA(cudaMallocManaged(&g_ctl, sizeof(unsigned long long) * per * kProbeMax));
     std::memset(g_ctl, 0, sizeof(unsigned long long) * per * kProbeMax);
+    probe_to_device();
   }
   g_ctl_ph[g_ctl_n] = n_phases;
   return g_ctl + per * g_ctl_n++;
@@ -1728,7 +1746,10 @@ int chain_probe_dump(unsigned long long* times, int max_launches, int* phases) {
   const size_t per = static_cast<size_t>(kMaxPhases) * 160 * 16;
   if (n > 0) std::memcpy(times, g_ctl, sizeof(unsigned long long) * per * n);
   for (int i = 0; i < n; ++i) phases[i] = g_ctl_ph[i];
-  if (g_ctl) std::memset(g_ctl, 0, sizeof(unsigned long long) * per * kProbeMax);
+  if (g_ctl) {
+    std::memset(g_ctl, 0, sizeof(unsigned long long) * per * kProbeMax);
+    probe_to_device();
+  }
   g_ctl_n = 0;
   return n;
 }

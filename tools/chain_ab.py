@@ -164,6 +164,25 @@ if cyc:
     c = np.median(np.array(cyc), axis=0)
     print(f"ATTN cycles (median CTA, median chain): softmax loop {c[0]:.0f}, of which waiting for S {c[1]:.0f}; "
           f"MMA waiting for K/V {c[2]:.0f}, for P {c[3]:.0f}; output/park loop {c[4]:.0f}, split merge {c[5]:.0f}")
+# launch boundaries (probe slot of phase KMAX - 1): previous chain's last exit -> this chain's
+# first CTA entry -> prologue done -> past the PDL wait -> first phase-0 event
+gaps = []
+for i in range(1, n):
+    e_prev = times[i - 1, KMAX - 1, :160, 3].astype(np.int64)
+    e = times[i, KMAX - 1, :160].astype(np.int64)
+    ok = e[:, 0] > 0
+    if not ok.any() or not (e_prev > 0).any():
+        continue
+    t_exit = e_prev[e_prev > 0].max()
+    ph0 = times[i, 0, :160, 0].astype(np.int64)
+    ph0 = ph0[ph0 > 0]
+    gaps.append([(e[ok, 0].min() - t_exit) / 1e3, (e[ok, 0].max() - t_exit) / 1e3, (e[ok, 1].max() - t_exit) / 1e3,
+                 (e[ok, 2][e[ok, 2] > 0].max() - t_exit) / 1e3 if (e[ok, 2] > 0).any() else float("nan"),
+                 (ph0.min() - t_exit) / 1e3 if len(ph0) else float("nan")])
+if gaps:
+    g = np.median(np.array(gaps), axis=0)
+    print(f"launch boundary (median of {len(gaps)}), us after the previous chain's last exit: first entry {g[0]:.1f}, "
+          f"last entry {g[1]:.1f}, prologue done {g[2]:.1f}, past PDL wait {g[3]:.1f}, first phase-0 event {g[4]:.1f}")
 print("per phase (median over chains), us")
 for key, rows in agg.items():
     keys = sorted({k for r_ in rows for k in r_})
