@@ -13,8 +13,9 @@ import bench  # noqa: E402
 import paper_2311_04934_b200 as pcb  # noqa: E402
 
 layers = int(os.environ.get("PROF_LAYERS", "32"))
-cfg = dict(bench.CFG_7B, n_layers=layers)
-schema_text, prompts = bench.workload(4096, 64, 1)
+cfg = dict(bench.CFG_7B, n_layers=layers)  # max_position 32768
+schema_text, prompts = bench.workload(int(os.environ.get("PROF_CACHED", "4096")), int(os.environ.get("PROF_UNC", "64")),
+                                     int(os.environ.get("PROF_MODS", "1")))  # configs[2]: 16384 128 3
 m = pcb.Model(cfg, dtype=pcb.BF16)
 m.set_option("zero_copy", int(os.environ.get("PROF_ZC", "1")))  # 0: requests assemble (copy) their cache
 s = pcb.Schema.parse(schema_text)
