@@ -324,6 +324,15 @@ def _worker(args):
     return _ref_sample(n_s, P, reps)
 
 
+def request_config(config: str, n_cached: int, n_unc: int, n_mod: int, world: int) -> dict:
+    """The bench line's ``config`` for the single-request workloads; both arms print the same object."""
+    return {"workload": f"configs[{1 if config == 'c2' else 2}]: Llama-2-7B shape, {n_cached} cached "
+                        f"tokens ({n_mod} module{'s' if n_mod > 1 else ''}) + {n_unc} uncached, one request "
+                        "per step per GPU, modules in HBM",
+            "cached_tokens": n_cached, "uncached_tokens": n_unc, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (12.9 GB weights + 2.1 GB KV per step)"}
+
+
 def run_reference(a) -> None:
     """--impl reference: the reference's own CPU path on this host, all usable cores (one process each,
     the reference is single-threaded), W warm-up + K timed steps; a step = every worker timing one
@@ -367,8 +376,8 @@ def run_reference(a) -> None:
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": statistics.mean(per_step) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference synthetic_text generator; seeded PCG weights; synthetic past rows)",
-        "config": {"workload": "configs[1]: Llama-2-7B shape, 4096 cached module tokens + 64 uncached, "
-                               "single request per worker", "cached_tokens": n_cached, "uncached_tokens": n_unc},
+        # the same config object as our arm's line (the sample each worker times is in cpu_baseline)
+        "config": request_config("c2", n_cached, n_unc, 1, int(os.environ.get("WORLD_SIZE", "1"))),
         "ttft_ms": t_req * 1e3,
         "cpu_baseline": {"value": value, "unit": "requests/s", "cores": workers, "kind": "reference",
                          "sample": f"{workers} processes x [1-layer 7B model: concat_kv({n_cached} rows) + "
@@ -650,11 +659,7 @@ def run_ours(a) -> None:
             "warmup": a.warmup, "ms_per_step": region_ms / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference synthetic_text text; random-init weights from the reference's PCG32 streams)",
-            "config": {"workload": f"configs[{1 if a.config == 'c2' else 2}]: Llama-2-7B shape, {n_cached} cached "
-                                   f"tokens ({n_mod} module{'s' if n_mod > 1 else ''}) + {n_unc} uncached, one request "
-                                   "per step per GPU, modules in HBM",
-                       "cached_tokens": n_cached, "uncached_tokens": n_unc, "parallelism": f"dp{D.world}",
-                       "l2": "inputs larger than L2 (12.9 GB weights + 2.1 GB KV per step)"},
+            "config": request_config(a.config, n_cached, n_unc, n_mod, D.world),
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
