@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import math
 import os
 import statistics
@@ -577,7 +578,9 @@ def run_ours(a) -> None:
     # DRAM traffic of the same chain launches from the committed ncu capture (profiles/)
     traffic, traffic_src = None, None
     import glob
-    tr = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), key=os.path.getmtime)
+    # latest capture by round tag (r<round><letter>_traffic.json); file mtimes are checkout times
+    tr = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")),
+                key=lambda p: (int(re.match(r"r(\d+)", os.path.basename(p)).group(1)), os.path.basename(p)))
     if tr and a.config == "c2":
         with open(tr[-1]) as f:
             t = json.load(f)
