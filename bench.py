@@ -384,7 +384,8 @@ def run_reference(a) -> None:
                          "sample": f"{workers} processes x [1-layer 7B model: concat_kv({n_cached} rows) + "
                                    f"forward({n_s} suffix tokens)]; per-request time extrapolated to 32 layers x "
                                    f"{n_unc} tokens by MAC count + 2x32 cache copies"},
-        "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "extrapolated": "per-request time scaled from the timed sample (cpu_baseline.sample)"},
     }
     print(json.dumps(line), flush=True)
 
