@@ -496,7 +496,12 @@ def run_c5(a) -> None:
 
 
 def run_ours(a) -> None:
-    D = Dist()
+    # --share-device: every data-parallel rank on GPU 0 (a functional multi-process run on a
+    # one-GPU box: gloo for the timing plumbing; the ranks time-slice the GPU, so it is not a
+    # scaling point)
+    D = Dist(backend="gloo" if a.share_device else "nccl")
+    if a.share_device:
+        D.local = 0
     import numpy as np
 
     import paper_2311_04934_b200 as pcb
@@ -663,7 +668,8 @@ def run_ours(a) -> None:
             "warmup": a.warmup, "ms_per_step": region_ms / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference synthetic_text text; random-init weights from the reference's PCG32 streams)",
-            "config": request_config(a.config, n_cached, n_unc, n_mod, D.world),
+            "config": dict(request_config(a.config, n_cached, n_unc, n_mod, D.world),
+                           **({"ranks_share_one_gpu": True} if a.share_device else {})),
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
@@ -796,7 +802,7 @@ def main():
     ap.add_argument("--c5-layers", type=int, default=80)
     ap.add_argument("--c5-modules", type=int, default=64)
     ap.add_argument("--tp-transport", default="nccl", choices=["nccl", "peer"])
-    ap.add_argument("--share-device", action="store_true", help="c5: all ranks on GPU 0 (peer transport)")
+    ap.add_argument("--share-device", action="store_true", help="all ranks on GPU 0 (c5: peer transport; c2: data-parallel replicas, functional only)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--skip-batch", action="store_true")

@@ -125,3 +125,20 @@ def test_bench_two_ranks_data_parallel():
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["batch"]["requests"] == 512
+
+
+def test_bench_two_ranks_data_parallel_share_one_gpu():
+    """Data-parallel bench path as two processes (replicas on GPU 0, gloo plumbing): per-rank
+    request streams, every rank's model / store / micro-batches, barrier + max-over-ranks timing
+    and rank 0's single JSON line.  Functional only -- the ranks time-slice one GPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--share-device", "--steps", "3",
+                          "--warmup", "3", "--skip-cpu", "--skip-slow", "--skip-c3", "--skip-sweep",
+                          "--micro-batches", "16"],
+                         capture_output=True, text=True, timeout=1200, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["ranks_share_one_gpu"]
+    assert line["config"]["parallelism"] == "dp2" and line["batch"]["requests"] == 512
