@@ -1687,22 +1687,30 @@ void launch_chain(const ChainStep* steps, int n, float* ws, size_t ws_bytes, int
   }
   o.last = s;
   PdlClass pc(PDL_GEMM);
-  static const bool coop = std::getenv("PCB_CHAIN_COOP") != nullptr;  // A/B: cooperative launch attribute
+  // cooperative launch attribute (default on; PCB_CHAIN_COOP=0: off): the driver guarantees every
+  // CTA of the grid-barrier kernel co-resident or fails the launch, instead of a partly resident
+  // grid spinning into the watchdog (same-box A/B neutral: tools/runs/gpu_r5d.sh)
+  static const bool coop = [] {
+    const char* v = std::getenv("PCB_CHAIN_COOP");
+    return v == nullptr || v[0] != '0';
+  }();
   if (dsm) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kChainThreads);
     cfg.dynamicSmemBytes = Sm::kBytes;
     cfg.stream = s;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 4;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = (pdl_enabled() && ((pdl_mask() >> PDL_GEMM) & 1)) ? 1 : 0;
+    at[2].id = cudaLaunchAttributeCooperative;  // co-residency guaranteed by the launch (grid barrier)
+    at[2].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = coop ? 3 : 2;
     PCB_CUDA(cudaLaunchKernelEx(&cfg, k_chain<BN, STAGES>, p));
   } else if (coop) {
     cudaLaunchConfig_t cfg = {};
